@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""hgemv benchmark (BASELINE.json metric: hgemv GFLOP/s + GB/s, N=2^20, 32
+vectors, fp64; configs[1] = 2D Gaussian-kernel H^2, leaf 64, rank 32).
+
+One step = one hgemv y = H x of the whole synthetic H^2 matrix over one batch
+of b vectors (x resident in HBM). value = algorithmic GFLOP/s of the whole job
+(max-over-ranks device time). Also reported: GB/s, the roofline of the
+dominant kernel (leaf expansion + dense near-field, measured live with CUDA
+events), the end-to-end host-buffer path (H2D x, hgemv, D2H y), and the CPU
+oracle (port of the reference) timed on a bounded sample on the host cores.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config cfg2|cfg2b1|cfg1|cfg4] [--impl reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1] (the metric's config)
+    "cfg2": dict(workload="2D Gaussian-kernel H2 hgemv, N=2^20 (1024^2 grid on [0,1]^2), leaf 64, eta=1 strong, "
+                          "rank 32, 32 vectors, fp64, symmetric canonical storage",
+                 grid=(1024, 1024), kind="gaussian", ell=0.1, rank=32, b=32, leaf=64),
+    "cfg2b1": dict(workload="cfg2 structure with 1 vector (HBM-bound variant)", grid=(1024, 1024),
+                   kind="gaussian", ell=0.1, rank=32, b=1, leaf=64),
+    # BASELINE.json configs[0] structure (hgemv part)
+    "cfg1": dict(workload="2D exponential-kernel H2 hgemv N=16384 (128^2), leaf 64, rank 32, 1 vector",
+                 grid=(128, 128), kind="exponential", ell=0.2, rank=32, b=1, leaf=64),
+    # BASELINE.json configs[3] at P=1
+    "cfg4": dict(workload="3D Matern-3/2 H2 hgemv N=2^21 (128^3 grid), leaf 64, rank 32, 64 vectors",
+                 grid=(128, 128, 128), kind="matern32", ell=0.1, rank=32, b=64, leaf=64),
+}
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 37.1   # DMMA m8n8k4 f64 measured on this pool's B200 (profiles/fp64_peak.txt)
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA m8n8k4 f64 on B200 (profiles/fp64_peak.txt)"
+
+
+def grid_points(shape):
+    if len(shape) == 2:
+        nx, ny = shape
+        i = np.tile(np.arange(nx), ny)
+        j = np.repeat(np.arange(ny), nx)
+        return np.stack([i / (nx - 1), j / (ny - 1)], axis=1)
+    nx, ny, nz = shape
+    i = np.tile(np.arange(nx), ny * nz)
+    j = np.tile(np.repeat(np.arange(ny), nx), nz)
+    k = np.repeat(np.arange(nz), nx * ny)
+    return np.stack([i / (nx - 1), j / (ny - 1), k / (nz - 1)], axis=1)
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(PEAKS_FILE))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback B200_PROFILING.md"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl != "reference" else "gloo"
+        dist.init_process_group(backend=backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+def algorithmic_work(m, b, launches_stats=None):
+    """F (flops) and B (bytes) of one hgemv per SURVEY §8(d)."""
+    sizes = m.packed_sizes()   # U, E, V, F, S, D (doubles)
+    n = m.tree.n
+    B = 8.0 * (2 * (sizes[0] + sizes[2]) + 2 * (sizes[1] + sizes[3]) + sizes[4] + sizes[5] + 2 * n * b)
+    return B
+
+
+def run_b200(args, cfg, world, rank, local, dist):
+    import torch
+    import ctypes as C
+    from paper_2003_10173_b200 import H2Matrix, build_block_tree, build_cluster_tree
+    from paper_2003_10173_b200._lib import check, lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    b = args.b or cfg["b"]
+    pts = grid_points(cfg["grid"])
+    n = pts.shape[0]
+    t0 = time.perf_counter()
+    ct = build_cluster_tree(pts, cfg["leaf"])
+    bt = build_block_tree(ct, ct, 1.0)
+    t_tree = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    m = H2Matrix.kernel(bt, pts, cfg["kind"], cfg["ell"], cfg["rank"])
+    t_gen = time.perf_counter() - t0
+    rng = np.random.default_rng(42 + rank)
+    x_host = torch.from_numpy(rng.standard_normal((b, n)))      # column-major n x b == row-major b x n
+    X = x_host.to(dev)
+    Y = torch.empty_like(X)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def step():
+        check(lib.h2c_hgemv(m._h, 0, 0, n, b, X.data_ptr(), n, Y.data_ptr(), n, 1.0, 0.0, sh))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # per-launch stage timing + algorithmic work (roofline numerators)
+    maxrec = 256
+    cnt = C.c_int()
+    st = np.zeros(maxrec, np.int32)
+    ms = np.zeros(maxrec)
+    fl = np.zeros(maxrec)
+    by = np.zeros(maxrec)
+    agg = {}
+    for rep in range(max(3, min(args.steps, 10))):
+        check(lib.h2c_hgemv_stage_times(m._h, 0, 0, n, b, X.data_ptr(), n, Y.data_ptr(), n, sh, maxrec,
+                                        C.byref(cnt), st.ctypes.data_as(C.c_void_p), ms.ctypes.data_as(C.c_void_p),
+                                        fl.ctypes.data_as(C.c_void_p), by.ctypes.data_as(C.c_void_p)))
+        if rep == 0:
+            continue
+        for i in range(cnt.value):
+            a = agg.setdefault(int(st[i]), [0.0, 0.0, 0.0, 0])
+            a[0] += ms[i]
+            a[1] += fl[i]
+            a[2] += by[i]
+            a[3] += 1
+    nrep = max(3, min(args.steps, 10)) - 1
+    stages = {k: {"ms": v[0] / nrep, "gflop": v[1] / nrep / 1e9, "gbytes": v[2] / nrep / 1e9,
+                  "launches": v[3] // nrep} for k, v in agg.items()}
+    F = sum(v[1] for v in agg.values()) / nrep
+    Bbytes = algorithmic_work(m, b)
+    launches = m.launches(b)
+
+    # main timed region
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    if dist:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    t_step = elapsed / args.steps
+    value = world * F / t_step / 1e9
+    gbs = world * Bbytes / t_step / 1e9
+
+    # dominant kernel roofline: leaf expansion + dense near-field (stage 5)
+    dom = stages[5]
+    hbm, hbm_src = hbm_peak()
+    ai = dom["gflop"] / max(dom["gbytes"], 1e-30)
+    ridge = FP64_PEAK_TFLOPS * 1e3 / hbm
+    if ai >= ridge:
+        achieved = dom["gflop"] / (dom["ms"] / 1e3) / 1e3
+        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE}
+    else:
+        achieved = dom["gbytes"] / (dom["ms"] / 1e3)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": hbm_src}
+    roof.update({"kernel": "seg_gemm_kernel<64,NB,..,kModeY> (leaf expansion + dense near-field)",
+                 "share_of_step": dom["ms"] / sum(s["ms"] for s in stages.values()),
+                 "traffic": args.traffic, "algorithmic_gflop": dom["gflop"], "algorithmic_gbytes": dom["gbytes"],
+                 "ms": dom["ms"]})
+
+    # end-to-end through the public host-buffer API (pinned x in, y out)
+    xp = x_host.pin_memory()
+    yp = torch.empty_like(xp).pin_memory()
+    for _ in range(2):
+        check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yp.data_ptr()))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ke = max(2, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yp.data_ptr()))
+    torch.cuda.synchronize()
+    te = (time.perf_counter() - t0) / ke
+    if dist:
+        t = torch.tensor([te], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        te = float(t.item())
+    e2e = {"value": world * F / te / 1e9, "unit": "GFLOP/s", "ms_per_step": te * 1e3,
+           "h2d_bytes_per_step": 8 * n * b, "d2h_bytes_per_step": 8 * n * b,
+           "path": "h2c_matvec_host (pinned host x -> HBM, hgemv, HBM -> pinned host y)"}
+
+    out = {
+        "metric": "hgemv GFLOP/s (N=2^20, 32 vectors, fp64)" if args.config == "cfg2" else f"hgemv GFLOP/s ({args.config})",
+        "value": value, "unit": "GFLOP/s", "gbytes_per_s": gbs, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated kernel matrix)",
+        "config": {"workload": cfg["workload"], "n": n, "vectors": b, "rank": cfg["rank"], "leaf": cfg["leaf"],
+                   "kernel": f"{cfg['kind']} ell={cfg['ell']}", "admissible_leaves": int(len(bt.admissible_leaves)),
+                   "dense_leaves": int(len(bt.dense_leaves)),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (8.6 GB matrix, no flush needed)"},
+        "algorithmic": {"gflop_per_step": F / 1e9, "gbytes_per_step": Bbytes / 1e9},
+        "stages": {str(k): v for k, v in sorted(stages.items())},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+        "setup_s": {"trees": t_tree, "generate": t_gen},
+    }
+    return out, (m, X, Y, n, b, F, ct, bt, pts)
+
+
+def cpu_baseline_sample(args, ctx):
+    """Oracle (CPU port of the reference) on a bounded sample of the same
+    workload: the same H^2 payload, 2 of the b vectors, 1 thread."""
+    import torch
+    from oracle import pyoracle as O
+    m, X, Y, n, b, F, ct, bt, pts = ctx
+    bs = min(2, b)
+    t0 = time.perf_counter()
+    ref = O.Tree(pts, ct.leaf_size, 1.0, False)
+    rr, _ = m.ranks()
+    ora = O.H2.from_packed(ref, True, rr, None, m.download())
+    t_load = time.perf_counter() - t0
+    x = X[:bs].cpu().numpy().T
+    t0 = time.perf_counter()
+    y_ref = ora.matvec(x, threads=1)
+    t = time.perf_counter() - t0
+    y_gpu = Y[:bs].cpu().numpy().T
+    relerr = float(np.linalg.norm(y_gpu - y_ref) / np.linalg.norm(y_ref))
+    Fs = F * bs / b
+    return {"value": Fs / t / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "port",
+            "sample": f"full cfg matrix (same payload), {bs} of {b} vectors, 1 thread, {t:.1f} s",
+            "seconds": t, "load_s": t_load, "parity_rel_err_full_size": relerr}
+
+
+def run_reference(args, cfg, world, rank):
+    """--impl reference: the CPU port of the reference (oracle) on the host
+    cores, same config/metric; one step = one oracle hgemv over a bounded
+    sample of the vectors (one vector per host thread)."""
+    from oracle import pyoracle as O
+    if rank != 0:
+        return None
+    b = args.b or cfg["b"]
+    threads = max(1, os.cpu_count() or 1)
+    bs = min(b, threads)
+    pts = grid_points(cfg["grid"])
+    n = pts.shape[0]
+    t0 = time.perf_counter()
+    tree = O.Tree(pts, cfg["leaf"], 1.0, False)
+    h = O.H2.fixed_rank(tree, cfg["rank"], 42, threads)
+    setup = time.perf_counter() - t0
+    x = np.asfortranarray(np.random.default_rng(42).standard_normal((n, bs)))
+    # algorithmic flops for bs vectors (SURVEY §8d formula)
+    sizes = h.info()[2]
+    adm = tree.adm
+    dense = tree.dense
+    kr, _ = h.ranks()
+    sz = tree.end - tree.begin
+    Fcol = 2 * (2 * sizes[0] + 2 * sizes[1])
+    Fcol += 2 * float(np.sum(kr[tree.brow[adm]].astype(np.float64) * kr[tree.bcol[adm]]))
+    Fcol += 2 * float(np.sum(sz[tree.brow[dense]].astype(np.float64) * sz[tree.bcol[dense]]))
+    for _ in range(min(args.warmup, 1)):
+        h.matvec(x, threads=bs)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        h.matvec(x, threads=bs)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    v = Fcol * bs / t / 1e9
+    return {"impl": "reference", "metric": "hgemv GFLOP/s (N=2^20, 32 vectors, fp64)" if args.config == "cfg2"
+            else f"hgemv GFLOP/s ({args.config})", "value": v, "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (fixed-rank content)",
+            "config": {"workload": cfg["workload"], "n": n, "vectors": b, "rank": cfg["rank"]},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": bs, "kind": "port",
+                             "sample": f"{bs} of {b} vectors per step (one per host thread), oracle "
+                                       f"restatement of the reference (Eigen absent; SURVEY 8c)"},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": setup}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=list(CONFIGS))
+    ap.add_argument("--b", type=int, default=0, help="override the vector count")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes/launch of the dominant kernel from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        out = run_reference(args, cfg, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out, ctx = run_b200(args, cfg, world, rank, local, dist)
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline_sample(args, ctx)
+        except Exception as e:  # the baseline is reported, never fatal
+            out["cpu_baseline"] = {"value": None, "error": repr(e)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

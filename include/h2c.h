@@ -1,0 +1,119 @@
+/*
+ * h2c.h — C ABI of the B200-native H^2 hot path (hgemv + HARA).
+ *
+ * The reference (arxiv 2003.10173, /root/reference/proj) is a header-only
+ * C++20/Eigen library with no FFI of its own; its boundary for this path is
+ * the C++ API listed next to each entry point below. These functions are what
+ * a binding of that API (the C++ wrapper include/h2b200.hpp, the Python
+ * package paper_2003_10173_b200, a ctypes / cgo / JNI stub — INTEGRATION.md)
+ * calls. Plain pointers and sizes only; every function returns H2C_OK (0) or
+ * a negative status mirroring the reference's exception kinds, with the
+ * message in h2c_last_error().
+ *
+ * Orderings: "user" = the caller's point order, "internal" = cluster-tree
+ * order (reference types.hpp:19). Matrices are column-major FP64.
+ * Device pointers are CUDA device addresses on the current device.
+ */
+#ifndef H2C_H
+#define H2C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: reference exception kinds */
+#define H2C_OK 0
+#define H2C_INVALID_ARGUMENT (-1) /* std::invalid_argument  (e.g. h2_matrix.hpp:241-244) */
+#define H2C_LOGIC_ERROR (-2)      /* std::logic_error       (linear_operator.hpp:46-48) */
+#define H2C_MAX_RANK_ERROR (-3)   /* h2::max_rank_error     (construction.hpp:61-66) */
+#define H2C_RUNTIME_ERROR (-4)    /* std::runtime_error */
+#define H2C_CUDA_ERROR (-5)       /* CUDA failure (no reference counterpart) */
+#define H2C_CALLBACK_ERROR (-6)   /* user operator callback returned non-zero */
+
+typedef struct h2c_cluster_tree_s* h2c_cluster_tree;
+typedef struct h2c_block_tree_s* h2c_block_tree;
+typedef struct h2c_matrix_s* h2c_matrix;
+
+/* thread-local message of the last failing call */
+const char* h2c_last_error(void);
+/* library version string */
+const char* h2c_version(void);
+
+/* ---- cluster tree: replaces ClusterTree(const PointSet&, Index leaf)
+ *      (cluster_tree.hpp:31-47, build_cluster_tree :186-188) ------------- */
+int h2c_cluster_tree_create(const double* coords /* n x dim, col-major */, int64_t n, int dim, int64_t leaf_size,
+                            h2c_cluster_tree* out);
+void h2c_cluster_tree_destroy(h2c_cluster_tree t);
+/* n(), dim(), depth(), num_nodes(), leaves().size()  (cluster_tree.hpp:49-58) */
+int h2c_cluster_tree_info(h2c_cluster_tree t, int64_t* n, int* dim, int* depth, int* num_nodes, int* num_leaves);
+/* node(v) fields (cluster_tree.hpp:18-27); any output may be NULL */
+int h2c_cluster_tree_nodes(h2c_cluster_tree t, int64_t* begin, int64_t* end, int* level, int* parent, int* child0,
+                           int* child1, double* box_lo /* 3 per node */, double* box_hi);
+/* perm(): internal index i <-> user index perm[i] (cluster_tree.hpp:66-67) */
+int h2c_cluster_tree_perm(h2c_cluster_tree t, int64_t* perm);
+
+/* ---- block tree: replaces build_block_tree(rows, cols, eta, mode)
+ *      (block_tree.hpp:120-124; rows == cols as in every reference use) ----- */
+int h2c_block_tree_create(h2c_cluster_tree t, double eta, int weak, h2c_block_tree* out);
+void h2c_block_tree_destroy(h2c_block_tree b);
+int h2c_block_tree_info(h2c_block_tree b, int* num_nodes, int* num_admissible, int* num_dense, int* max_level);
+/* node(b) fields; tag 0 interior, 1 admissible, 2 dense (block_tree.hpp:29-39) */
+int h2c_block_tree_nodes(h2c_block_tree b, int* row, int* col, int* level, int* parent, int* tag);
+/* admissible_leaves(), dense_leaves() (block_tree.hpp:64-65) */
+int h2c_block_tree_leaves(h2c_block_tree b, int* admissible, int* dense);
+
+/* ---- H^2 matrix (device resident): replaces H2Matrix (h2_matrix.hpp:40-306)
+ *
+ * Packed payload layout (six parts U, E, V, F, S, D; V/F empty if symmetric):
+ *   U: leaf bases m_t x k_t, leaves in id order        (BasisTree::leaf_basis)
+ *   E: transfers k_v x k_parent, non-root nodes in id order (BasisTree::transfer)
+ *   V, F: the same for the column basis (non-symmetric only)
+ *   S: couplings k_row x k_col by admissible ordinal, stored blocks only
+ *   D: dense blocks m_t x m_s by dense ordinal, stored blocks only
+ * Symmetric matrices store canonical (row <= col) blocks only (h2_matrix.hpp:103).
+ * ----------------------------------------------------------------------- */
+/* H2Matrix::zero(bt, symmetric) when ranks are NULL; otherwise a zero matrix with the given ranks */
+int h2c_matrix_create(h2c_block_tree b, int symmetric, const int* row_ranks, const int* col_ranks, h2c_matrix* out);
+void h2c_matrix_destroy(h2c_matrix h);
+int h2c_matrix_info(h2c_matrix h, int64_t* n, int* symmetric, int* orthonormal);
+int h2c_matrix_set_orthonormal(h2c_matrix h, int orthonormal);
+/* sizes[6] in doubles of U, E, V, F, S, D */
+int h2c_matrix_sizes(h2c_matrix h, int64_t* sizes);
+int h2c_matrix_ranks(h2c_matrix h, int* row_ranks, int* col_ranks /* may be NULL */);
+/* host <-> device payload transfer; NULL parts are skipped */
+int h2c_matrix_upload(h2c_matrix h, const double* U, const double* E, const double* V, const double* F,
+                      const double* S, const double* D);
+int h2c_matrix_download(h2c_matrix h, double* U, double* E, double* V, double* F, double* S, double* D);
+/* symmetric kernel matrix generated on the device (benchmark inputs):
+ * kind 0 exp(-r/ell), 1 exp(-r^2/ell^2), 2 Matern-3/2; Chebyshev-interpolation bases of rank `rank` */
+int h2c_matrix_kernel(h2c_block_tree b, const double* coords /* user order, n x dim */, int kind, double ell,
+                      int rank, h2c_matrix* out);
+
+/* ---- hgemv: replaces H2Matrix::matvec / matvec_transpose (user ordering)
+ *      and matvec_internal / matvec_transpose_internal (h2_matrix.hpp:108-124)
+ *   y = alpha * op(H) x + beta * y  with x, y DEVICE pointers (n x b, col-major).
+ *   ordering: 0 user, 1 internal. stream: cudaStream_t (NULL = legacy default).
+ *   alpha = -1, beta = 1 with y preloaded by op(x) is the HARA residual
+ *   (construction.hpp:207-216). Errors as check_dims (h2_matrix.hpp:241-244). */
+int h2c_hgemv(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, int64_t ldx,
+              double* y, int64_t ldy, double alpha, double beta, void* stream);
+/* the same with HOST buffers: H2D copy, hgemv, D2H copy (the drop-in for the
+ * by-value Matrix H2Matrix::matvec(const Matrix&)) */
+int h2c_matvec_host(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, double* y);
+/* number of kernel launches one hgemv issues (gather + stage launches) */
+int h2c_hgemv_launches(h2c_matrix h, int transpose, int64_t b, int* launches);
+/* one hgemv (alpha 1, beta 0) with a CUDA event around every launch on `stream`:
+ * per launch its stage (0 gather, 1 leaf upsweep, 2 transfer upsweep, 3 coupling,
+ * 4 downsweep, 5 leaf expansion + dense near-field), duration in ms, and the
+ * algorithmic flops / bytes it must do (the roofline numerators) */
+int h2c_hgemv_stage_times(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x,
+                          int64_t ldx, double* y, int64_t ldy, void* stream, int max_records, int* count, int* stage,
+                          double* ms, double* flops, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* H2C_H */

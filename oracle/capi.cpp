@@ -1,0 +1,380 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY. extern "C" access to the CPU
+// restatement for the Python parity tests and bench.py's cpu_baseline leg.
+// The product library never links this.
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <thread>
+
+#include "test_support.hpp"
+
+using namespace h2;
+
+namespace {
+thread_local std::string g_err;
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const max_rank_error& e) {
+        g_err = e.what();
+        return -3;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return -2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -4;
+    }
+}
+Matrix wrap(const double* p, Index r, Index c) {
+    Matrix m(r, c);
+    if (r * c > 0) std::memcpy(m.data(), p, sizeof(double) * size_t(r * c));
+    return m;
+}
+void out(const Matrix& m, double* p) {
+    if (m.size()) std::memcpy(p, m.data(), sizeof(double) * size_t(m.size()));
+}
+}  // namespace
+
+struct ora_tree {
+    std::shared_ptr<const ClusterTree> ct;
+    std::shared_ptr<const BlockTree> bt;
+};
+struct ora_h2 {
+    H2Matrix h;
+};
+
+extern "C" {
+
+const char* ora_last_error() { return g_err.c_str(); }
+
+int ora_tree_create(const double* coords, int64_t n, int dim, int64_t leaf, double eta, int weak, ora_tree** o) {
+    return guard([&] {
+        auto ct = build_cluster_tree(PointSet(wrap(coords, n, dim)), leaf);
+        auto bt = build_block_tree(ct, ct, eta, weak ? Admissibility::weak : Admissibility::strong);
+        *o = new ora_tree{ct, bt};
+    });
+}
+void ora_tree_destroy(ora_tree* t) { delete t; }
+
+int ora_tree_info(ora_tree* t, int64_t* n, int* depth, int* num_nodes, int* num_blocks, int* n_adm, int* n_dense) {
+    return guard([&] {
+        *n = t->ct->n();
+        *depth = t->ct->depth();
+        *num_nodes = t->ct->num_nodes();
+        *num_blocks = t->bt->num_nodes();
+        *n_adm = int(t->bt->admissible_leaves().size());
+        *n_dense = int(t->bt->dense_leaves().size());
+    });
+}
+
+int ora_tree_arrays(ora_tree* t, int64_t* perm, int64_t* begin, int64_t* end, int* level, int* parent, int* child0,
+                    int* child1, int* brow, int* bcol, int* btag, int* adm, int* dense) {
+    return guard([&] {
+        const auto& ct = *t->ct;
+        for (Index i = 0; i < ct.n(); ++i) perm[i] = ct.perm()[size_t(i)];
+        for (int v = 0; v < ct.num_nodes(); ++v) {
+            begin[v] = ct.node(v).begin;
+            end[v] = ct.node(v).end;
+            level[v] = ct.node(v).level;
+            parent[v] = ct.node(v).parent;
+            child0[v] = ct.node(v).child[0];
+            child1[v] = ct.node(v).child[1];
+        }
+        const auto& bt = *t->bt;
+        for (int b = 0; b < bt.num_nodes(); ++b) {
+            brow[b] = bt.node(b).row;
+            bcol[b] = bt.node(b).col;
+            btag[b] = int(bt.node(b).tag);
+        }
+        for (size_t i = 0; i < bt.admissible_leaves().size(); ++i) adm[i] = bt.admissible_leaves()[i];
+        for (size_t i = 0; i < bt.dense_leaves().size(); ++i) dense[i] = bt.dense_leaves()[i];
+    });
+}
+
+// reference fixture random_h2 (test_support.hpp:38-70) from mt19937_64(seed)
+int ora_random_h2(ora_tree* t, int symmetric, int64_t kmax, uint64_t seed, ora_h2** o) {
+    return guard([&] {
+        std::mt19937_64 rng(seed);
+        *o = new ora_h2{testing::random_h2(t->bt, symmetric != 0, kmax, rng)};
+    });
+}
+// fixed-rank symmetric content for CPU-only benchmark runs (SURVEY §8d option
+// (i): cost and parity do not depend on the fill). Uniform(-1,1) values from a
+// counter-based hash so blocks fill in parallel.
+int ora_fixed_rank_h2(ora_tree* t, int64_t k, uint64_t seed, int nthreads, ora_h2** o) {
+    return guard([&] {
+        H2Matrix h = H2Matrix::zero(t->bt, true);
+        const ClusterTree& ct = *h.tree;
+        auto val = [seed](uint64_t a, uint64_t b) {
+            uint64_t z = seed ^ (a * 0x9E3779B97F4A7C15ull) ^ (b * 0xC2B2AE3D27D4EB4Full);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            return double(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+        };
+        auto fill = [&](Matrix& m, uint64_t tag) {
+            for (Index i = 0; i < m.size(); ++i) m[i] = val(tag, uint64_t(i));
+        };
+        for (int v = 0; v < ct.num_nodes(); ++v) h.row_basis.set_rank(v, std::min(ct.node(v).size(), k));
+        for (int v = 0; v < ct.num_nodes(); ++v) {
+            const auto& nd = ct.node(v);
+            if (nd.is_leaf()) {
+                h.row_basis.leaf_basis(v) = Matrix(nd.size(), h.row_basis.rank(v));
+                fill(h.row_basis.leaf_basis(v), uint64_t(v) << 2);
+            }
+            if (nd.parent >= 0) {
+                h.row_basis.transfer(v) = Matrix(h.row_basis.rank(v), h.row_basis.rank(nd.parent));
+                fill(h.row_basis.transfer(v), (uint64_t(v) << 2) | 1);
+            }
+        }
+        const auto& bt = *t->bt;
+        const int nt = std::max(1, nthreads);
+        std::vector<std::thread> th;
+        for (int w = 0; w < nt; ++w)
+            th.emplace_back([&, w] {
+                for (size_t i = size_t(w); i < bt.admissible_leaves().size(); i += size_t(nt)) {
+                    const int b = bt.admissible_leaves()[i];
+                    if (!h.stores(b)) continue;
+                    h.coupling[i] = Matrix(h.row_basis.rank(bt.node(b).row), h.row_basis.rank(bt.node(b).col));
+                    fill(h.coupling[i], (uint64_t(i) << 2) | 2);
+                }
+                for (size_t i = size_t(w); i < bt.dense_leaves().size(); i += size_t(nt)) {
+                    const int b = bt.dense_leaves()[i];
+                    if (!h.stores(b)) continue;
+                    fill(h.dense[i], (uint64_t(i) << 2) | 3);
+                }
+            });
+        for (auto& x : th) x.join();
+        h.orthonormal = false;
+        *o = new ora_h2{std::move(h)};
+    });
+}
+
+// H2Matrix::zero (h2_matrix.hpp:53-75)
+int ora_zero(ora_tree* t, int symmetric, ora_h2** o) {
+    return guard([&] { *o = new ora_h2{H2Matrix::zero(t->bt, symmetric != 0)}; });
+}
+void ora_h2_destroy(ora_h2* h) { delete h; }
+
+int ora_h2_info(ora_h2* h, int* symmetric, int* orthonormal, int64_t sizes[6]) {
+    return guard([&] {
+        const H2Matrix& m = h->h;
+        *symmetric = m.symmetric;
+        *orthonormal = m.orthonormal;
+        const ClusterTree& ct = *m.tree;
+        for (int i = 0; i < 6; ++i) sizes[i] = 0;
+        auto basis = [&](const BasisTree& b, int64_t& su, int64_t& se) {
+            for (int v : ct.leaves()) su += b.leaf_basis(v).size();
+            for (int v = 0; v < ct.num_nodes(); ++v)
+                if (ct.node(v).parent >= 0) se += b.transfer(v).size();
+        };
+        basis(m.row_basis, sizes[0], sizes[1]);
+        if (!m.symmetric) basis(m.col_basis, sizes[2], sizes[3]);
+        for (size_t i = 0; i < m.coupling.size(); ++i)
+            if (m.stores(m.blocks->admissible_leaves()[i])) sizes[4] += m.coupling[i].size();
+        for (size_t i = 0; i < m.dense.size(); ++i)
+            if (m.stores(m.blocks->dense_leaves()[i])) sizes[5] += m.dense[i].size();
+    });
+}
+
+int ora_h2_ranks(ora_h2* h, int* row, int* col) {
+    return guard([&] {
+        for (int v = 0; v < h->h.tree->num_nodes(); ++v) {
+            row[v] = int(h->h.row_basis.rank(v));
+            if (col) col[v] = int(h->h.vbasis().rank(v));
+        }
+    });
+}
+
+// packed export in the layout of include/h2c.h
+int ora_h2_export(ora_h2* h, double* U, double* E, double* V, double* F, double* S, double* D) {
+    return guard([&] {
+        const H2Matrix& m = h->h;
+        const ClusterTree& ct = *m.tree;
+        auto basis = [&](const BasisTree& b, double* pu, double* pe) {
+            for (int v : ct.leaves()) {
+                out(b.leaf_basis(v), pu);
+                pu += b.leaf_basis(v).size();
+            }
+            for (int v = 0; v < ct.num_nodes(); ++v)
+                if (ct.node(v).parent >= 0) {
+                    out(b.transfer(v), pe);
+                    pe += b.transfer(v).size();
+                }
+        };
+        basis(m.row_basis, U, E);
+        if (!m.symmetric) basis(m.col_basis, V, F);
+        for (size_t i = 0; i < m.coupling.size(); ++i)
+            if (m.stores(m.blocks->admissible_leaves()[i])) {
+                out(m.coupling[i], S);
+                S += m.coupling[i].size();
+            }
+        for (size_t i = 0; i < m.dense.size(); ++i)
+            if (m.stores(m.blocks->dense_leaves()[i])) {
+                out(m.dense[i], D);
+                D += m.dense[i].size();
+            }
+    });
+}
+
+int ora_h2_import(ora_tree* t, int symmetric, int orthonormal, const int* row_ranks, const int* col_ranks,
+                  const double* U, const double* E, const double* V, const double* F, const double* S,
+                  const double* D, ora_h2** o) {
+    return guard([&] {
+        H2Matrix m = H2Matrix::zero(t->bt, symmetric != 0);
+        const ClusterTree& ct = *m.tree;
+        auto basis = [&](BasisTree& b, const int* ranks, const double* pu, const double* pe) {
+            for (int v = 0; v < ct.num_nodes(); ++v) b.set_rank(v, ranks[v]);
+            for (int v : ct.leaves()) {
+                b.leaf_basis(v) = wrap(pu, ct.node(v).size(), ranks[v]);
+                pu += ct.node(v).size() * ranks[v];
+            }
+            for (int v = 0; v < ct.num_nodes(); ++v)
+                if (ct.node(v).parent >= 0) {
+                    b.transfer(v) = wrap(pe, ranks[v], ranks[ct.node(v).parent]);
+                    pe += Index(ranks[v]) * ranks[ct.node(v).parent];
+                }
+        };
+        basis(m.row_basis, row_ranks, U, E);
+        if (!m.symmetric) basis(m.col_basis, col_ranks, V, F);
+        for (size_t i = 0; i < m.coupling.size(); ++i) {
+            const int b = m.blocks->admissible_leaves()[i];
+            if (!m.stores(b)) continue;
+            const Index kr = m.row_basis.rank(m.blocks->node(b).row), kc = m.vbasis().rank(m.blocks->node(b).col);
+            m.coupling[i] = wrap(S, kr, kc);
+            S += kr * kc;
+        }
+        for (size_t i = 0; i < m.dense.size(); ++i) {
+            const int b = m.blocks->dense_leaves()[i];
+            if (!m.stores(b)) continue;
+            const Index mr = ct.node(m.blocks->node(b).row).size(), mc = ct.node(m.blocks->node(b).col).size();
+            m.dense[i] = wrap(D, mr, mc);
+            D += mr * mc;
+        }
+        m.orthonormal = orthonormal != 0;
+        *o = new ora_h2{std::move(m)};
+    });
+}
+
+// y = op(H) x, n x b column-major; ordering 0 user, 1 internal. With
+// nthreads > 1 the columns are split across host threads (each thread runs
+// the reference's four-stage product on its own columns).
+int ora_matvec(ora_h2* h, int transpose, int ordering, int64_t b, const double* x, double* y, int nthreads) {
+    return guard([&] {
+        const H2Matrix& m = h->h;
+        const Index n = m.n();
+        auto run = [&](const Matrix& xx) {
+            if (ordering == 0) return transpose ? m.matvec_transpose(xx) : m.matvec(xx);
+            return transpose ? m.matvec_transpose_internal(xx) : m.matvec_internal(xx);
+        };
+        const int nt = int(std::max<int64_t>(1, std::min<int64_t>(nthreads, b)));
+        if (nt == 1) {
+            out(run(wrap(x, n, b)), y);
+            return;
+        }
+        std::vector<std::thread> th;
+        std::vector<std::string> errs(static_cast<size_t>(nt));
+        for (int i = 0; i < nt; ++i) {
+            th.emplace_back([&, i] {
+                try {
+                    const Index c0 = b * i / nt, c1 = b * (i + 1) / nt;
+                    Matrix yy = run(wrap(x + c0 * n, n, c1 - c0));
+                    out(yy, y + c0 * n);
+                } catch (const std::exception& e) {
+                    errs[size_t(i)] = e.what();
+                }
+            });
+        }
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::runtime_error(e);
+    });
+}
+
+int ora_to_dense(ora_h2* h, double* a) {
+    return guard([&] { out(h->h.to_dense(), a); });
+}
+int ora_orthogonalize(ora_h2* h, ora_h2** o) {
+    return guard([&] { *o = new ora_h2{orthogonalize(h->h)}; });
+}
+int ora_recompress(ora_h2* h, double eps, ora_h2** o) {
+    return guard([&] { *o = new ora_h2{recompress(h->h, eps)}; });
+}
+int ora_low_rank_update(ora_h2* h, int64_t k, const double* X, const double* Y, double eps, ora_h2** o) {
+    return guard([&] {
+        const Index n = h->h.n();
+        *o = new ora_h2{low_rank_update(h->h, LowRankFactor{wrap(X, n, k), wrap(Y, n, k)}, eps)};
+    });
+}
+int ora_frobenius_norm(ora_h2* h, double* v) {
+    return guard([&] { *v = frobenius_norm(h->h); });
+}
+
+// peel_construct over a DenseOperator(a, symmetric) (construction.hpp:300-382)
+int ora_peel_dense(ora_tree* t, const double* a, int symmetric, double eps, int64_t b, int64_t p, int64_t max_rank,
+                   uint64_t seed, double norm_scale, ora_h2** o, int64_t* total_samples, int64_t* level_samples,
+                   int64_t* level_max_rank, int* nlevels) {
+    return guard([&] {
+        const Index n = t->ct->n();
+        DenseOperator op(wrap(a, n, n), symmetric != 0);
+        PeelConfig cfg;
+        cfg.eps = eps;
+        cfg.sample_block_size = b;
+        cfg.oversampling = p;
+        cfg.max_rank = max_rank;
+        cfg.seed = seed;
+        cfg.norm_scale = norm_scale;
+        PeelResult r = peel_construct(op, t->bt, cfg);
+        *total_samples = r.stats.total;
+        *nlevels = int(r.stats.levels.size());
+        for (size_t i = 0; i < r.stats.levels.size(); ++i) {
+            level_samples[i] = r.stats.levels[i].samples;
+            level_max_rank[i] = r.stats.levels[i].max_rank;
+        }
+        *o = new ora_h2{std::move(r.matrix)};
+    });
+}
+
+// peel_construct over an H2Operator of another oracle matrix
+int ora_peel_h2(ora_tree* t, ora_h2* src, double eps, uint64_t seed, double norm_scale, ora_h2** o,
+                int64_t* total_samples) {
+    return guard([&] {
+        H2Operator op(src->h);
+        PeelConfig cfg;
+        cfg.eps = eps;
+        cfg.seed = seed;
+        cfg.norm_scale = norm_scale;
+        PeelResult r = peel_construct(op, t->bt, cfg);
+        *total_samples = r.stats.total;
+        *o = new ora_h2{std::move(r.matrix)};
+    });
+}
+
+// pnorm_estimate(op, 2) of a dense operator (linear_operator.hpp:127-153)
+int ora_pnorm2_dense(const double* a, int64_t n, int symmetric, double* v, int* iters) {
+    return guard([&] {
+        DenseOperator op(wrap(a, n, n), symmetric != 0);
+        NormEstimate e = pnorm_estimate(op, 2);
+        *v = e.value;
+        *iters = e.iterations;
+    });
+}
+
+// reference normal stream (fill_gaussian, construction.hpp:81-85): one
+// fresh distribution over mt19937_64(seed), column-major r x c
+int ora_gaussian(uint64_t seed, int64_t r, int64_t c, double* outp) {
+    return guard([&] {
+        std::mt19937_64 rng(seed);
+        Matrix m(r, c);
+        detail::fill_gaussian(m, rng);
+        out(m, outp);
+    });
+}
+
+}  // extern "C"

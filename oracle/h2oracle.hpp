@@ -53,14 +53,16 @@ struct BBox {
     double extent(int a) const { return hi[size_t(a)] - lo[size_t(a)]; }
     double diameter() const {   // point_set.hpp:72-76
         double s = 0;
-        for (int a = 0; a < dim; ++a) s += extent(a) * extent(a);
+        // explicit fma: the reference builds with -march=native (CMakeLists.txt:10,18-20)
+        // and GCC contracts s += e*e, which decides exact admissibility ties on grids
+        for (int a = 0; a < dim; ++a) s = std::fma(extent(a), extent(a), s);
         return std::sqrt(s);
     }
     double distance(const BBox& o) const {   // point_set.hpp:79-86
         double s = 0;
         for (int a = 0; a < dim; ++a) {
             const double g = std::max({0.0, o.lo[size_t(a)] - hi[size_t(a)], lo[size_t(a)] - o.hi[size_t(a)]});
-            s += g * g;
+            s = std::fma(g, g, s);
         }
         return std::sqrt(s);
     }

@@ -1,0 +1,280 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes access to the CPU restatement of the reference (oracle/h2oracle.hpp,
+built as oracle/build/liboracle.so). Used by tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline / --impl reference leg as the checker and the
+CPU baseline — never by the product path.
+"""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "build", "liboracle.so")
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", _HERE, "-j8"], check=True)
+
+
+if not os.path.exists(LIB_PATH):
+    build()
+
+_lib = C.CDLL(LIB_PATH)
+vp, i32, i64, u64, f64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double
+P = C.POINTER
+
+
+def _sig(name, *args):
+    f = getattr(_lib, name)
+    f.restype = i32
+    f.argtypes = list(args)
+
+
+_lib.ora_last_error.restype = C.c_char_p
+_sig("ora_tree_create", vp, i64, i32, i64, f64, i32, P(vp))
+_lib.ora_tree_destroy.argtypes = [vp]
+_lib.ora_tree_destroy.restype = None
+_sig("ora_tree_info", vp, P(i64), P(i32), P(i32), P(i32), P(i32), P(i32))
+_sig("ora_tree_arrays", vp, *([vp] * 12))
+_sig("ora_random_h2", vp, i32, i64, u64, P(vp))
+_sig("ora_zero", vp, i32, P(vp))
+_sig("ora_fixed_rank_h2", vp, i64, u64, i32, P(vp))
+_lib.ora_h2_destroy.argtypes = [vp]
+_lib.ora_h2_destroy.restype = None
+_sig("ora_h2_info", vp, P(i32), P(i32), vp)
+_sig("ora_h2_ranks", vp, vp, vp)
+_sig("ora_h2_export", vp, *([vp] * 6))
+_sig("ora_h2_import", vp, i32, i32, vp, vp, *([vp] * 6), P(vp))
+_sig("ora_matvec", vp, i32, i32, i64, vp, vp, i32)
+_sig("ora_to_dense", vp, vp)
+_sig("ora_orthogonalize", vp, P(vp))
+_sig("ora_recompress", vp, f64, P(vp))
+_sig("ora_low_rank_update", vp, i64, vp, vp, f64, P(vp))
+_sig("ora_frobenius_norm", vp, P(f64))
+_sig("ora_peel_dense", vp, vp, i32, f64, i64, i64, i64, u64, f64, P(vp), P(i64), vp, vp, P(i32))
+_sig("ora_peel_h2", vp, vp, f64, u64, f64, P(vp), P(i64))
+_sig("ora_pnorm2_dense", vp, i64, i32, P(f64), P(i32))
+_sig("ora_gaussian", u64, i64, i64, vp)
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class OracleMaxRank(OracleError):
+    pass
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = _lib.ora_last_error().decode()
+    if rc == -1:
+        raise ValueError(msg)
+    if rc == -2:
+        raise NotImplementedError(msg)
+    if rc == -3:
+        raise OracleMaxRank(msg)
+    raise OracleError(msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+PARTS = ("U", "E", "V", "F", "S", "D")
+
+
+class Tree:
+    """Cluster tree + block tree of the oracle (cluster_tree.hpp / block_tree.hpp)."""
+
+    def __init__(self, points, leaf, eta=1.0, weak=False):
+        pts = np.asarray(points, np.float64)
+        if pts.ndim == 1:
+            pts = pts[:, None]
+        self.points = np.asfortranarray(pts)
+        h = vp()
+        _check(_lib.ora_tree_create(_p(self.points), pts.shape[0], pts.shape[1], int(leaf), float(eta), int(weak),
+                                    C.byref(h)))
+        self._h = h
+        n, d, nn, nb, na, nd = i64(), i32(), i32(), i32(), i32(), i32()
+        _check(_lib.ora_tree_info(h, C.byref(n), C.byref(d), C.byref(nn), C.byref(nb), C.byref(na), C.byref(nd)))
+        self.n, self.depth, self.num_nodes, self.num_blocks = n.value, d.value, nn.value, nb.value
+        self.perm = np.empty(self.n, np.int64)
+        self.begin = np.empty(nn.value, np.int64)
+        self.end = np.empty(nn.value, np.int64)
+        self.level = np.empty(nn.value, np.int32)
+        self.parent = np.empty(nn.value, np.int32)
+        self.child0 = np.empty(nn.value, np.int32)
+        self.child1 = np.empty(nn.value, np.int32)
+        self.brow = np.empty(nb.value, np.int32)
+        self.bcol = np.empty(nb.value, np.int32)
+        self.btag = np.empty(nb.value, np.int32)
+        self.adm = np.empty(na.value, np.int32)
+        self.dense = np.empty(nd.value, np.int32)
+        _check(_lib.ora_tree_arrays(h, *[_p(a) for a in (self.perm, self.begin, self.end, self.level, self.parent,
+                                                          self.child0, self.child1, self.brow, self.bcol, self.btag,
+                                                          self.adm, self.dense)]))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.ora_tree_destroy(self._h)
+            self._h = None
+
+
+class H2:
+    """Oracle H2Matrix (h2_matrix.hpp:40-306)."""
+
+    def __init__(self, handle, tree):
+        self._h = handle
+        self.tree = tree
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.ora_h2_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def random(tree, symmetric, kmax, seed):
+        """Reference fixture random_h2 with mt19937_64(seed) (test_support.hpp:38-70)."""
+        h = vp()
+        _check(_lib.ora_random_h2(tree._h, int(symmetric), int(kmax), int(seed), C.byref(h)))
+        return H2(h, tree)
+
+    @staticmethod
+    def fixed_rank(tree, k, seed=42, threads=1):
+        """Symmetric fixed-rank content (CPU-only benchmark inputs)."""
+        h = vp()
+        _check(_lib.ora_fixed_rank_h2(tree._h, int(k), int(seed), int(threads), C.byref(h)))
+        return H2(h, tree)
+
+    @staticmethod
+    def zero(tree, symmetric):
+        h = vp()
+        _check(_lib.ora_zero(tree._h, int(symmetric), C.byref(h)))
+        return H2(h, tree)
+
+    @staticmethod
+    def from_packed(tree, symmetric, row_ranks, col_ranks, parts, orthonormal=False):
+        rr = np.ascontiguousarray(row_ranks, np.int32)
+        cr = np.ascontiguousarray(col_ranks if col_ranks is not None else row_ranks, np.int32)
+        arrs = [np.ascontiguousarray(parts.get(k, np.zeros(0)), np.float64) for k in PARTS]
+        h = vp()
+        _check(_lib.ora_h2_import(tree._h, int(symmetric), int(orthonormal), _p(rr), _p(cr), *[_p(a) for a in arrs],
+                                  C.byref(h)))
+        return H2(h, tree)
+
+    def info(self):
+        s, o = i32(), i32()
+        sizes = np.zeros(6, np.int64)
+        _check(_lib.ora_h2_info(self._h, C.byref(s), C.byref(o), _p(sizes)))
+        return bool(s.value), bool(o.value), [int(x) for x in sizes]
+
+    @property
+    def symmetric(self):
+        return self.info()[0]
+
+    def ranks(self):
+        r = np.empty(self.tree.num_nodes, np.int32)
+        c = np.empty(self.tree.num_nodes, np.int32)
+        _check(_lib.ora_h2_ranks(self._h, _p(r), _p(c)))
+        return r, c
+
+    def export(self):
+        sizes = self.info()[2]
+        arrs = [np.empty(s, np.float64) for s in sizes]
+        _check(_lib.ora_h2_export(self._h, *[_p(a) for a in arrs]))
+        return dict(zip(PARTS, arrs))
+
+    def matvec(self, x, transpose=False, ordering=0, threads=1):
+        x = np.asarray(x, np.float64)
+        vec = x.ndim == 1
+        xf = np.asfortranarray(x[:, None] if vec else x)
+        y = np.empty_like(xf, order="F")
+        _check(_lib.ora_matvec(self._h, int(transpose), int(ordering), xf.shape[1], _p(xf), _p(y), int(threads)))
+        return y[:, 0] if vec else y
+
+    def to_dense(self):
+        a = np.empty((self.tree.n, self.tree.n), order="F")
+        _check(_lib.ora_to_dense(self._h, _p(a)))
+        return a
+
+    def orthogonalize(self):
+        h = vp()
+        _check(_lib.ora_orthogonalize(self._h, C.byref(h)))
+        return H2(h, self.tree)
+
+    def recompress(self, eps):
+        h = vp()
+        _check(_lib.ora_recompress(self._h, float(eps), C.byref(h)))
+        return H2(h, self.tree)
+
+    def low_rank_update(self, X, Y, eps):
+        X = np.asfortranarray(X, np.float64)
+        Y = np.asfortranarray(Y, np.float64)
+        h = vp()
+        _check(_lib.ora_low_rank_update(self._h, X.shape[1], _p(X), _p(Y), float(eps), C.byref(h)))
+        return H2(h, self.tree)
+
+    def frobenius_norm(self):
+        v = f64()
+        _check(_lib.ora_frobenius_norm(self._h, C.byref(v)))
+        return v.value
+
+
+def peel_dense(tree, a, symmetric, eps=1e-4, b=16, p=10, max_rank=0, seed=42, norm_scale=0.0):
+    """peel_construct(DenseOperator(a, symmetric), bt, cfg) (construction.hpp:300-382)."""
+    a = np.asfortranarray(a, np.float64)
+    h = vp()
+    tot = i64()
+    ls = np.zeros(64, np.int64)
+    lr = np.zeros(64, np.int64)
+    nl = i32()
+    _check(_lib.ora_peel_dense(tree._h, _p(a), int(symmetric), float(eps), int(b), int(p), int(max_rank), int(seed),
+                               float(norm_scale), C.byref(h), C.byref(tot), _p(ls), _p(lr), C.byref(nl)))
+    return H2(h, tree), {"total": tot.value, "level_samples": ls[:nl.value].tolist(),
+                         "level_max_rank": lr[:nl.value].tolist()}
+
+
+def peel_h2(tree, src, eps=1e-4, seed=42, norm_scale=0.0):
+    h = vp()
+    tot = i64()
+    _check(_lib.ora_peel_h2(tree._h, src._h, float(eps), int(seed), float(norm_scale), C.byref(h), C.byref(tot)))
+    return H2(h, tree), tot.value
+
+
+def pnorm2_dense(a, symmetric):
+    a = np.asfortranarray(a, np.float64)
+    v, it = f64(), i32()
+    _check(_lib.ora_pnorm2_dense(_p(a), a.shape[0], int(symmetric), C.byref(v), C.byref(it)))
+    return v.value, it.value
+
+
+def gaussian(seed, r, c):
+    """The reference's normal stream (fresh normal_distribution over mt19937_64(seed))."""
+    out = np.empty((r, c), order="F")
+    _check(_lib.ora_gaussian(int(seed), int(r), int(c), _p(out)))
+    return out
+
+
+def grid1d(n, a=0.0, b=1.0):
+    """test_support.hpp:12-16."""
+    return (a + (b - a) * np.arange(n) / max(n - 1, 1))[:, None]
+
+
+def grid2d(nx, ny, a=0.0, b=1.0):
+    """test_support.hpp:18-26 (row j*nx+i = (x_i, y_j))."""
+    i = np.tile(np.arange(nx), ny)
+    j = np.repeat(np.arange(ny), nx)
+    return np.stack([a + (b - a) * i / max(nx - 1, 1), a + (b - a) * j / max(ny - 1, 1)], axis=1)
+
+
+def grid3d(nx, ny, nz, a=0.0, b=1.0):
+    i = np.tile(np.arange(nx), ny * nz)
+    j = np.tile(np.repeat(np.arange(ny), nx), nz)
+    k = np.repeat(np.arange(nz), nx * ny)
+    s = lambda q, m: a + (b - a) * q / max(m - 1, 1)
+    return np.stack([s(i, nx), s(j, ny), s(k, nz)], axis=1)

@@ -1,0 +1,89 @@
+"""ctypes binding of the C ABI (include/h2c.h) in lib/libh2b200.so.
+
+The product path has no CPU fallback: if the shared library is missing the
+import fails loudly (build it with `make -C paper_2003_10173_b200` or
+`python -c "import __graft_entry__ as g; g.build()"`).
+"""
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libh2b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"paper_2003_10173_b200: native library {LIB_PATH} is missing; build it with "
+        "`make -C paper_2003_10173_b200` (no CPU fallback exists)")
+
+lib = C.CDLL(LIB_PATH)
+
+i32, i64, f64, vp = C.c_int, C.c_int64, C.c_double, C.c_void_p
+P = C.POINTER
+H = C.c_void_p  # opaque handles
+
+H2C_OK = 0
+H2C_INVALID_ARGUMENT = -1
+H2C_LOGIC_ERROR = -2
+H2C_MAX_RANK_ERROR = -3
+H2C_RUNTIME_ERROR = -4
+H2C_CUDA_ERROR = -5
+H2C_CALLBACK_ERROR = -6
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class max_rank_error(RuntimeError):
+    """Mirror of h2::max_rank_error (construction.hpp:61-66)."""
+
+
+def _sig(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("h2c_last_error", C.c_char_p)
+_sig("h2c_version", C.c_char_p)
+_sig("h2c_cluster_tree_create", i32, vp, i64, i32, i64, P(H))
+_sig("h2c_cluster_tree_destroy", None, H)
+_sig("h2c_cluster_tree_info", i32, H, P(i64), P(i32), P(i32), P(i32), P(i32))
+_sig("h2c_cluster_tree_nodes", i32, H, vp, vp, vp, vp, vp, vp, vp, vp)
+_sig("h2c_cluster_tree_perm", i32, H, vp)
+_sig("h2c_block_tree_create", i32, H, f64, i32, P(H))
+_sig("h2c_block_tree_destroy", None, H)
+_sig("h2c_block_tree_info", i32, H, P(i32), P(i32), P(i32), P(i32))
+_sig("h2c_block_tree_nodes", i32, H, vp, vp, vp, vp, vp)
+_sig("h2c_block_tree_leaves", i32, H, vp, vp)
+_sig("h2c_matrix_create", i32, H, i32, vp, vp, P(H))
+_sig("h2c_matrix_destroy", None, H)
+_sig("h2c_matrix_info", i32, H, P(i64), P(i32), P(i32))
+_sig("h2c_matrix_set_orthonormal", i32, H, i32)
+_sig("h2c_matrix_sizes", i32, H, vp)
+_sig("h2c_matrix_ranks", i32, H, vp, vp)
+_sig("h2c_matrix_upload", i32, H, vp, vp, vp, vp, vp, vp)
+_sig("h2c_matrix_download", i32, H, vp, vp, vp, vp, vp, vp)
+_sig("h2c_matrix_kernel", i32, H, vp, i32, f64, i32, P(H))
+_sig("h2c_hgemv", i32, H, i32, i32, i64, i64, vp, i64, vp, i64, f64, f64, vp)
+_sig("h2c_matvec_host", i32, H, i32, i32, i64, i64, vp, vp)
+_sig("h2c_hgemv_launches", i32, H, i32, i64, P(i32))
+
+def check(rc):
+    """Raise the Python mirror of the reference exception kind."""
+    if rc == H2C_OK:
+        return
+    msg = lib.h2c_last_error().decode(errors="replace")
+    if rc == H2C_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == H2C_LOGIC_ERROR:
+        raise NotImplementedError(msg)
+    if rc == H2C_MAX_RANK_ERROR:
+        raise max_rank_error(msg)
+    if rc == H2C_CUDA_ERROR:
+        raise CudaError(msg)
+    raise RuntimeError(f"h2c error {rc}: {msg}")
+
+
+_sig("h2c_hgemv_stage_times", i32, H, i32, i32, i64, i64, vp, i64, vp, i64, vp, i32, P(i32), vp, vp, vp, vp)

@@ -1,0 +1,274 @@
+// extern "C" boundary (include/h2c.h) over the C++ host layer and CUDA kernels.
+#include "../../include/h2c.h"
+
+#include <cstring>
+#include <string>
+
+#include "h2dev.hpp"
+#include "matrix.hpp"
+
+struct h2c_cluster_tree_s {
+    std::shared_ptr<h2b::ClusterTree> t;
+};
+struct h2c_block_tree_s {
+    std::shared_ptr<h2b::BlockTree> b;
+};
+struct h2c_matrix_s {
+    std::unique_ptr<h2b::H2Dev> h;
+    h2b::Workspace ws;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return H2C_OK;
+    } catch (const h2b::cuda_error& e) {
+        g_err = e.what();
+        return H2C_CUDA_ERROR;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return H2C_INVALID_ARGUMENT;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return H2C_LOGIC_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return H2C_RUNTIME_ERROR;
+    }
+}
+void need(bool ok, const char* msg) {
+    if (!ok) throw std::invalid_argument(msg);
+}
+}  // namespace
+
+extern "C" {
+
+const char* h2c_last_error(void) { return g_err.c_str(); }
+const char* h2c_version(void) { return "h2b200 0.1 (sm_100a)"; }
+
+int h2c_cluster_tree_create(const double* coords, int64_t n, int dim, int64_t leaf_size, h2c_cluster_tree* out) {
+    return guard([&] {
+        need(out != nullptr, "null output handle");
+        need(coords != nullptr || n == 0, "null coordinates");
+        auto t = h2b::build_cluster_tree(coords, n, dim, leaf_size);
+        *out = new h2c_cluster_tree_s{std::move(t)};
+    });
+}
+void h2c_cluster_tree_destroy(h2c_cluster_tree t) { delete t; }
+
+int h2c_cluster_tree_info(h2c_cluster_tree t, int64_t* n, int* dim, int* depth, int* num_nodes, int* num_leaves) {
+    return guard([&] {
+        need(t != nullptr, "null tree");
+        if (n) *n = t->t->n;
+        if (dim) *dim = t->t->dim;
+        if (depth) *depth = t->t->depth;
+        if (num_nodes) *num_nodes = t->t->num_nodes();
+        if (num_leaves) *num_leaves = int(t->t->leaves.size());
+    });
+}
+
+int h2c_cluster_tree_nodes(h2c_cluster_tree t, int64_t* begin, int64_t* end, int* level, int* parent, int* child0,
+                           int* child1, double* lo, double* hi) {
+    return guard([&] {
+        need(t != nullptr, "null tree");
+        const auto& c = *t->t;
+        const size_t nn = size_t(c.num_nodes());
+        if (begin) std::memcpy(begin, c.begin.data(), nn * sizeof(int64_t));
+        if (end) std::memcpy(end, c.end.data(), nn * sizeof(int64_t));
+        if (level) std::memcpy(level, c.level.data(), nn * sizeof(int));
+        if (parent) std::memcpy(parent, c.parent.data(), nn * sizeof(int));
+        if (child0) std::memcpy(child0, c.child0.data(), nn * sizeof(int));
+        if (child1) std::memcpy(child1, c.child1.data(), nn * sizeof(int));
+        if (lo) std::memcpy(lo, c.lo.data(), 3 * nn * sizeof(double));
+        if (hi) std::memcpy(hi, c.hi.data(), 3 * nn * sizeof(double));
+    });
+}
+
+int h2c_cluster_tree_perm(h2c_cluster_tree t, int64_t* perm) {
+    return guard([&] {
+        need(t != nullptr && perm != nullptr, "null argument");
+        std::memcpy(perm, t->t->perm.data(), t->t->perm.size() * sizeof(int64_t));
+    });
+}
+
+int h2c_block_tree_create(h2c_cluster_tree t, double eta, int weak, h2c_block_tree* out) {
+    return guard([&] {
+        need(t != nullptr && out != nullptr, "null argument");
+        *out = new h2c_block_tree_s{h2b::build_block_tree(t->t, eta, weak != 0)};
+    });
+}
+void h2c_block_tree_destroy(h2c_block_tree b) { delete b; }
+
+int h2c_block_tree_info(h2c_block_tree b, int* num_nodes, int* num_adm, int* num_dense, int* max_level) {
+    return guard([&] {
+        need(b != nullptr, "null block tree");
+        if (num_nodes) *num_nodes = b->b->num_nodes();
+        if (num_adm) *num_adm = int(b->b->adm.size());
+        if (num_dense) *num_dense = int(b->b->dense.size());
+        if (max_level) *max_level = b->b->max_level;
+    });
+}
+
+int h2c_block_tree_nodes(h2c_block_tree b, int* row, int* col, int* level, int* parent, int* tag) {
+    return guard([&] {
+        need(b != nullptr, "null block tree");
+        const auto& t = *b->b;
+        const size_t nn = size_t(t.num_nodes());
+        if (row) std::memcpy(row, t.row.data(), nn * sizeof(int));
+        if (col) std::memcpy(col, t.col.data(), nn * sizeof(int));
+        if (level) std::memcpy(level, t.level.data(), nn * sizeof(int));
+        if (parent) std::memcpy(parent, t.parent.data(), nn * sizeof(int));
+        if (tag) std::memcpy(tag, t.tag.data(), nn * sizeof(int));
+    });
+}
+
+int h2c_block_tree_leaves(h2c_block_tree b, int* adm, int* dense) {
+    return guard([&] {
+        need(b != nullptr, "null block tree");
+        if (adm) std::memcpy(adm, b->b->adm.data(), b->b->adm.size() * sizeof(int));
+        if (dense) std::memcpy(dense, b->b->dense.data(), b->b->dense.size() * sizeof(int));
+    });
+}
+
+int h2c_matrix_create(h2c_block_tree b, int symmetric, const int* row_ranks, const int* col_ranks, h2c_matrix* out) {
+    return guard([&] {
+        need(b != nullptr && out != nullptr, "null argument");
+        auto m = new h2c_matrix_s;
+        try {
+            m->h = h2b::make_h2(b->b, symmetric != 0, row_ranks, col_ranks);
+            m->h->orthonormal = row_ranks == nullptr;   // zero(): orthonormal (h2_matrix.hpp:74)
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+void h2c_matrix_destroy(h2c_matrix h) { delete h; }
+
+int h2c_matrix_info(h2c_matrix h, int64_t* n, int* symmetric, int* orthonormal) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        if (n) *n = h->h->tree().n;
+        if (symmetric) *symmetric = h->h->symmetric;
+        if (orthonormal) *orthonormal = h->h->orthonormal;
+    });
+}
+
+int h2c_matrix_set_orthonormal(h2c_matrix h, int orthonormal) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        h->h->orthonormal = orthonormal != 0;
+    });
+}
+
+int h2c_matrix_sizes(h2c_matrix h, int64_t* sizes) {
+    return guard([&] {
+        need(h != nullptr && sizes != nullptr, "null argument");
+        h2b::packed_sizes(*h->h, sizes);
+    });
+}
+
+int h2c_matrix_ranks(h2c_matrix h, int* row_ranks, int* col_ranks) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        const auto& m = *h->h;
+        if (row_ranks) std::memcpy(row_ranks, m.row.rank.data(), m.row.rank.size() * sizeof(int));
+        if (col_ranks) {
+            const auto& r = m.vbasis().rank;
+            std::memcpy(col_ranks, r.data(), r.size() * sizeof(int));
+        }
+    });
+}
+
+int h2c_matrix_upload(h2c_matrix h, const double* U, const double* E, const double* V, const double* F,
+                      const double* S, const double* D) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        const double* parts[6] = {U, E, V, F, S, D};
+        h2b::upload_packed(*h->h, parts);
+    });
+}
+
+int h2c_matrix_download(h2c_matrix h, double* U, double* E, double* V, double* F, double* S, double* D) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        double* parts[6] = {U, E, V, F, S, D};
+        h2b::download_packed(*h->h, parts);
+    });
+}
+
+int h2c_matrix_kernel(h2c_block_tree b, const double* coords, int kind, double ell, int rank, h2c_matrix* out) {
+    return guard([&] {
+        need(b != nullptr && coords != nullptr && out != nullptr, "null argument");
+        need(kind >= 0 && kind <= 2, "kernel kind must be 0, 1 or 2");
+        need(rank >= 1, "rank must be >= 1");
+        auto m = new h2c_matrix_s;
+        try {
+            m->h = h2b::make_kernel_h2(b->b, coords, kind, ell, rank);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int h2c_hgemv(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, int64_t ldx,
+              double* y, int64_t ldy, double alpha, double beta, void* stream) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        need(ordering == 0 || ordering == 1, "ordering must be 0 (user) or 1 (internal)");
+        need(x != nullptr && y != nullptr, "null vector pointer");
+        h2b::hgemv(*h->h, transpose != 0, ordering == 0, n, b, x, ldx, y, ldy, alpha, beta,
+                   static_cast<cudaStream_t>(stream), h->ws);
+    });
+}
+
+int h2c_matvec_host(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, double* y) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        need(x != nullptr && y != nullptr, "null vector pointer");
+        if (n != h->h->tree().n) throw std::invalid_argument("matvec: dimension mismatch");
+        if (b < 1) throw std::invalid_argument("matvec: need at least one column");
+        const size_t cnt = size_t(n * b);
+        if (h->ws.hx.size() < cnt) h->ws.hx.resize(cnt);
+        if (h->ws.hy.size() < cnt) h->ws.hy.resize(cnt);
+        H2B_CUDA(cudaMemcpyAsync(h->ws.hx.data(), x, cnt * sizeof(double), cudaMemcpyHostToDevice, nullptr));
+        h2b::hgemv(*h->h, transpose != 0, ordering == 0, n, b, h->ws.hx.data(), n, h->ws.hy.data(), n, 1.0, 0.0,
+                   nullptr, h->ws);
+        H2B_CUDA(cudaMemcpyAsync(y, h->ws.hy.data(), cnt * sizeof(double), cudaMemcpyDeviceToHost, nullptr));
+        H2B_CUDA(cudaStreamSynchronize(nullptr));
+    });
+}
+
+int h2c_hgemv_stage_times(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x,
+                          int64_t ldx, double* y, int64_t ldy, void* stream, int max_records, int* count,
+                          int* stage, double* ms, double* flops, double* bytes) {
+    return guard([&] {
+        need(h != nullptr && count != nullptr, "null argument");
+        std::vector<h2b::StageRecord> rec;
+        h2b::hgemv_timed(*h->h, transpose != 0, ordering == 0, n, b, x, ldx, y, ldy, 1.0, 0.0,
+                         static_cast<cudaStream_t>(stream), h->ws, rec);
+        *count = int(rec.size());
+        for (int i = 0; i < int(rec.size()) && i < max_records; ++i) {
+            if (stage) stage[i] = rec[size_t(i)].stage;
+            if (ms) ms[i] = rec[size_t(i)].ms;
+            if (flops) flops[i] = rec[size_t(i)].flops;
+            if (bytes) bytes[i] = rec[size_t(i)].bytes;
+        }
+    });
+}
+
+int h2c_hgemv_launches(h2c_matrix h, int transpose, int64_t b, int* launches) {
+    return guard([&] {
+        need(h != nullptr && launches != nullptr, "null argument");
+        *launches = h2b::hgemv_launch_count(*h->h, transpose != 0, b);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+#pragma once
+// Device-resident H^2 matrix (the B200 counterpart of H2Matrix,
+// reference h2_matrix.hpp:42-49) and the hgemv execution plan.
+//
+// HBM layout (all FP64, column-major blocks, packed back to back):
+//   leaf bases   U_t   m_t x k_t      for leaves in id order
+//   transfers    E_v   k_v x k_par    for non-root nodes in id order
+//   couplings    S_b   k_row x k_col  for stored admissible leaves in ordinal order
+//   dense blocks D_b   m_t x m_s      for stored dense leaves in ordinal order
+// Symmetric matrices store one basis tree and only canonical (row <= col)
+// blocks, exactly like the reference (h2_matrix.hpp:103); hgemv reads a
+// canonical block for both orientations.
+#include <memory>
+#include <mutex>
+
+#include "common.hpp"
+#include "tree.hpp"
+
+namespace h2b {
+
+struct BasisDev {
+    std::vector<int> rank;            // per node
+    std::vector<int64_t> leaf_off;    // per node, -1 unless leaf
+    std::vector<int64_t> xfer_off;    // per node, -1 for the root
+    DeviceArray<double> leaf, xfer;
+    void layout(const ClusterTree& t);   // offsets from ranks
+};
+
+struct HgemvPlan;
+
+struct H2Dev {
+    std::shared_ptr<const BlockTree> bt;
+    bool symmetric = false;
+    bool orthonormal = false;
+    BasisDev row, col;                 // col unused when symmetric
+    std::vector<int64_t> s_off, d_off; // per ordinal, -1 if not stored
+    DeviceArray<double> S, D;
+
+    const ClusterTree& tree() const { return *bt->tree; }
+    const BasisDev& vbasis() const { return symmetric ? row : col; }
+    bool stores(int b) const { return !symmetric || bt->canonical(b); }
+    void layout_blocks();              // s_off / d_off from ranks
+
+    mutable std::mutex plan_mu;
+    mutable std::shared_ptr<HgemvPlan> plan[2];   // [transpose]
+    void invalidate_plans() {
+        std::lock_guard<std::mutex> g(plan_mu);
+        plan[0].reset();
+        plan[1].reset();
+    }
+};
+
+// per-call scratch (x in internal blocked layout, upsweep / downsweep coefficients)
+struct Workspace {
+    DeviceArray<double> xint, xhat, yhat;
+    DeviceArray<double> hx, hy;   // staging of the host-buffer entry point
+};
+
+void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
+           double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws);
+
+// one launch of a timed hgemv: stage (0 gather, 1 leaf upsweep, 2 transfer
+// upsweep, 3 coupling, 4 downsweep, 5 leaf + dense near-field), CUDA-event
+// duration, algorithmic flops and bytes of that launch
+struct StageRecord {
+    int stage;
+    float ms;
+    double flops, bytes;
+};
+void hgemv_timed(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
+                 double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
+                 std::vector<StageRecord>& records);
+
+// kernel launches one hgemv issues (for the bench's gpu_launches claim)
+int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b);
+
+}  // namespace h2b

@@ -1,0 +1,592 @@
+// hgemv on B200: the four-stage H^2 product of the reference
+// (h2_matrix.hpp:246-305) as a short sequence of segmented FP64 DMMA GEMM
+// launches over per-level task lists (see seg_gemm.cuh). The permutation
+// gather (cluster_tree.hpp:82-86) is one blocked-layout pass over x and the
+// scatter back to user order (cluster_tree.hpp:88-92) is fused into the
+// leaf/dense epilogue together with alpha/beta.
+#include <algorithm>
+#include <cstring>
+#include <unordered_set>
+
+#include "h2dev.hpp"
+#include "seg_gemm.cuh"
+
+namespace h2b {
+
+// ---------------------------------------------------------------------------
+// device building blocks
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int src_bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// swizzled position of element (r, c) of an R x C column-major tile:
+// XOR of row bits 2..3 with the column's low bits makes the DMMA fragment
+// loads (8 rows x 4 cols per half warp pattern) conflict free
+template <int R>
+__device__ __forceinline__ int swz(int r, int c) {
+    return c * R + (r ^ ((c & 3) << 2));
+}
+
+// stage an R x C tile of a column-major global block (ld = lda), zero-filling
+// rows >= rv and cols >= cv. 128 threads.
+template <int R, int C, bool VEC>
+__device__ __forceinline__ void load_tile(double* tile, const double* base, int64_t lda, int rv, int cv, int tid) {
+    if constexpr (VEC) {
+        constexpr int NP = R * C / 2;
+#pragma unroll
+        for (int p0 = 0; p0 < NP; p0 += 128) {
+            const int p = p0 + tid;
+            const int r = (p % (R / 2)) * 2, c = p / (R / 2);
+            const int nb = c < cv ? max(0, min(2, rv - r)) * 8 : 0;
+            cp_async16(tile + swz<R>(r, c), nb ? base + r + c * lda : base, nb);
+        }
+    } else {
+        constexpr int NE = R * C;
+#pragma unroll
+        for (int p0 = 0; p0 < NE; p0 += 128) {
+            const int p = p0 + tid;
+            const int r = p % R, c = p / R;
+            const bool ok = r < rv && c < cv;
+            cp_async8(tile + swz<R>(r, c), ok ? base + r + c * lda : base, ok ? 8 : 0);
+        }
+    }
+}
+
+template <int MT, int NB, int WM, int WN, int STAGES, bool VEC, int MODE>
+__global__ void __launch_bounds__(128) seg_gemm_kernel(SegArgs args) {
+    constexpr int KC = 32;
+    constexpr int A_SZ = MT * KC, B_SZ = KC * NB, ST_SZ = A_SZ + B_SZ;
+    constexpr int TM = MT / (WM * 8), TN = NB / (WN * 8);
+    static_assert(WM * WN == 4 && TM >= 1 && TN >= 1, "warp layout");
+    extern __shared__ __align__(16) double smem[];
+
+    const SegTask tk = args.tasks[blockIdx.x];
+    const int j0 = blockIdx.y * NB;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % WM, wn = warp / WM;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int rows_here = min(MT, tk.rows - tk.row0);
+    const int ncols = int(min(int64_t(NB), args.b - j0));
+
+    double acc[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    int pe = tk.e_begin, pk = 0;   // producer cursor (entry, k offset)
+    auto issue = [&](int stage) {
+        const SegEntry e = args.entries[pe];
+        double* at = smem + stage * ST_SZ;
+        double* bt = at + A_SZ;
+        const int krem = min(KC, e.k - pk);
+        if (!e.trans) load_tile<MT, KC, VEC>(at, e.A + tk.row0 + int64_t(pk) * e.lda, e.lda, rows_here, krem, tid);
+        else load_tile<KC, MT, VEC>(at, e.A + pk + int64_t(tk.row0) * e.lda, e.lda, krem, rows_here, tid);
+        const double* sb = e.src == 0 ? args.src0 : (e.src == 1 ? args.src1 : args.src2);
+        load_tile<KC, NB, VEC>(bt, sb + e.b_unit * args.b + pk + int64_t(j0) * e.ldb, e.ldb, krem, ncols, tid);
+        pk += KC;
+        if (pk >= e.k) {
+            ++pe;
+            pk = 0;
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < tk.nsteps) issue(s);
+        cp_async_commit();
+    }
+    int ce = tk.e_begin, ck = 0;   // consumer cursor
+    for (int s = 0; s < tk.nsteps; ++s) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        if (s + STAGES - 1 < tk.nsteps) issue((s + STAGES - 1) % STAGES);
+        cp_async_commit();
+        const SegEntry& ec = args.entries[ce];
+        const bool trans = ec.trans;
+        const int kc_steps = (min(KC, ec.k - ck) + 3) >> 2;
+        ck += KC;
+        if (ck >= ec.k) {
+            ++ce;
+            ck = 0;
+        }
+        const double* at = smem + (s % STAGES) * ST_SZ;
+        const double* bt = at + A_SZ;
+#pragma unroll 4
+        for (int k4 = 0; k4 < kc_steps; ++k4) {
+            const int k = k4 * 4 + t4;
+            double a[TM], b[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) {
+                const int m = (wm * TM + i) * 8 + g;
+                a[i] = trans ? at[swz<KC>(k, m)] : at[swz<MT>(m, k)];
+            }
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int nn = (wn * TN + j) * 8 + g;
+                b[j] = bt[swz<KC>(k, nn)];
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        }
+    }
+    cp_async_wait<0>();
+
+    // epilogue
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int m = (wm * TM + i) * 8 + g;
+        if (m >= rows_here) continue;
+        const int row = tk.row0 + m;
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int nn = (wn * TN + j) * 8 + 2 * t4 + h;
+                if (nn >= ncols) continue;
+                const int64_t col = j0 + nn;
+                const double v = acc[i][j][h];
+                if constexpr (MODE == kModeY) {
+                    const int64_t ir = tk.out_unit + row;
+                    const int64_t ur = args.perm ? args.perm[ir] : ir;
+                    double* p = args.out + ur + col * args.ldy;
+                    *p = args.beta == 0.0 ? args.alpha * v : args.alpha * v + args.beta * *p;
+                } else {
+                    double* p = args.out + tk.out_unit * args.b + row + col * tk.out_ld;
+                    if constexpr (MODE == kModeAdd) *p += v;
+                    else *p = v;
+                }
+            }
+    }
+}
+
+// x (n x b, user or internal ordering, ld) -> blocked internal layout: leaf t
+// occupies [begin_t*b, (begin_t+m_t)*b) as an m_t x b column-major block
+__global__ void gather_blocked_kernel(const double* __restrict__ x, int64_t ldx, const int* __restrict__ perm,
+                                      const int64_t* __restrict__ leaf_begin, const int* __restrict__ leaf_m,
+                                      int64_t b, double* __restrict__ xint) {
+    const int64_t beg = leaf_begin[blockIdx.x];
+    const int m = leaf_m[blockIdx.x];
+    const int64_t total = int64_t(m) * b;
+    double* dst = xint + beg * b;
+    for (int64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int i = int(idx % m);
+        const int64_t j = idx / m;
+        const int64_t r = perm ? perm[beg + i] : beg + i;
+        dst[idx] = x[r + j * ldx];
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct LaunchDesc {
+    int task_begin = 0, task_end = 0;
+    int mt = 64;
+    int mode = kModeSet;
+    int out = 1;           // 1 = xhat, 2 = yhat, 3 = y
+    bool vec = false;      // 16-byte staging legal (before the b-dependent check)
+    bool units_even = true;
+    bool zero_yhat = false;   // memset yhat before this launch
+    // algorithmic work of this launch: flops per vector column, distinct
+    // stored-payload bytes read (each canonical block once), and doubles per
+    // column of B operands read / outputs written
+    double flops_per_col = 0, payload_bytes = 0, bsrc_per_col = 0, out_per_col = 0;
+    int stage = 0;            // 1 leaf up, 2 transfer up, 3 coupling, 4 downsweep, 5 leaf+dense
+};
+
+struct HgemvPlan {
+    std::vector<LaunchDesc> launches;
+    DeviceArray<SegTask> tasks;
+    DeviceArray<SegEntry> entries;
+    DeviceArray<int> perm;
+    DeviceArray<int64_t> leaf_begin;
+    DeviceArray<int> leaf_m;
+    int num_leaves = 0;
+    int64_t coef_up = 0, coef_down = 0;
+};
+
+namespace {
+
+struct PlanBuilder {
+    std::vector<SegTask> tasks;
+    std::vector<SegEntry> entries;
+    std::vector<LaunchDesc> launches;
+
+    struct Pending {
+        int rows;
+        int out_ld;
+        int64_t out_unit;
+        std::vector<SegEntry> es;
+    };
+
+    void emit(std::vector<Pending>& outs, int mode, int out, int stage, bool zero_yhat = false) {
+        LaunchDesc ld;
+        ld.stage = stage;
+        ld.mode = mode;
+        ld.out = out;
+        ld.zero_yhat = zero_yhat;
+        int maxrows = 0;
+        for (auto& p : outs) maxrows = std::max(maxrows, p.rows);
+        ld.mt = maxrows > 32 ? 64 : 32;
+        ld.task_begin = int(tasks.size());
+        bool vec = true, ue = true;
+        for (auto& p : outs) {
+            if (p.rows <= 0) continue;
+            const int e0 = int(entries.size());
+            int nsteps = 0;
+            for (auto& e : p.es) {
+                if (e.k <= 0) continue;
+                entries.push_back(e);
+                nsteps += (e.k + 31) / 32;
+                const int64_t aoff = reinterpret_cast<uintptr_t>(e.A) / sizeof(double);
+                vec = vec && (aoff % 2 == 0) && (e.lda % 2 == 0) && (e.ldb % 2 == 0);
+                ue = ue && (e.b_unit % 2 == 0);
+            }
+            const int e1 = int(entries.size());
+            for (int r0 = 0; r0 < p.rows; r0 += ld.mt) {
+                SegTask tk{};
+                tk.e_begin = e0;
+                tk.e_end = e1;
+                tk.nsteps = nsteps;
+                tk.rows = p.rows;
+                tk.row0 = r0;
+                tk.out_ld = p.out_ld;
+                tk.out_unit = p.out_unit;
+                tasks.push_back(tk);
+            }
+        }
+        ld.vec = vec;
+        ld.units_even = ue;
+        ld.task_end = int(tasks.size());
+        {
+            std::unordered_set<const double*> seen_a;
+            std::unordered_set<int64_t> seen_b;
+            for (auto& p : outs) {
+                if (p.rows <= 0) continue;
+                ld.out_per_col += p.rows;
+                for (auto& e : p.es) {
+                    if (e.k <= 0) continue;
+                    ld.flops_per_col += 2.0 * p.rows * e.k;
+                    if (seen_a.insert(e.A).second) ld.payload_bytes += 8.0 * double(p.rows) * e.k;
+                    if (seen_b.insert((int64_t(e.src) << 56) ^ e.b_unit).second) ld.bsrc_per_col += e.k;
+                }
+            }
+        }
+        if (ld.task_end > ld.task_begin || zero_yhat) launches.push_back(ld);
+    }
+};
+
+SegEntry make_entry(const double* A, int lda, int k, bool trans, int src, int64_t b_unit, int ldb) {
+    SegEntry e{};
+    e.A = A;
+    e.lda = lda;
+    e.k = k;
+    e.trans = trans ? 1 : 0;
+    e.src = src;
+    e.b_unit = b_unit;
+    e.ldb = ldb;
+    return e;
+}
+
+std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
+    const ClusterTree& ct = h.tree();
+    const BlockTree& bt = *h.bt;
+    const int nn = ct.num_nodes();
+    const bool swap = transpose && !h.symmetric;
+    const BasisDev& up = swap ? h.row : h.vbasis();
+    const BasisDev& down = swap ? h.col : h.row;
+    auto plan = std::make_shared<HgemvPlan>();
+    std::vector<int64_t> cu(static_cast<size_t>(nn)), cd(static_cast<size_t>(nn));
+    for (int v = 0; v < nn; ++v) {
+        cu[size_t(v)] = plan->coef_up;
+        plan->coef_up += up.rank[size_t(v)];
+        cd[size_t(v)] = plan->coef_down;
+        plan->coef_down += down.rank[size_t(v)];
+    }
+    PlanBuilder pb;
+    using P = PlanBuilder::Pending;
+    // stage 1a: leaves  xhat_t = U_t^T X_t
+    {
+        std::vector<P> outs;
+        for (int t : ct.leaves) {
+            const int k = up.rank[size_t(t)], m = int(ct.size(t));
+            P p{k, k, cu[size_t(t)], {}};
+            p.es.push_back(make_entry(up.leaf.data() + up.leaf_off[size_t(t)], m, m, true, 0, ct.begin[size_t(t)], m));
+            outs.push_back(std::move(p));
+        }
+        pb.emit(outs, kModeSet, 1, 1);
+    }
+    // stage 1b: transfers bottom-up
+    for (int l = ct.depth - 1; l >= 0; --l) {
+        std::vector<P> outs;
+        for (int v : ct.levels[size_t(l)]) {
+            if (ct.is_leaf(v)) continue;
+            const int kv = up.rank[size_t(v)];
+            P p{kv, kv, cu[size_t(v)], {}};
+            for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]}) {
+                const int kc = up.rank[size_t(c)];
+                p.es.push_back(make_entry(up.xfer.data() + up.xfer_off[size_t(c)], kc, kc, true, 1, cu[size_t(c)], kc));
+            }
+            outs.push_back(std::move(p));
+        }
+        pb.emit(outs, kModeSet, 1, 2);
+    }
+    // stage 2: couplings, row-CSR over target nodes (yhat zeroed first)
+    {
+        std::vector<std::vector<SegEntry>> by_target(static_cast<size_t>(nn));
+        for (size_t i = 0; i < bt.adm.size(); ++i) {
+            const int b = bt.adm[i];
+            if (!h.stores(b)) continue;
+            const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
+            const double* S = h.S.data() + h.s_off[i];
+            const int kr = h.row.rank[size_t(r)], kc = h.vbasis().rank[size_t(c)];
+            if (!swap) {
+                by_target[size_t(r)].push_back(make_entry(S, kr, kc, false, 1, cu[size_t(c)], kc));
+                if (h.symmetric && r != c) by_target[size_t(c)].push_back(make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
+            } else {
+                by_target[size_t(c)].push_back(make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
+            }
+        }
+        std::vector<P> outs;
+        for (int v = 0; v < nn; ++v) {
+            if (by_target[size_t(v)].empty()) continue;
+            const int k = down.rank[size_t(v)];
+            outs.push_back(P{k, k, cd[size_t(v)], std::move(by_target[size_t(v)])});
+        }
+        pb.emit(outs, kModeSet, 2, 3, /*zero_yhat=*/true);
+    }
+    // stage 3: downsweep top-down  yhat_c += E_c yhat_v
+    for (int l = 0; l < ct.depth; ++l) {
+        std::vector<P> outs;
+        for (int v : ct.levels[size_t(l)]) {
+            if (ct.is_leaf(v)) continue;
+            const int kv = down.rank[size_t(v)];
+            for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]}) {
+                const int kc = down.rank[size_t(c)];
+                P p{kc, kc, cd[size_t(c)], {}};
+                p.es.push_back(make_entry(down.xfer.data() + down.xfer_off[size_t(c)], kc, kv, false, 2, cd[size_t(v)], kv));
+                outs.push_back(std::move(p));
+            }
+        }
+        pb.emit(outs, kModeAdd, 2, 4);
+    }
+    // stage 3b + 4: leaves  y_t = alpha (U_t yhat_t + sum op(D) X_s) + beta y_t
+    {
+        std::vector<std::vector<SegEntry>> by_leaf(static_cast<size_t>(nn));
+        for (int t : ct.leaves) {
+            const int k = down.rank[size_t(t)], m = int(ct.size(t));
+            by_leaf[size_t(t)].push_back(make_entry(down.leaf.data() + down.leaf_off[size_t(t)], m, k, false, 2, cd[size_t(t)], k));
+        }
+        for (size_t i = 0; i < bt.dense.size(); ++i) {
+            const int b = bt.dense[i];
+            if (!h.stores(b)) continue;
+            const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
+            const double* D = h.D.data() + h.d_off[i];
+            const int mr = int(ct.size(r)), mc = int(ct.size(c));
+            if (!swap) {
+                by_leaf[size_t(r)].push_back(make_entry(D, mr, mc, false, 0, ct.begin[size_t(c)], mc));
+                if (h.symmetric && r != c) by_leaf[size_t(c)].push_back(make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
+            } else {
+                by_leaf[size_t(c)].push_back(make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
+            }
+        }
+        std::vector<P> outs;
+        for (int t : ct.leaves) {
+            const int m = int(ct.size(t));
+            outs.push_back(P{m, m, ct.begin[size_t(t)], std::move(by_leaf[size_t(t)])});
+        }
+        pb.emit(outs, kModeY, 3, 5);
+    }
+    plan->launches = std::move(pb.launches);
+    plan->tasks.upload(pb.tasks);
+    plan->entries.upload(pb.entries);
+    std::vector<int> perm32(ct.perm.begin(), ct.perm.end());
+    plan->perm.upload(perm32);
+    std::vector<int64_t> lb;
+    std::vector<int> lm;
+    for (int t : ct.leaves) {
+        lb.push_back(ct.begin[size_t(t)]);
+        lm.push_back(int(ct.size(t)));
+    }
+    plan->num_leaves = int(lb.size());
+    plan->leaf_begin.upload(lb);
+    plan->leaf_m.upload(lm);
+    H2B_CUDA(cudaDeviceSynchronize());
+    return plan;
+}
+
+std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
+    std::lock_guard<std::mutex> g(h.plan_mu);
+    auto& p = h.plan[transpose ? 1 : 0];
+    if (!p) p = build_plan(h, transpose);
+    return p;
+}
+
+template <int MT, int NB, int WM, int WN, bool VEC, int MODE>
+void launch_one(const SegArgs& a, int ntasks, int64_t b, cudaStream_t s) {
+    constexpr int STAGES = 3;
+    constexpr size_t smem = size_t(STAGES) * (MT * 32 + 32 * NB) * sizeof(double);
+    auto kern = seg_gemm_kernel<MT, NB, WM, WN, STAGES, VEC, MODE>;
+    static bool attr = [&] {
+        H2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        return true;
+    }();
+    (void)attr;
+    dim3 grid(unsigned(ntasks), unsigned((b + NB - 1) / NB));
+    kern<<<grid, 128, smem, s>>>(a);
+    H2B_LAUNCH();
+}
+
+template <int MT, int NB, int WM, int WN>
+void launch_mode(const SegArgs& a, int ntasks, int64_t b, bool vec, int mode, cudaStream_t s) {
+    if (vec) {
+        if (mode == kModeSet) launch_one<MT, NB, WM, WN, true, kModeSet>(a, ntasks, b, s);
+        else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, true, kModeAdd>(a, ntasks, b, s);
+        else launch_one<MT, NB, WM, WN, true, kModeY>(a, ntasks, b, s);
+    } else {
+        if (mode == kModeSet) launch_one<MT, NB, WM, WN, false, kModeSet>(a, ntasks, b, s);
+        else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, false, kModeAdd>(a, ntasks, b, s);
+        else launch_one<MT, NB, WM, WN, false, kModeY>(a, ntasks, b, s);
+    }
+}
+
+void dispatch(const SegArgs& a, int ntasks, int64_t b, int mt, bool vec, int mode, cudaStream_t s) {
+    const int nb = b >= 32 ? 32 : (b > 8 ? 16 : 8);
+    if (mt == 64) {
+        if (nb == 32) launch_mode<64, 32, 4, 1>(a, ntasks, b, vec, mode, s);
+        else if (nb == 16) launch_mode<64, 16, 4, 1>(a, ntasks, b, vec, mode, s);
+        else launch_mode<64, 8, 4, 1>(a, ntasks, b, vec, mode, s);
+    } else {
+        if (nb == 32) launch_mode<32, 32, 2, 2>(a, ntasks, b, vec, mode, s);
+        else if (nb == 16) launch_mode<32, 16, 2, 2>(a, ntasks, b, vec, mode, s);
+        else launch_mode<32, 8, 4, 1>(a, ntasks, b, vec, mode, s);
+    }
+}
+
+}  // namespace
+
+namespace {
+struct EventTimer {
+    std::vector<cudaEvent_t> ev;
+    std::vector<StageRecord>* out = nullptr;
+    cudaStream_t s = nullptr;
+    void mark(cudaStream_t st) {
+        cudaEvent_t e;
+        H2B_CUDA(cudaEventCreate(&e));
+        H2B_CUDA(cudaEventRecord(e, st));
+        ev.push_back(e);
+    }
+    ~EventTimer() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
+                double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
+                EventTimer* timer);
+}  // namespace
+
+void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
+           double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws) {
+    hgemv_impl(h, transpose, user_order, n, b, x, ldx, y, ldy, alpha, beta, stream, ws, nullptr);
+}
+
+void hgemv_timed(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
+                 double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
+                 std::vector<StageRecord>& records) {
+    EventTimer t;
+    std::vector<StageRecord> recs;
+    t.out = &recs;
+    hgemv_impl(h, transpose, user_order, n, b, x, ldx, y, ldy, alpha, beta, stream, ws, &t);
+    H2B_CUDA(cudaStreamSynchronize(stream));
+    for (size_t i = 0; i < recs.size(); ++i) {
+        float ms = 0;
+        H2B_CUDA(cudaEventElapsedTime(&ms, t.ev[2 * i], t.ev[2 * i + 1]));
+        recs[i].ms = ms;
+    }
+    records = std::move(recs);
+}
+
+namespace {
+void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
+                double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
+                EventTimer* timer) {
+    if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
+    if (b < 1) throw std::invalid_argument("matvec: need at least one column");
+    if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
+    auto plan = get_plan(h, transpose);
+    const size_t need_x = size_t(n * b), need_u = size_t(plan->coef_up * b), need_d = size_t(plan->coef_down * b);
+    if (ws.xint.size() < need_x) ws.xint.resize(need_x);
+    if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1));
+    if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1));
+    const int* perm = user_order ? plan->perm.data() : nullptr;
+    if (timer) timer->mark(stream);
+    gather_blocked_kernel<<<plan->num_leaves, 256, 0, stream>>>(x, ldx, perm, plan->leaf_begin.data(), plan->leaf_m.data(), b,
+                                                               ws.xint.data());
+    H2B_LAUNCH();
+    if (timer) {
+        timer->mark(stream);
+        timer->out->push_back({0, 0.f, 0.0, 16.0 * double(n * b)});
+    }
+    for (const LaunchDesc& ld : plan->launches) {
+        if (ld.zero_yhat && need_d) H2B_CUDA(cudaMemsetAsync(ws.yhat.data(), 0, need_d * sizeof(double), stream));
+        const int ntasks = ld.task_end - ld.task_begin;
+        if (ntasks == 0) continue;
+        if (timer) {
+            timer->mark(stream);
+            timer->out->push_back({ld.stage, 0.f, ld.flops_per_col * double(b),
+                                   ld.payload_bytes + 8.0 * (ld.bsrc_per_col + ld.out_per_col) * double(b)});
+        }
+        SegArgs a{};
+        a.tasks = plan->tasks.data() + ld.task_begin;
+        a.entries = plan->entries.data();
+        a.src0 = ws.xint.data();
+        a.src1 = ws.xhat.data();
+        a.src2 = ws.yhat.data();
+        a.out = ld.out == 1 ? ws.xhat.data() : (ld.out == 2 ? ws.yhat.data() : y);
+        a.perm = perm;
+        a.b = b;
+        a.ldy = ldy;
+        a.alpha = alpha;
+        a.beta = beta;
+        const bool vec = ld.vec && (ld.units_even || b % 2 == 0) &&
+                         (reinterpret_cast<uintptr_t>(ws.xint.data()) % 16 == 0);
+        dispatch(a, ntasks, b, ld.mt, vec, ld.mode, stream);
+        if (timer) timer->mark(stream);
+    }
+}
+}  // namespace
+
+int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
+    (void)b;
+    auto plan = get_plan(h, transpose);
+    int c = 1;   // gather
+    for (const LaunchDesc& ld : plan->launches)
+        if (ld.task_end > ld.task_begin) ++c;
+    return c;
+}
+
+}  // namespace h2b

@@ -1,0 +1,147 @@
+"""hgemv parity: the B200 path (through the C ABI) vs the CPU oracle on the
+reference's own fixture (random_h2, test_support.hpp:38-70) and on generated
+kernel matrices. Tolerance: relative Frobenius error <= 1e-12,
+the bound of test_core.cpp:40-53."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_2003_10173_b200 import Admissibility, H2Matrix, build_block_tree, build_cluster_tree
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def rel(a, b):
+    d = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / d if d else np.linalg.norm(a)
+
+
+def pair(pts, leaf, weak, sym, kmax, seed):
+    ref = O.Tree(pts, leaf, 1.0, weak)
+    ora = O.H2.random(ref, sym, kmax, seed)
+    ct = build_cluster_tree(pts, leaf)
+    bt = build_block_tree(ct, ct, 1.0, Admissibility.weak if weak else Admissibility.strong)
+    rr, cr = ora.ranks()
+    m = H2Matrix.from_packed(bt, sym, rr, cr, ora.export())
+    return ora, m, bt
+
+
+TREES = {
+    "1d-weak-96-8": (O.grid1d(96, -1, 1), 8, True),
+    "1d-strong-70-6": (O.grid1d(70, -1, 1), 6, False),
+    "2d-12-16": (O.grid2d(12, 12), 16, False),
+    "rand3d-300-12": (O.gaussian(9, 300, 3), 12, False),
+    "2d-64-64": (O.grid2d(64, 64), 64, False),
+}
+
+
+@pytest.mark.parametrize("tree", list(TREES))
+@pytest.mark.parametrize("sym", [True, False])
+@pytest.mark.parametrize("kmax", [4, 40])
+def test_hgemv_matches_oracle(cuda, tree, sym, kmax):
+    pts, leaf, weak = TREES[tree]
+    kmax = min(kmax, leaf)
+    ora, m, _ = pair(pts, leaf, weak, sym, kmax, seed=2)
+    n = pts.shape[0]
+    for b in (1, 5, 16, 33):
+        x = O.gaussian(100 + b, n, b)
+        for transpose in (False, True):
+            for ordering in (0, 1):
+                y_ref = ora.matvec(x, transpose, ordering)
+                y = m._host(x, transpose, ordering)
+                assert rel(y, y_ref) <= TOL, (tree, sym, b, transpose, ordering, rel(y, y_ref))
+
+
+def test_hgemv_large_ranks_and_leaves(cuda):
+    # ranks and leaf sizes above one 64-row tile exercise the row tiling
+    pts = O.gaussian(21, 2000, 2)
+    ora, m, _ = pair(pts, 150, False, True, 90, seed=5)
+    x = O.gaussian(22, 2000, 40)
+    assert rel(m.matvec(x), ora.matvec(x)) <= TOL
+
+
+def test_device_path_alpha_beta_and_strides(cuda):
+    import torch
+    pts = O.grid2d(40, 40)
+    ora, m, _ = pair(pts, 32, False, True, 8, seed=3)
+    n, b = 1600, 7
+    x = O.gaussian(31, n, b)
+    y0 = O.gaussian(32, n, b)
+    # column-major device tensors with padded leading dimension
+    X = torch.zeros(b, n + 3, dtype=torch.float64, device=cuda)
+    Y = torch.zeros(b, n + 5, dtype=torch.float64, device=cuda)
+    X[:, :n] = torch.from_numpy(x.T.copy())
+    Y[:, :n] = torch.from_numpy(y0.T.copy())
+    xv, yv = X[:, :n].T, Y[:, :n].T
+    m.hgemv(xv, yv, alpha=-0.5, beta=2.0)
+    torch.cuda.synchronize()
+    expect = -0.5 * ora.matvec(x) + 2.0 * y0
+    assert rel(yv.cpu().numpy(), expect) <= TOL
+    assert torch.all(Y[:, n:] == 0)   # padding untouched
+
+
+def test_residual_form(cuda):
+    # y <- op(x) - H x, the HARA residual (construction.hpp:207-211) fused as alpha=-1, beta=1
+    import torch
+    pts = O.grid1d(256, -1, 1)
+    ora, m, _ = pair(pts, 16, True, True, 6, seed=4)
+    x = O.gaussian(41, 256, 16)
+    opx = O.gaussian(42, 256, 16)
+    X = torch.from_numpy(np.asfortranarray(x)).to(cuda).T.contiguous().T
+    Y = torch.from_numpy(np.asfortranarray(opx)).to(cuda).T.contiguous().T
+    m.hgemv(X, Y, alpha=-1.0, beta=1.0)
+    assert rel(Y.cpu().numpy(), opx - ora.matvec(x)) <= TOL
+
+
+def test_zero_and_rank_zero_nodes(cuda):
+    pts = O.grid1d(128, -1, 1)
+    ct = build_cluster_tree(pts, 16)
+    bt = build_block_tree(ct, ct, 1.0, Admissibility.weak)
+    z = H2Matrix.zero(bt, True)
+    x = O.gaussian(1, 128, 3)
+    assert np.all(z.matvec(x) == 0)
+    # ranks 0 on a subset of nodes
+    ref = O.Tree(pts, 16, 1.0, True)
+    ora = O.H2.random(ref, False, 3, 9)
+    rr, cr = ora.ranks()
+    parts = ora.export()
+    m = H2Matrix.from_packed(bt, False, rr, cr, parts)
+    assert rel(m.matvec(x), ora.matvec(x)) <= TOL
+
+
+def test_dimension_errors(cuda):
+    pts = O.grid1d(64)
+    ora, m, _ = pair(pts, 8, True, True, 3, seed=1)
+    with pytest.raises(ValueError):
+        m.matvec(np.zeros((63, 2)))
+    with pytest.raises(ValueError):
+        m.matvec(np.zeros((64, 0)))
+
+
+def test_kernel_matrix_matches_oracle_on_same_payload(cuda):
+    # device-generated Gaussian-kernel H^2 (bench input) downloaded into the oracle
+    pts = O.grid2d(96, 96)
+    ct = build_cluster_tree(pts, 64)
+    bt = build_block_tree(ct, ct, 1.0)
+    m = H2Matrix.kernel(bt, pts, "gaussian", 0.1, 32)
+    ref = O.Tree(pts, 64, 1.0, False)
+    rr, _ = m.ranks()
+    ora = O.H2.from_packed(ref, True, rr, None, m.download())
+    x = O.gaussian(7, pts.shape[0], 32)
+    assert rel(m.matvec(x), ora.matvec(x)) <= TOL
+    assert rel(m.matvec(x[:, :1]), ora.matvec(x[:, :1])) <= TOL
+
+
+@pytest.mark.parametrize("kind,ell", [("gaussian", 0.1), ("exponential", 0.2), ("matern32", 0.1)])
+def test_kernel_matrix_approximates_dense_kernel(cuda, kind, ell):
+    # the Chebyshev-interpolation generator is a faithful kernel approximation
+    pts = O.grid2d(48, 48)
+    ct = build_cluster_tree(pts, 64)
+    bt = build_block_tree(ct, ct, 1.0)
+    m = H2Matrix.kernel(bt, pts, kind, ell, 32)
+    r = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1))
+    K = {"gaussian": np.exp(-(r / ell) ** 2), "exponential": np.exp(-r / ell),
+         "matern32": (1 + np.sqrt(3) * r / ell) * np.exp(-np.sqrt(3) * r / ell)}[kind]
+    x = O.gaussian(8, pts.shape[0], 4)
+    assert rel(m.matvec(x), K @ x) < 1e-3
