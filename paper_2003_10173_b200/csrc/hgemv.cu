@@ -38,54 +38,150 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-// swizzled position of element (r, c) of an R x C column-major tile:
-// XOR of row bits 2..3 with the column's low bits makes the DMMA fragment
-// loads (8 rows x 4 cols per half warp pattern) conflict free
-template <int R>
-__device__ __forceinline__ int swz(int r, int c) {
-    return c * R + (r ^ ((c & 3) << 2));
+// Shared-memory tile formats (FP64, one 32-wide K chunk):
+//  * "mc" (m-contiguous, for A = stored block used as is): element (m, k) at
+//    k*MT + (m ^ ((k & 3) << 2)). The XOR on m bits 2..3 makes the DMMA A
+//    fragment (lane (g, t4) reads (m0 + g, 4 k4 + t4)) bank-conflict free and
+//    keeps the per-lane address linear in k4.
+//  * "kc" (k-contiguous, for A^T and for every B operand): element (k, c) at
+//    c*KP + k with KP = 32 + 4 doubles of padding: conflict free for the
+//    fragments (c0 + g, 4 k4 + t4), again linear in k4.
+// KC = K chunk per pipeline stage (32 or 16); KP = KC + 4 (padded leading dim)
+
+template <int MT>
+__device__ __forceinline__ int mc_pos(int m, int k) {
+    return k * MT + (m ^ ((k & 3) << 2));
 }
 
-// stage an R x C tile of a column-major global block (ld = lda), zero-filling
-// rows >= rv and cols >= cv. 128 threads.
-template <int R, int C, bool VEC>
-__device__ __forceinline__ void load_tile(double* tile, const double* base, int64_t lda, int rv, int cv, int tid) {
+// stage an MT x KC block (m-contiguous in global, column stride lda): rows >= rv
+// or k >= kv are zero-filled
+template <int MT, int KC, int NT, bool VEC>
+__device__ __forceinline__ void load_mc(double* tile, const double* base, int64_t lda, int rv, int kv, int tid) {
     if constexpr (VEC) {
-        constexpr int NP = R * C / 2;
+        constexpr int NP = MT * KC / 2;
 #pragma unroll
-        for (int p0 = 0; p0 < NP; p0 += 128) {
+        for (int p0 = 0; p0 < NP; p0 += NT) {
             const int p = p0 + tid;
-            const int r = (p % (R / 2)) * 2, c = p / (R / 2);
-            const int nb = c < cv ? max(0, min(2, rv - r)) * 8 : 0;
-            cp_async16(tile + swz<R>(r, c), nb ? base + r + c * lda : base, nb);
+            if (NP % NT == 0 || p < NP) {
+                const int m = (p % (MT / 2)) * 2, k = p / (MT / 2);
+                const int nb = k < kv ? max(0, min(2, rv - m)) * 8 : 0;
+                cp_async16(tile + mc_pos<MT>(m, k), nb ? base + m + k * lda : base, nb);
+            }
         }
     } else {
-        constexpr int NE = R * C;
+        constexpr int NE = MT * KC;
 #pragma unroll
-        for (int p0 = 0; p0 < NE; p0 += 128) {
+        for (int p0 = 0; p0 < NE; p0 += NT) {
             const int p = p0 + tid;
-            const int r = p % R, c = p / R;
-            const bool ok = r < rv && c < cv;
-            cp_async8(tile + swz<R>(r, c), ok ? base + r + c * lda : base, ok ? 8 : 0);
+            if (NE % NT == 0 || p < NE) {
+                const int m = p % MT, k = p / MT;
+                const bool ok = m < rv && k < kv;
+                cp_async8(tile + mc_pos<MT>(m, k), ok ? base + m + k * lda : base, ok ? 8 : 0);
+            }
         }
     }
 }
 
-template <int MT, int NB, int WM, int WN, int STAGES, bool VEC, int MODE>
-__global__ void __launch_bounds__(128) seg_gemm_kernel(SegArgs args) {
-    constexpr int KC = 32;
-    constexpr int A_SZ = MT * KC, B_SZ = KC * NB, ST_SZ = A_SZ + B_SZ;
+// stage a KC x C block whose K index is contiguous in global (element (k, c) at
+// base[k + c*ld]) into the padded "kc" format; k >= kv or c >= cv zero-filled
+template <int C, int KC, int NT, bool VEC>
+__device__ __forceinline__ void load_kc(double* tile, const double* base, int64_t ld, int kv, int cv, int tid) {
+    constexpr int KP = KC + 4;
+    if constexpr (VEC) {
+        constexpr int NP = C * KC / 2;
+#pragma unroll
+        for (int p0 = 0; p0 < NP; p0 += NT) {
+            const int p = p0 + tid;
+            if (NP % NT == 0 || p < NP) {
+                const int k = (p % (KC / 2)) * 2, c = p / (KC / 2);
+                const int nb = c < cv ? max(0, min(2, kv - k)) * 8 : 0;
+                cp_async16(tile + c * KP + k, nb ? base + k + c * ld : base, nb);
+            }
+        }
+    } else {
+        constexpr int NE = C * KC;
+#pragma unroll
+        for (int p0 = 0; p0 < NE; p0 += NT) {
+            const int p = p0 + tid;
+            if (NE % NT == 0 || p < NE) {
+                const int k = p % KC, c = p / KC;
+                const bool ok = k < kv && c < cv;
+                cp_async8(tile + c * KP + k, ok ? base + k + c * ld : base, ok ? 8 : 0);
+            }
+        }
+    }
+}
+
+// one K chunk of DMMA work for one warp: acc[TM][TN] += op(A) B over ksteps*4
+// K values; fragments are double buffered in registers so the shared-memory
+// loads of step k4+1 overlap the DMMAs of step k4
+template <int MT, int KC, int TM, int TN, bool TRANS>
+__device__ __forceinline__ void chunk_mma(const double* __restrict__ at, const double* __restrict__ bt,
+                                          double (&acc)[TM][TN][2], const int (&offa)[TM], const int (&offb)[TN],
+                                          int ksteps) {
+    constexpr int ASTEP = TRANS ? 4 : 4 * MT;
+    double a[2][TM], b[2][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) a[0][i] = at[offa[i]];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) b[0][j] = bt[offb[j]];
+    if (ksteps == KC / 4) {
+#pragma unroll
+        for (int k4 = 0; k4 < KC / 4; ++k4) {
+            const int cur = k4 & 1, nxt = cur ^ 1;
+            if (k4 + 1 < KC / 4) {
+#pragma unroll
+                for (int i = 0; i < TM; ++i) a[nxt][i] = at[offa[i] + (k4 + 1) * ASTEP];
+#pragma unroll
+                for (int j = 0; j < TN; ++j) b[nxt][j] = bt[offb[j] + (k4 + 1) * 4];
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+        }
+    } else {
+        for (int k4 = 0; k4 < ksteps; ++k4) {
+            double aa[TM], bb[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) aa[i] = at[offa[i] + k4 * ASTEP];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bb[j] = bt[offb[j] + k4 * 4];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], aa[i], bb[j]);
+        }
+    }
+}
+
+template <int MT, int NB, int WM, int WN, int STAGES, int KC, bool VEC, int MODE>
+__global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int KP = KC + 4;
+    constexpr int A_SZ = MT * KP, B_SZ = NB * KP, ST_SZ = A_SZ + B_SZ;
     constexpr int TM = MT / (WM * 8), TN = NB / (WN * 8);
-    static_assert(WM * WN == 4 && TM >= 1 && TN >= 1, "warp layout");
+    static_assert(TM >= 1 && TN >= 1 && MT % 16 == 0, "warp layout");
     extern __shared__ __align__(16) double smem[];
 
     const SegTask tk = args.tasks[blockIdx.x];
+    const int nsteps = KC == 32 ? tk.nsteps : tk.nsteps16;
     const int j0 = blockIdx.y * NB;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int wm = warp % WM, wn = warp / WM;
     const int g = lane >> 2, t4 = lane & 3;
     const int rows_here = min(MT, tk.rows - tk.row0);
     const int ncols = int(min(int64_t(NB), args.b - j0));
+
+    int offa_n[TM], offa_t[TM], offb[TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int m = (wm * TM + i) * 8 + g;
+        offa_n[i] = t4 * MT + (m ^ (t4 << 2));
+        offa_t[i] = m * KP + t4;
+    }
+#pragma unroll
+    for (int j = 0; j < TN; ++j) offb[j] = ((wn * TN + j) * 8 + g) * KP + t4;
 
     double acc[TM][TN][2];
 #pragma unroll
@@ -99,10 +195,10 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(SegArgs args) {
         double* at = smem + stage * ST_SZ;
         double* bt = at + A_SZ;
         const int krem = min(KC, e.k - pk);
-        if (!e.trans) load_tile<MT, KC, VEC>(at, e.A + tk.row0 + int64_t(pk) * e.lda, e.lda, rows_here, krem, tid);
-        else load_tile<KC, MT, VEC>(at, e.A + pk + int64_t(tk.row0) * e.lda, e.lda, krem, rows_here, tid);
+        if (!e.trans) load_mc<MT, KC, NT, VEC>(at, e.A + tk.row0 + int64_t(pk) * e.lda, e.lda, rows_here, krem, tid);
+        else load_kc<MT, KC, NT, VEC>(at, e.A + pk + int64_t(tk.row0) * e.lda, e.lda, krem, rows_here, tid);
         const double* sb = e.src == 0 ? args.src0 : (e.src == 1 ? args.src1 : args.src2);
-        load_tile<KC, NB, VEC>(bt, sb + e.b_unit * args.b + pk + int64_t(j0) * e.ldb, e.ldb, krem, ncols, tid);
+        load_kc<NB, KC, NT, VEC>(bt, sb + e.b_unit * args.b + pk + int64_t(j0) * e.ldb, e.ldb, krem, ncols, tid);
         pk += KC;
         if (pk >= e.k) {
             ++pe;
@@ -112,18 +208,18 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(SegArgs args) {
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < tk.nsteps) issue(s);
+        if (s < nsteps) issue(s);
         cp_async_commit();
     }
     int ce = tk.e_begin, ck = 0;   // consumer cursor
-    for (int s = 0; s < tk.nsteps; ++s) {
+    for (int s = 0; s < nsteps; ++s) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
-        if (s + STAGES - 1 < tk.nsteps) issue((s + STAGES - 1) % STAGES);
+        if (s + STAGES - 1 < nsteps) issue((s + STAGES - 1) % STAGES);
         cp_async_commit();
         const SegEntry& ec = args.entries[ce];
         const bool trans = ec.trans;
-        const int kc_steps = (min(KC, ec.k - ck) + 3) >> 2;
+        const int ksteps = (min(KC, ec.k - ck) + 3) >> 2;
         ck += KC;
         if (ck >= ec.k) {
             ++ce;
@@ -131,25 +227,8 @@ __global__ void __launch_bounds__(128) seg_gemm_kernel(SegArgs args) {
         }
         const double* at = smem + (s % STAGES) * ST_SZ;
         const double* bt = at + A_SZ;
-#pragma unroll 4
-        for (int k4 = 0; k4 < kc_steps; ++k4) {
-            const int k = k4 * 4 + t4;
-            double a[TM], b[TN];
-#pragma unroll
-            for (int i = 0; i < TM; ++i) {
-                const int m = (wm * TM + i) * 8 + g;
-                a[i] = trans ? at[swz<KC>(k, m)] : at[swz<MT>(m, k)];
-            }
-#pragma unroll
-            for (int j = 0; j < TN; ++j) {
-                const int nn = (wn * TN + j) * 8 + g;
-                b[j] = bt[swz<KC>(k, nn)];
-            }
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-                for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
+        if (trans) chunk_mma<MT, KC, TM, TN, true>(at, bt, acc, offa_t, offb, ksteps);
+        else chunk_mma<MT, KC, TM, TN, false>(at, bt, acc, offa_n, offb, ksteps);
     }
     cp_async_wait<0>();
 
@@ -257,11 +336,12 @@ struct PlanBuilder {
         for (auto& p : outs) {
             if (p.rows <= 0) continue;
             const int e0 = int(entries.size());
-            int nsteps = 0;
+            int nsteps = 0, nsteps16 = 0;
             for (auto& e : p.es) {
                 if (e.k <= 0) continue;
                 entries.push_back(e);
                 nsteps += (e.k + 31) / 32;
+                nsteps16 += (e.k + 15) / 16;
                 const int64_t aoff = reinterpret_cast<uintptr_t>(e.A) / sizeof(double);
                 vec = vec && (aoff % 2 == 0) && (e.lda % 2 == 0) && (e.ldb % 2 == 0);
                 ue = ue && (e.b_unit % 2 == 0);
@@ -272,6 +352,7 @@ struct PlanBuilder {
                 tk.e_begin = e0;
                 tk.e_end = e1;
                 tk.nsteps = nsteps;
+                tk.nsteps16 = nsteps16;
                 tk.rows = p.rows;
                 tk.row0 = r0;
                 tk.out_ld = p.out_ld;
@@ -446,42 +527,63 @@ std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
     return p;
 }
 
-template <int MT, int NB, int WM, int WN, bool VEC, int MODE>
+template <int MT, int NB, int WM, int WN, int STAGES, int KC, bool VEC, int MODE>
 void launch_one(const SegArgs& a, int ntasks, int64_t b, cudaStream_t s) {
-    constexpr int STAGES = 3;
-    constexpr size_t smem = size_t(STAGES) * (MT * 32 + 32 * NB) * sizeof(double);
-    auto kern = seg_gemm_kernel<MT, NB, WM, WN, STAGES, VEC, MODE>;
+    constexpr size_t smem = size_t(STAGES) * (MT + NB) * (KC + 4) * sizeof(double);
+    auto kern = seg_gemm_kernel<MT, NB, WM, WN, STAGES, KC, VEC, MODE>;
     static bool attr = [&] {
         H2B_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         return true;
     }();
     (void)attr;
     dim3 grid(unsigned(ntasks), unsigned((b + NB - 1) / NB));
-    kern<<<grid, 128, smem, s>>>(a);
+    kern<<<grid, WM * WN * 32, smem, s>>>(a);
     H2B_LAUNCH();
 }
 
-template <int MT, int NB, int WM, int WN>
+template <int MT, int NB, int WM, int WN, int STAGES = 2, int KC = 32>
 void launch_mode(const SegArgs& a, int ntasks, int64_t b, bool vec, int mode, cudaStream_t s) {
     if (vec) {
-        if (mode == kModeSet) launch_one<MT, NB, WM, WN, true, kModeSet>(a, ntasks, b, s);
-        else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, true, kModeAdd>(a, ntasks, b, s);
-        else launch_one<MT, NB, WM, WN, true, kModeY>(a, ntasks, b, s);
+        if (mode == kModeSet) launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeSet>(a, ntasks, b, s);
+        else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeAdd>(a, ntasks, b, s);
+        else launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeY>(a, ntasks, b, s);
     } else {
-        if (mode == kModeSet) launch_one<MT, NB, WM, WN, false, kModeSet>(a, ntasks, b, s);
-        else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, false, kModeAdd>(a, ntasks, b, s);
-        else launch_one<MT, NB, WM, WN, false, kModeY>(a, ntasks, b, s);
+        if (mode == kModeSet) launch_one<MT, NB, WM, WN, STAGES, KC, false, kModeSet>(a, ntasks, b, s);
+        else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, STAGES, KC, false, kModeAdd>(a, ntasks, b, s);
+        else launch_one<MT, NB, WM, WN, STAGES, KC, false, kModeY>(a, ntasks, b, s);
     }
+}
+
+// tile-shape variants of the b >= 32 instances (selected by h2b_tune; 0 = default)
+int g_tune[2] = {0, 0};
+
+template <int MT, int NB, int WM, int WN, int STAGES, int KC = 32>
+void launch_vec_mode(const SegArgs& a, int ntasks, int64_t b, int mode, cudaStream_t s) {
+    if (mode == kModeSet) launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeSet>(a, ntasks, b, s);
+    else if (mode == kModeAdd) launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeAdd>(a, ntasks, b, s);
+    else launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeY>(a, ntasks, b, s);
 }
 
 void dispatch(const SegArgs& a, int ntasks, int64_t b, int mt, bool vec, int mode, cudaStream_t s) {
     const int nb = b >= 32 ? 32 : (b > 8 ? 16 : 8);
     if (mt == 64) {
-        if (nb == 32) launch_mode<64, 32, 4, 1>(a, ntasks, b, vec, mode, s);
+        if (nb == 32) {
+            if (vec) switch (g_tune[0]) {
+                case 1: return launch_vec_mode<64, 32, 2, 2, 2, 32>(a, ntasks, b, mode, s);
+                default: break;
+            }
+            launch_mode<64, 32, 4, 1>(a, ntasks, b, vec, mode, s);
+        }
         else if (nb == 16) launch_mode<64, 16, 4, 1>(a, ntasks, b, vec, mode, s);
         else launch_mode<64, 8, 4, 1>(a, ntasks, b, vec, mode, s);
     } else {
-        if (nb == 32) launch_mode<32, 32, 2, 2>(a, ntasks, b, vec, mode, s);
+        if (nb == 32) {
+            if (vec) switch (g_tune[1]) {
+                case 1: return launch_vec_mode<32, 32, 2, 2, 3, 32>(a, ntasks, b, mode, s);
+                default: break;
+            }
+            launch_mode<32, 32, 2, 2>(a, ntasks, b, vec, mode, s);
+        }
         else if (nb == 16) launch_mode<32, 16, 2, 2>(a, ntasks, b, vec, mode, s);
         else launch_mode<32, 8, 4, 1>(a, ntasks, b, vec, mode, s);
     }
@@ -590,3 +692,10 @@ int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
 }
 
 }  // namespace h2b
+
+// tuning hook (not part of the public ABI): select a tile-shape variant
+extern "C" int h2b_tune(int which, int value) {
+    if (which < 0 || which > 1) return -1;
+    h2b::g_tune[which] = value;
+    return 0;
+}

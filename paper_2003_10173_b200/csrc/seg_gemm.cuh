@@ -19,6 +19,7 @@ namespace h2b {
 struct SegTask {
     int e_begin, e_end;   // entry range
     int nsteps;           // sum over entries of ceil(k / 32)
+    int nsteps16;         // sum over entries of ceil(k / 16)
     int rows;             // total output rows of this output block
     int row0;             // first output row handled by this task (row tiling)
     int out_ld;           // leading dimension of the output block (coefficient outputs)
