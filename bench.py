@@ -231,7 +231,7 @@ def run_b200(args, cfg, world, rank, local, dist):
         achieved = dom["gbytes"] / (dom["ms"] / 1e3)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "peak_source": hbm_src}
-    roof.update({"kernel": "seg_gemm_kernel<64,NB,..,kModeY> (leaf expansion + dense near-field)",
+    roof.update({"kernel": "seg_gemm_kernel<64,32,4,1,2,32,VEC,kModeY> (leaf expansion + dense near-field)",
                  "share_of_step": dom["ms"] / sum(s["ms"] for s in stages.values()),
                  "traffic": args.traffic, "algorithmic_gflop": dom["gflop"], "algorithmic_gbytes": dom["gbytes"],
                  "ms": dom["ms"]})
