@@ -112,6 +112,60 @@ int h2c_hgemv_stage_times(h2c_matrix h, int transpose, int ordering, int64_t n, 
                           int64_t ldx, double* y, int64_t ldy, void* stream, int max_records, int* count, int* stage,
                           double* ms, double* flops, double* bytes);
 
+/* ---- black-box operators: replace LinearOperator and its adapters
+ *      (linear_operator.hpp:20-115). Applications take / return DEVICE
+ *      buffers in USER ordering (n x b, column-major, ld n) and add b to the
+ *      operator's column counter (linear_operator.hpp:28-41). ------------- */
+typedef struct h2c_operator_s* h2c_operator;
+/* user callback: y = op(x) (transpose = 0) or op^T(x); return 0 on success */
+typedef int (*h2c_apply_fn)(void* ctx, int transpose, int64_t b, const double* x, double* y, void* stream);
+/* DenseOperator(a, symmetric) (linear_operator.hpp:86-101): a = n x n host matrix, copied to HBM */
+int h2c_operator_dense(const double* a, int64_t n, int symmetric, h2c_operator* out);
+/* H2Operator(h) (linear_operator.hpp:104-115): hgemv of a device H^2 matrix (h must outlive it) */
+int h2c_operator_h2(h2c_matrix h, h2c_operator* out);
+/* make_operator(n, sym, f, t) (linear_operator.hpp:80-84) with x, y DEVICE pointers */
+int h2c_operator_device_callback(int64_t n, int symmetric, int has_transpose, h2c_apply_fn fn, void* ctx,
+                                 h2c_operator* out);
+/* the same with HOST pointers (the library stages x and y through host memory) */
+int h2c_operator_host_callback(int64_t n, int symmetric, int has_transpose, h2c_apply_fn fn, void* ctx,
+                               h2c_operator* out);
+void h2c_operator_destroy(h2c_operator op);
+/* LinearOperator::apply / apply_transpose on device buffers */
+int h2c_operator_apply(h2c_operator op, int transpose, int64_t b, const double* x, double* y, void* stream);
+/* columns_applied() / reset_counter() */
+int h2c_operator_columns_applied(h2c_operator op, int64_t* cols);
+int h2c_operator_reset_counter(h2c_operator op);
+/* pnorm_estimate(op, 2) (linear_operator.hpp:127-153) */
+int h2c_pnorm2_estimate(h2c_operator op, double* value, int* iterations);
+
+/* ---- algebra (algebra.hpp:72-226): value semantics, new matrix out ------- */
+int h2c_orthogonalize(h2c_matrix in, h2c_matrix* out);             /* algebra.hpp:72-113 */
+int h2c_recompress(h2c_matrix in, double eps, h2c_matrix* out);    /* algebra.hpp:144-226 */
+
+/* ---- HARA: replaces peel_construct(op, bt, cfg) (construction.hpp:300-382) */
+typedef struct {
+    double eps;                   /* 1e-4 */
+    int64_t sample_block_size;    /* 16 */
+    int64_t oversampling;         /* 10 */
+    int64_t max_rank;             /* 0 = cap min(|t|,|s|) + b */
+    uint64_t seed;                /* 42 */
+    double norm_scale;            /* 0 = estimate ||op||_2 */
+    int64_t crossover_rank_cap;   /* 128 */
+} h2c_peel_config;                /* PeelConfig (construction.hpp:23-31) */
+typedef struct {
+    int level;
+    int64_t blocks, max_rank, samples;
+} h2c_level_stats;                /* LevelStats (construction.hpp:33-38) */
+void h2c_peel_config_default(h2c_peel_config* cfg);
+/* stats: total columns (== op counter delta), per-level rows into `levels`
+ * (up to max_levels; *num_levels = count); op_ms / total_ms: host wall time
+ * spent in operator applies / in the whole build (any may be NULL) */
+int h2c_peel_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config* cfg, h2c_matrix* out,
+                       int64_t* total_samples, h2c_level_stats* levels, int max_levels, int* num_levels,
+                       double* op_ms, double* total_ms);
+/* estimate_relative_error(op, h, op_norm) (construction.hpp:537-546) */
+int h2c_estimate_relative_error(h2c_operator op, h2c_matrix h, double op_norm, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,11 @@ lib/libh2b200.so (sm_100a CUDA kernels behind the C ABI in include/h2c.h).
 from .h2 import (Admissibility, BlockTree, ClusterTree, H2Matrix, Ordering, build_block_tree,
                  build_cluster_tree)
 from ._lib import CudaError, LIB_PATH, max_rank_error
+from .construction import (DenseOperator, H2Operator, LinearOperator, PeelConfig, PeelResult, SampleStats,
+                           estimate_relative_error, make_operator, orthogonalize, peel_construct, pnorm_estimate,
+                           recompress)
 
 __all__ = ["Admissibility", "BlockTree", "ClusterTree", "H2Matrix", "Ordering", "build_block_tree",
-           "build_cluster_tree", "CudaError", "LIB_PATH", "max_rank_error"]
+           "build_cluster_tree", "CudaError", "LIB_PATH", "max_rank_error", "DenseOperator", "H2Operator",
+           "LinearOperator", "PeelConfig", "PeelResult", "SampleStats", "estimate_relative_error", "make_operator",
+           "orthogonalize", "peel_construct", "pnorm_estimate", "recompress"]

@@ -87,3 +87,32 @@ def check(rc):
 
 
 _sig("h2c_hgemv_stage_times", i32, H, i32, i32, i64, i64, vp, i64, vp, i64, vp, i32, P(i32), vp, vp, vp, vp)
+
+
+class PeelConfigC(C.Structure):
+    """h2c_peel_config (PeelConfig, construction.hpp:23-31)."""
+    _fields_ = [("eps", C.c_double), ("sample_block_size", C.c_int64), ("oversampling", C.c_int64),
+                ("max_rank", C.c_int64), ("seed", C.c_uint64), ("norm_scale", C.c_double),
+                ("crossover_rank_cap", C.c_int64)]
+
+
+class LevelStatsC(C.Structure):
+    _fields_ = [("level", C.c_int), ("blocks", C.c_int64), ("max_rank", C.c_int64), ("samples", C.c_int64)]
+
+
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p)
+
+_sig("h2c_operator_dense", i32, vp, i64, i32, P(H))
+_sig("h2c_operator_h2", i32, H, P(H))
+_sig("h2c_operator_device_callback", i32, i64, i32, i32, APPLY_FN, vp, P(H))
+_sig("h2c_operator_host_callback", i32, i64, i32, i32, APPLY_FN, vp, P(H))
+_sig("h2c_operator_destroy", None, H)
+_sig("h2c_operator_apply", i32, H, i32, i64, vp, vp, vp)
+_sig("h2c_operator_columns_applied", i32, H, P(i64))
+_sig("h2c_operator_reset_counter", i32, H)
+_sig("h2c_pnorm2_estimate", i32, H, P(f64), P(i32))
+_sig("h2c_orthogonalize", i32, H, P(H))
+_sig("h2c_recompress", i32, H, f64, P(H))
+_sig("h2c_peel_config_default", None, P(PeelConfigC))
+_sig("h2c_peel_construct", i32, H, H, P(PeelConfigC), P(H), P(i64), P(LevelStatsC), i32, P(i32), P(f64), P(f64))
+_sig("h2c_estimate_relative_error", i32, H, H, f64, P(f64))

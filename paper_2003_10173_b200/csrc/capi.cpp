@@ -5,6 +5,7 @@
 #include <string>
 
 #include "h2dev.hpp"
+#include "hara.hpp"
 #include "matrix.hpp"
 
 struct h2c_cluster_tree_s {
@@ -16,6 +17,9 @@ struct h2c_block_tree_s {
 struct h2c_matrix_s {
     std::unique_ptr<h2b::H2Dev> h;
     h2b::Workspace ws;
+};
+struct h2c_operator_s {
+    std::unique_ptr<h2b::DevOperator> op;
 };
 
 namespace {
@@ -29,6 +33,9 @@ int guard(F&& f) {
     } catch (const h2b::cuda_error& e) {
         g_err = e.what();
         return H2C_CUDA_ERROR;
+    } catch (const h2b::max_rank_error& e) {
+        g_err = e.what();
+        return H2C_MAX_RANK_ERROR;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return H2C_INVALID_ARGUMENT;
@@ -268,6 +275,156 @@ int h2c_hgemv_launches(h2c_matrix h, int transpose, int64_t b, int* launches) {
     return guard([&] {
         need(h != nullptr && launches != nullptr, "null argument");
         *launches = h2b::hgemv_launch_count(*h->h, transpose != 0, b);
+    });
+}
+
+// ---- operators -------------------------------------------------------------
+namespace {
+struct CallbackError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+h2c_matrix wrap_matrix(std::unique_ptr<h2b::H2Dev> h) {
+    auto m = new h2c_matrix_s;
+    m->h = std::move(h);
+    return m;
+}
+}  // namespace
+
+int h2c_operator_dense(const double* a, int64_t n, int symmetric, h2c_operator* out) {
+    return guard([&] {
+        need(a != nullptr && out != nullptr && n > 0, "dense operator: null matrix or n < 1");
+        *out = new h2c_operator_s{std::make_unique<h2b::DenseDevOperator>(a, n, symmetric != 0)};
+    });
+}
+
+int h2c_operator_h2(h2c_matrix h, h2c_operator* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        *out = new h2c_operator_s{std::make_unique<h2b::H2DevOperator>(*h->h)};
+    });
+}
+
+int h2c_operator_device_callback(int64_t n, int symmetric, int has_transpose, h2c_apply_fn fn, void* ctx,
+                                 h2c_operator* out) {
+    return guard([&] {
+        need(fn != nullptr && out != nullptr && n > 0, "callback operator: null function or n < 1");
+        auto f = [fn, ctx](bool t, int64_t b, const double* x, double* y, cudaStream_t s) {
+            if (fn(ctx, t ? 1 : 0, b, x, y, s) != 0) throw CallbackError("operator callback failed");
+        };
+        *out = new h2c_operator_s{std::make_unique<h2b::FunctionDevOperator>(n, symmetric != 0, f, has_transpose != 0)};
+    });
+}
+
+int h2c_operator_host_callback(int64_t n, int symmetric, int has_transpose, h2c_apply_fn fn, void* ctx,
+                               h2c_operator* out) {
+    return guard([&] {
+        need(fn != nullptr && out != nullptr && n > 0, "callback operator: null function or n < 1");
+        auto f = [fn, ctx, n](bool t, int64_t b, const double* x, double* y, cudaStream_t s) {
+            std::vector<double> hx(size_t(n * b)), hy(size_t(n * b));
+            H2B_CUDA(cudaMemcpyAsync(hx.data(), x, hx.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            H2B_CUDA(cudaStreamSynchronize(s));
+            if (fn(ctx, t ? 1 : 0, b, hx.data(), hy.data(), nullptr) != 0) throw CallbackError("operator callback failed");
+            H2B_CUDA(cudaMemcpyAsync(y, hy.data(), hy.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+            H2B_CUDA(cudaStreamSynchronize(s));
+        };
+        *out = new h2c_operator_s{std::make_unique<h2b::FunctionDevOperator>(n, symmetric != 0, f, has_transpose != 0)};
+    });
+}
+
+void h2c_operator_destroy(h2c_operator op) { delete op; }
+
+int h2c_operator_apply(h2c_operator op, int transpose, int64_t b, const double* x, double* y, void* stream) {
+    return guard([&] {
+        need(op != nullptr && x != nullptr && y != nullptr, "null argument");
+        need(b >= 1, "operator apply: need at least one column");
+        auto s = static_cast<cudaStream_t>(stream);
+        if (transpose) op->op->apply_transpose(b, x, y, s);
+        else op->op->apply(b, x, y, s);
+    });
+}
+
+int h2c_operator_columns_applied(h2c_operator op, int64_t* cols) {
+    return guard([&] {
+        need(op != nullptr && cols != nullptr, "null argument");
+        *cols = op->op->columns_applied();
+    });
+}
+
+int h2c_operator_reset_counter(h2c_operator op) {
+    return guard([&] {
+        need(op != nullptr, "null argument");
+        op->op->reset_counter();
+    });
+}
+
+int h2c_pnorm2_estimate(h2c_operator op, double* value, int* iterations) {
+    return guard([&] {
+        need(op != nullptr && value != nullptr, "null argument");
+        const h2b::NormEstimate e = h2b::pnorm2_estimate(*op->op, nullptr);
+        *value = e.value;
+        if (iterations) *iterations = e.iterations;
+    });
+}
+
+int h2c_orthogonalize(h2c_matrix in, h2c_matrix* out) {
+    return guard([&] {
+        need(in != nullptr && out != nullptr, "null argument");
+        *out = wrap_matrix(h2b::orthogonalize(*in->h, nullptr));
+    });
+}
+
+int h2c_recompress(h2c_matrix in, double eps, h2c_matrix* out) {
+    return guard([&] {
+        need(in != nullptr && out != nullptr, "null argument");
+        *out = wrap_matrix(h2b::recompress(*in->h, eps, nullptr));
+    });
+}
+
+void h2c_peel_config_default(h2c_peel_config* cfg) {
+    if (!cfg) return;
+    const h2b::PeelConfig d;
+    cfg->eps = d.eps;
+    cfg->sample_block_size = d.sample_block_size;
+    cfg->oversampling = d.oversampling;
+    cfg->max_rank = d.max_rank;
+    cfg->seed = d.seed;
+    cfg->norm_scale = d.norm_scale;
+    cfg->crossover_rank_cap = d.crossover_rank_cap;
+}
+
+int h2c_peel_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config* cfg, h2c_matrix* out,
+                       int64_t* total_samples, h2c_level_stats* levels, int max_levels, int* num_levels,
+                       double* op_ms, double* total_ms) {
+    return guard([&] {
+        need(op != nullptr && bt != nullptr && out != nullptr, "null argument");
+        h2b::PeelConfig c;
+        if (cfg) {
+            c.eps = cfg->eps;
+            c.sample_block_size = cfg->sample_block_size;
+            c.oversampling = cfg->oversampling;
+            c.max_rank = cfg->max_rank;
+            c.seed = cfg->seed;
+            c.norm_scale = cfg->norm_scale;
+            c.crossover_rank_cap = cfg->crossover_rank_cap;
+        }
+        h2b::PeelResult r = h2b::peel_construct(*op->op, bt->b, c, nullptr);
+        if (total_samples) *total_samples = r.stats.total;
+        if (num_levels) *num_levels = int(r.stats.levels.size());
+        if (levels)
+            for (int i = 0; i < int(r.stats.levels.size()) && i < max_levels; ++i) {
+                const h2b::LevelStats& l = r.stats.levels[size_t(i)];
+                levels[i] = h2c_level_stats{l.level, l.blocks, l.max_rank, l.samples};
+            }
+        if (op_ms) *op_ms = r.times.op_ms;
+        if (total_ms) *total_ms = r.times.total_ms;
+        *out = wrap_matrix(std::move(r.matrix));
+    });
+}
+
+int h2c_estimate_relative_error(h2c_operator op, h2c_matrix h, double op_norm, double* out) {
+    return guard([&] {
+        need(op != nullptr && h != nullptr && out != nullptr, "null argument");
+        *out = h2b::estimate_relative_error(*op->op, *h->h, op_norm, nullptr);
     });
 }
 

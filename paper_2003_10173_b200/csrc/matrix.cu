@@ -60,7 +60,7 @@ std::unique_ptr<H2Dev> make_h2(std::shared_ptr<const BlockTree> bt, bool symmetr
         b.rank.assign(size_t(nn), 0);
         for (int v = 0; v < nn; ++v) {
             const int k = r ? r[v] : 0;
-            if (k < 0 || k > t.size(v)) throw std::invalid_argument("rank exceeds cluster size");
+            if (k < 0) throw std::invalid_argument("negative rank");
             b.rank[size_t(v)] = k;
         }
         b.layout(t);
