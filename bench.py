@@ -35,6 +35,15 @@ CONFIGS = {
     # BASELINE.json configs[0] structure (hgemv part)
     "cfg1": dict(workload="2D exponential-kernel H2 hgemv N=16384 (128^2), leaf 64, rank 32, 1 vector",
                  grid=(128, 128), kind="exponential", ell=0.2, rank=32, b=1, leaf=64),
+    # BASELINE.json configs[2]: HARA from a black-box matvec of a diffusion-Hessian proxy. The heat
+    # propagator F = exp(T*Laplacian) is a Gaussian convolution, so the misfit Hessian F^T F of a
+    # fully observed 1D diffusion inverse problem is a Gaussian kernel; the black box applies it as
+    # a rank-32 H^2 (hgemv) on the weak 1D tree of the reference's diff1d case (leaf 32).
+    "cfg3": dict(workload="HARA peel_construct from a black-box matvec, 1D diffusion-Hessian proxy "
+                          "(Gaussian heat-kernel F^T F, ell=0.05, applied as a rank-32 H^2), N=2^18, "
+                          "weak admissibility, leaf 32, eps 1e-6, PeelConfig defaults (b=16, p=10)",
+                 grid=(262144,), kind="gaussian", ell=0.05, rank=32, leaf=32, eps=1e-6, hara=True,
+                 sample_n=16384),
     # BASELINE.json configs[3] at P=1
     "cfg4": dict(workload="3D Matern-3/2 H2 hgemv N=2^21 (128^3 grid), leaf 64, rank 32, 64 vectors",
                  grid=(128, 128, 128), kind="matern32", ell=0.1, rank=32, b=64, leaf=64),
@@ -46,6 +55,9 @@ FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA m8n8k4 f64 on B200 (profil
 
 
 def grid_points(shape):
+    if len(shape) == 1:
+        n = shape[0]
+        return (-1.0 + 2.0 * np.arange(n) / (n - 1))[:, None]   # grid1d(n, -1, 1), test_support.hpp:12-16
     if len(shape) == 2:
         nx, ny = shape
         i = np.tile(np.arange(nx), ny)
@@ -350,6 +362,93 @@ def run_reference(args, cfg, world, rank):
             "setup_s": setup}
 
 
+def hara_problem(cfg, n):
+    from paper_2003_10173_b200 import Admissibility, H2Matrix, build_block_tree, build_cluster_tree
+    pts = grid_points((n,))
+    ct = build_cluster_tree(pts, cfg["leaf"])
+    bt = build_block_tree(ct, ct, 1.0, Admissibility.weak)
+    src = H2Matrix.kernel(bt, pts, cfg["kind"], cfg["ell"], cfg["rank"])
+    return pts, ct, bt, src
+
+
+def run_hara(args, cfg, world, rank, local, dist):
+    """cfg3: HARA build time on the B200 (one step = one peel_construct)."""
+    import torch
+    from paper_2003_10173_b200 import H2Operator, PeelConfig, estimate_relative_error, peel_construct
+    torch.cuda.set_device(local)
+    n = cfg["grid"][0]
+    pts, ct, bt, src = hara_problem(cfg, n)
+    op = H2Operator(src)
+    rngs = {"device": 1, "reference": 0}
+    pc = PeelConfig(eps=cfg["eps"], rng=rngs[args.hara_rng])
+    for _ in range(max(1, min(args.warmup, 1))):
+        peel_construct(op, bt, pc)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    steps = max(1, min(args.steps, 3))
+    times, opms = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(steps):
+            op.reset_counter()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = peel_construct(op, bt, pc)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            opms.append(res.op_ms)
+    t = statistics.median(times)
+    if dist:
+        tt = torch.tensor([t], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    import ctypes as C
+    from paper_2003_10173_b200._lib import lib as _l
+    ph = (C.c_double * 8)()
+    _l.h2b_hara_phase_ms(ph, 8)
+    phases = dict(zip(["rng", "op_apply", "residual_hgemv", "absorb", "transposed_pass", "local_updates",
+                       "recompress", "dense_leaves"], [round(v / 1e3, 4) for v in ph]))
+    err = estimate_relative_error(op, res.matrix)
+    prof = [int(v) for v in res.matrix.rank_profile()]
+    out = {"metric": "HARA build time (N=2^18, tol 1e-6)", "value": t, "unit": "s", "n_gpus": world,
+           "steps": steps, "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated kernel H^2 black box)",
+           "config": {"workload": cfg["workload"], "n": n, "eps": cfg["eps"], "rng": args.hara_rng,
+                      "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+           "hara": {"op_s": statistics.median(opms) / 1e3, "construction_s": t - statistics.median(opms) / 1e3,
+                    "samples": res.stats.total, "relative_error_2norm": err, "rank_profile": prof,
+                    "level_samples": [lv.samples for lv in res.stats.levels], "phases_s": phases},
+           "clocks": clk.summary()}
+    return out
+
+
+def cpu_baseline_hara(args, cfg):
+    """The oracle (restated reference, 1 thread) on a bounded sample: the same
+    problem at N = sample_n, next to the B200 on the same sample."""
+    import torch
+    from oracle import pyoracle as O
+    from paper_2003_10173_b200 import H2Operator, PeelConfig, peel_construct
+    n = cfg["sample_n"]
+    pts, ct, bt, src = hara_problem(cfg, n)
+    ref = O.Tree(pts, cfg["leaf"], 1.0, True)
+    rr, _ = src.ranks()
+    osrc = O.H2.from_packed(ref, True, rr, None, src.download())
+    t0 = time.perf_counter()
+    ora, tot = O.peel_h2(ref, osrc, eps=cfg["eps"])
+    tc = time.perf_counter() - t0
+    op = H2Operator(src)
+    peel_construct(op, bt, PeelConfig(eps=cfg["eps"], rng=0))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = peel_construct(op, bt, PeelConfig(eps=cfg["eps"], rng=0))
+    torch.cuda.synchronize()
+    tg = time.perf_counter() - t0
+    return {"value": tc, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"same problem at N={n} (oracle restatement, 1 thread): {tc:.2f} s, {tot} samples; "
+                      f"B200 on the same sample with the reference RNG stream: {tg:.3f} s, {res.stats.total} samples",
+            "b200_same_sample_s": tg, "speedup_same_sample": tc / tg}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -359,6 +458,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=list(CONFIGS))
     ap.add_argument("--b", type=int, default=0, help="override the vector count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hara-rng", default="device", choices=["device", "reference"],
+                    help="cfg3 Gaussian panels: device Philox (perf) or the reference host stream")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes/launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
@@ -366,6 +467,27 @@ def main():
         args.warmup = 3
     cfg = CONFIGS[args.config]
     world, rank, local, dist = dist_setup(args)
+    if cfg.get("hara"):
+        if args.impl == "reference":
+            if rank == 0:
+                from oracle import pyoracle as O  # noqa: F401
+                import torch  # noqa: F401
+                cb = cpu_baseline_hara(args, cfg)
+                print(json.dumps({"impl": "reference", "metric": "HARA build time (N=2^18, tol 1e-6)",
+                                  "value": cb["value"], "unit": "s", "n_gpus": world, "steps": 1, "warmup": 0,
+                                  "higher_is_better": False, "config": {"workload": cfg["workload"]},
+                                  "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "s",
+                                                              "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+            return
+        out = run_hara(args, cfg, world, rank, local, dist)
+        if rank == 0 and not args.no_cpu_baseline:
+            try:
+                out["cpu_baseline"] = cpu_baseline_hara(args, cfg)
+            except Exception as e:
+                out["cpu_baseline"] = {"value": None, "error": repr(e)}
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
     if args.impl == "reference":
         out = run_reference(args, cfg, world, rank)
         if out is not None:

@@ -151,6 +151,8 @@ typedef struct {
     uint64_t seed;                /* 42 */
     double norm_scale;            /* 0 = estimate ||op||_2 */
     int64_t crossover_rank_cap;   /* 128 */
+    int rng;                      /* B200 extension: 0 = reference mt19937_64 normal stream (host,
+                                     bit-compatible panels), 1 = Philox normals generated in HBM */
 } h2c_peel_config;                /* PeelConfig (construction.hpp:23-31) */
 typedef struct {
     int level;

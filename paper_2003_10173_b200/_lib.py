@@ -93,7 +93,7 @@ class PeelConfigC(C.Structure):
     """h2c_peel_config (PeelConfig, construction.hpp:23-31)."""
     _fields_ = [("eps", C.c_double), ("sample_block_size", C.c_int64), ("oversampling", C.c_int64),
                 ("max_rank", C.c_int64), ("seed", C.c_uint64), ("norm_scale", C.c_double),
-                ("crossover_rank_cap", C.c_int64)]
+                ("crossover_rank_cap", C.c_int64), ("rng", C.c_int)]
 
 
 class LevelStatsC(C.Structure):

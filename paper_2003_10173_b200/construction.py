@@ -127,6 +127,7 @@ class PeelConfig:   # construction.hpp:23-31
     seed: int = 42
     norm_scale: float = 0.0
     crossover_rank_cap: int = 128
+    rng: int = 0   # B200 extension: 0 reference host stream, 1 device Philox
 
 
 @dataclasses.dataclass
@@ -158,7 +159,7 @@ def peel_construct(op, bt, cfg=None):
     """HARA (construction.hpp:300-382) on the B200."""
     cfg = cfg or PeelConfig()
     c = PeelConfigC(float(cfg.eps), int(cfg.sample_block_size), int(cfg.oversampling), int(cfg.max_rank),
-                    int(cfg.seed), float(cfg.norm_scale), int(cfg.crossover_rank_cap))
+                    int(cfg.seed), float(cfg.norm_scale), int(cfg.crossover_rank_cap), int(cfg.rng))
     h = H()
     tot = C.c_int64()
     lv = (LevelStatsC * 128)()

@@ -155,7 +155,10 @@ int h2c_matrix_create(h2c_block_tree b, int symmetric, const int* row_ranks, con
         *out = m;
     });
 }
-void h2c_matrix_destroy(h2c_matrix h) { delete h; }
+void h2c_matrix_destroy(h2c_matrix h) {
+    if (h) cudaDeviceSynchronize();   // device work on any stream may still read it
+    delete h;
+}
 
 int h2c_matrix_info(h2c_matrix h, int64_t* n, int* symmetric, int* orthonormal) {
     return guard([&] {
@@ -390,6 +393,7 @@ void h2c_peel_config_default(h2c_peel_config* cfg) {
     cfg->seed = d.seed;
     cfg->norm_scale = d.norm_scale;
     cfg->crossover_rank_cap = d.crossover_rank_cap;
+    cfg->rng = d.rng;
 }
 
 int h2c_peel_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config* cfg, h2c_matrix* out,
@@ -406,6 +410,7 @@ int h2c_peel_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config
             c.seed = cfg->seed;
             c.norm_scale = cfg->norm_scale;
             c.crossover_rank_cap = cfg->crossover_rank_cap;
+            c.rng = cfg->rng;
         }
         h2b::PeelResult r = h2b::peel_construct(*op->op, bt->b, c, nullptr);
         if (total_samples) *total_samples = r.stats.total;

@@ -22,38 +22,54 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define H2B_CUDA(x) ::h2b::cuda_check((x), #x, __FILE__, __LINE__)
 #define H2B_LAUNCH() ::h2b::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
 
-// owning device allocation (cudaMalloc; never host memory)
+// Device allocations come from the device's stream-ordered memory pool
+// (cudaMallocAsync / cudaFreeAsync) with the release threshold raised, so the
+// many short-lived H^2 values of a construction recycle HBM without a device
+// synchronisation per allocation (cudaMalloc / cudaFree would serialise).
+void ensure_mem_pool();
+
+// pinned host staging for small host->device uploads (descriptor lists, plans):
+// a pageable cudaMemcpyAsync would synchronise the stream first
+void* stage_to_device(const void* host, size_t bytes, void* dev_dst, cudaStream_t s);
+
+// owning device allocation (never host memory); `s` = the stream the buffer is
+// allocated on and freed on (nullptr = legacy default stream)
 template <class T>
 class DeviceArray {
 public:
     DeviceArray() = default;
-    explicit DeviceArray(size_t n) { resize(n); }
+    explicit DeviceArray(size_t n, cudaStream_t s = nullptr) { resize(n, s); }
     ~DeviceArray() { release(); }
     DeviceArray(const DeviceArray&) = delete;
     DeviceArray& operator=(const DeviceArray&) = delete;
-    DeviceArray(DeviceArray&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DeviceArray(DeviceArray&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
     DeviceArray& operator=(DeviceArray&& o) noexcept {
         if (this != &o) {
             release();
             p_ = o.p_;
             n_ = o.n_;
+            s_ = o.s_;
             o.p_ = nullptr;
             o.n_ = 0;
         }
         return *this;
     }
-    void resize(size_t n) {
+    void resize(size_t n, cudaStream_t s = nullptr) {
         if (n == n_) return;
         release();
-        if (n) H2B_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        s_ = s;
+        if (n) {
+            ensure_mem_pool();
+            H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+        }
         n_ = n;
     }
-    void upload(const T* h, size_t n, cudaStream_t s = 0) {
-        resize(n);
-        if (n) H2B_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    void upload(const T* h, size_t n, cudaStream_t s = nullptr) {
+        resize(n, s);
+        if (n) stage_to_device(h, n * sizeof(T), p_, s);
     }
-    void upload(const std::vector<T>& h, cudaStream_t s = 0) { upload(h.data(), h.size(), s); }
-    std::vector<T> download(cudaStream_t s = 0) const {
+    void upload(const std::vector<T>& h, cudaStream_t s = nullptr) { upload(h.data(), h.size(), s); }
+    std::vector<T> download(cudaStream_t s = nullptr) const {
         std::vector<T> h(n_);
         if (n_) {
             H2B_CUDA(cudaMemcpyAsync(h.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -61,7 +77,7 @@ public:
         }
         return h;
     }
-    void zero(cudaStream_t s = 0) {
+    void zero(cudaStream_t s = nullptr) {
         if (n_) H2B_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
     }
     T* data() { return p_; }
@@ -70,12 +86,13 @@ public:
 
 private:
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) cudaFreeAsync(p_, s_);
         p_ = nullptr;
         n_ = 0;
     }
     T* p_ = nullptr;
     size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
 };
 
 }  // namespace h2b

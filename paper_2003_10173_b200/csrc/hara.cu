@@ -9,6 +9,8 @@
 #include <cstring>
 #include <random>
 
+#include <curand_kernel.h>
+
 #include "hara.hpp"
 #include "la.hpp"
 #include "matrix.hpp"
@@ -69,6 +71,30 @@ void fill_gaussian(double* m, int64_t rows, int64_t cols, int64_t ld, std::mt199
     std::normal_distribution<double> g(0, 1);
     for (int64_t j = 0; j < cols; ++j)
         for (int64_t i = 0; i < rows; ++i) m[i + j * ld] = g(rng);
+}
+
+// device Gaussian panel rows [r0, r0 + rows) x [0, cols) of an n-row matrix
+// (Philox4x32-10, counter = (panel id, element index): deterministic for a seed)
+struct RngSeg {
+    int64_t r0, rows;
+};
+__global__ void philox_fill_kernel(const RngSeg* __restrict__ segs, int nseg, int64_t cols, int64_t n, double* out,
+                                   unsigned long long seed, unsigned long long panel) {
+    const RngSeg sg = segs[blockIdx.y];
+    const int64_t total = sg.rows * cols;
+    for (int64_t e = 2 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x); e < total;
+         e += 2 * int64_t(gridDim.x) * blockDim.x) {
+        curandStatePhilox4_32_10_t st;
+        curand_init(seed, panel, uint64_t(sg.r0 * cols + e), &st);
+        const double2 g = curand_normal2_double(&st);
+        const int64_t i0 = e % sg.rows, j0 = e / sg.rows;
+        out[sg.r0 + i0 + j0 * n] = g.x;
+        if (e + 1 < total) {
+            const int64_t i1 = (e + 1) % sg.rows, j1 = (e + 1) / sg.rows;
+            out[sg.r0 + i1 + j1 * n] = g.y;
+        }
+    }
+    (void)nseg;
 }
 
 }  // namespace
@@ -601,6 +627,22 @@ double ms_since(Clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }
 
+// host wall time per construction phase (stream synchronised at the phase end):
+// 0 panel RNG, 1 operator applies, 2 residual hgemv of the partial matrix,
+// 3 absorb_panel, 4 transposed-pass bookkeeping, 5 local updates, 6 recompress,
+// 7 dense-leaf extraction
+double g_phase_ms[8];
+struct Phase {
+    int id;
+    cudaStream_t s;
+    Clock::time_point t0;
+    Phase(int i, cudaStream_t st) : id(i), s(st), t0(Clock::now()) {}
+    ~Phase() {
+        cudaStreamSynchronize(s);
+        g_phase_ms[id] += ms_since(t0);
+    }
+};
+
 struct PeelContext {
     DevOperator& op;
     const H2Dev* partial = nullptr;   // residual = op - partial (ResidualOperator, :203-222)
@@ -609,6 +651,7 @@ struct PeelContext {
     double op_ms = 0;
     cudaStream_t s;
     int64_t n;
+    unsigned long long panel_counter = 0;
 
     PeelContext(DevOperator& o, const ClusterTree& ct, cudaStream_t st) : op(o), s(st), n(ct.n) {
         perm.upload(int32_perm(ct));
@@ -620,7 +663,11 @@ struct PeelContext {
         else op.apply(b, x, y, s);
         H2B_CUDA(cudaStreamSynchronize(s));
         op_ms += ms_since(t0);
-        if (partial) hgemv(*partial, transpose, true, n, b, x, n, y, n, -1.0, 1.0, s, ws);
+        g_phase_ms[1] += ms_since(t0);
+        if (partial) {
+            Phase ph(2, s);
+            hgemv(*partial, transpose, true, n, b, x, n, y, n, -1.0, 1.0, s, ws);
+        }
     }
 };
 
@@ -656,18 +703,37 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
         for (const auto& r : ranges)
             if (!r.converged) panel = std::max(panel, r.wants_full ? b : probes);
         // Omega in internal order: Gaussians on each unconverged pair's s rows
-        omh.assign(size_t(n * panel), 0.0);
-        for (auto& r : ranges) {
-            if (r.converged) continue;
-            fill_gaussian(omh.data() + ct.begin[size_t(r.s)], ct.size(r.s), panel, n, rng);
-        }
         om.alloc(size_t(n * panel), s);
         omu.alloc(size_t(n * panel), s);
         y.alloc(size_t(n * panel), s);
         yi.alloc(size_t(n * panel), s);
-        H2B_CUDA(cudaMemcpyAsync(om.data(), omh.data(), omh.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        Phase* ph_rng = new Phase(0, s);
+        if (cfg.rng == 0) {
+            omh.assign(size_t(n * panel), 0.0);
+            for (auto& r : ranges) {
+                if (r.converged) continue;
+                fill_gaussian(omh.data() + ct.begin[size_t(r.s)], ct.size(r.s), panel, n, rng);
+            }
+            H2B_CUDA(cudaMemcpyAsync(om.data(), omh.data(), omh.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+        } else {
+            om.zero();
+            std::vector<RngSeg> segs;
+            for (auto& r : ranges)
+                if (!r.converged) segs.push_back(RngSeg{ct.begin[size_t(r.s)], ct.size(r.s)});
+            DeviceArray<RngSeg> dsegs;
+            dsegs.upload(segs, s);
+            int64_t maxrows = 0;
+            for (const RngSeg& g : segs) maxrows = std::max(maxrows, g.rows);
+            const int64_t bx = std::min<int64_t>((maxrows * panel / 2 + 255) / 256, 4096);
+            philox_fill_kernel<<<dim3(unsigned(std::max<int64_t>(bx, 1)), unsigned(segs.size())), 256, 0, s>>>(
+                dsegs.data(), int(segs.size()), panel, n, om.data(), cfg.seed, ctx.panel_counter++);
+            H2B_LAUNCH();
+            H2B_CUDA(cudaStreamSynchronize(s));
+        }
         la::permute_rows(om.data(), n, omu.data(), n, ctx.perm.data(), n, panel, true, s);
+        delete ph_rng;
         ctx.residual(false, panel, omu.data(), y.data());
+        Phase ph_absorb(3, s);
         la::permute_rows(y.data(), n, yi.data(), n, ctx.perm.data(), n, panel, false, s);
         const double keep_tol = 0.5 * tol_abs * std::sqrt(double(panel));
         // absorb_panel (construction.hpp:105-129), batched over the unconverged pairs
@@ -768,6 +834,7 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
         bcopy(cp, s);
     }
     // transposed pass (:272-289): W = residual^T Z, Z = each pair's Q on its t rows
+    Phase ph_t(4, s);
     int kmax = 0;
     for (const auto& r : ranges) kmax = std::max(kmax, r.rank);
     if (kmax > 0) {
@@ -784,6 +851,7 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
 PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, const PeelConfig& cfg,
                           cudaStream_t s) {
     const auto t_start = Clock::now();
+    std::fill(g_phase_ms, g_phase_ms + 8, 0.0);
     const ClusterTree& ct = *bt->tree;
     if (ct.n != op.dim()) throw std::invalid_argument("peel_construct: dimension mismatch");
     std::mt19937_64 rng(cfg.seed);
@@ -816,6 +884,7 @@ PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, 
                                               Wi.data() + ct.begin[size_t(r.s)], ct.n});
             }
             if (!ups.empty()) {
+                Phase ph(5, s);
                 partial = apply_local_updates(*partial, ups, s);
                 H2B_CUDA(cudaStreamSynchronize(s));
             }
@@ -826,12 +895,16 @@ PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, 
             for (auto [t, u] : pairs) mirrored.emplace_back(u, t);
             group(mirrored);
         }
-        partial = recompress(*partial, 0.5 * cfg.eps, s);
+        {
+            Phase ph(6, s);
+            partial = recompress(*partial, 0.5 * cfg.eps, s);
+        }
         stats.add_level({level, int64_t(pairs.size()) * (sym ? 1 : 2), max_rank_seen, op.columns_applied() - before});
     }
     // dense diagonal leaves (:357-376): indicator columns, residual apply, symmetrise, add
     before = op.columns_applied();
     {
+        Phase ph(7, s);
         const int64_t n = ct.n, m = ct.max_leaf_size();
         DBuf om(size_t(n * m), s), omu(size_t(n * m), s), y(size_t(n * m), s), yi(size_t(n * m), s);
         om.zero();
@@ -884,3 +957,9 @@ double estimate_relative_error(DevOperator& op, const H2Dev& h, double op_norm, 
 }
 
 }  // namespace h2b
+
+// diagnostic hook (not part of the public ABI): per-phase host wall time of the last peel_construct
+extern "C" int h2b_hara_phase_ms(double* out, int n) {
+    for (int i = 0; i < n && i < 8; ++i) out[i] = h2b::g_phase_ms[i];
+    return 0;
+}

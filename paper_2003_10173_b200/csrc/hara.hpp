@@ -127,6 +127,11 @@ struct PeelConfig {   // construction.hpp:23-31
     uint64_t seed = 42;
     double norm_scale = 0;
     int64_t crossover_rank_cap = 128;
+    // B200 extension: 0 = the reference's Gaussian stream (host mt19937_64 +
+    // std::normal_distribution, construction.hpp:81-85; bit-compatible panels),
+    // 1 = counter-based Philox4x32-10 normals generated in HBM (same accuracy
+    // contract, no host RNG or PCIe upload on the sampling path)
+    int rng = 0;
 };
 struct LevelStats {
     int level = 0;

@@ -364,18 +364,39 @@ struct PlanBuilder {
         ld.units_even = ue;
         ld.task_end = int(tasks.size());
         {
-            std::unordered_set<const double*> seen_a;
-            std::unordered_set<int64_t> seen_b;
+            std::vector<const double*> as;
+            std::vector<int64_t> bs;
             for (auto& p : outs) {
                 if (p.rows <= 0) continue;
                 ld.out_per_col += p.rows;
                 for (auto& e : p.es) {
                     if (e.k <= 0) continue;
                     ld.flops_per_col += 2.0 * p.rows * e.k;
-                    if (seen_a.insert(e.A).second) ld.payload_bytes += 8.0 * double(p.rows) * e.k;
-                    if (seen_b.insert((int64_t(e.src) << 56) ^ e.b_unit).second) ld.bsrc_per_col += e.k;
+                    as.push_back(e.A);
+                    bs.push_back((int64_t(e.src) << 56) ^ e.b_unit);
                 }
             }
+            // each distinct stored block is read once; each distinct B operand block once per column
+            std::vector<std::pair<const double*, double>> ab;
+            for (auto& p : outs) {
+                if (p.rows <= 0) continue;
+                for (auto& e : p.es)
+                    if (e.k > 0) ab.emplace_back(e.A, 8.0 * double(p.rows) * e.k);
+            }
+            std::sort(ab.begin(), ab.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+            for (size_t i = 0; i < ab.size(); ++i)
+                if (i == 0 || ab[i].first != ab[i - 1].first) ld.payload_bytes += ab[i].second;
+            std::vector<std::pair<int64_t, int>> bk;
+            for (auto& p : outs) {
+                if (p.rows <= 0) continue;
+                for (auto& e : p.es)
+                    if (e.k > 0) bk.emplace_back((int64_t(e.src) << 56) ^ e.b_unit, e.k);
+            }
+            std::sort(bk.begin(), bk.end());
+            for (size_t i = 0; i < bk.size(); ++i)
+                if (i == 0 || bk[i].first != bk[i - 1].first) ld.bsrc_per_col += bk[i].second;
+            (void)as;
+            (void)bs;
         }
         if (ld.task_end > ld.task_begin || zero_yhat) launches.push_back(ld);
     }
@@ -641,9 +662,9 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
     auto plan = get_plan(h, transpose);
     const size_t need_x = size_t(n * b), need_u = size_t(plan->coef_up * b), need_d = size_t(plan->coef_down * b);
-    if (ws.xint.size() < need_x) ws.xint.resize(need_x);
-    if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1));
-    if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1));
+    if (ws.xint.size() < need_x) ws.xint.resize(need_x, stream);
+    if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1), stream);
+    if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
     const int* perm = user_order ? plan->perm.data() : nullptr;
     if (timer) timer->mark(stream);
     gather_blocked_kernel<<<plan->num_leaves, 256, 0, stream>>>(x, ldx, perm, plan->leaf_begin.data(), plan->leaf_m.data(), b,

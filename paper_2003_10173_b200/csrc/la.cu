@@ -20,8 +20,9 @@ struct DevVec {
     cudaStream_t s;
     DevVec(const std::vector<T>& h, cudaStream_t st) : s(st) {
         if (h.empty()) return;
+        ensure_mem_pool();
         H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), h.size() * sizeof(T), s));
-        H2B_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        stage_to_device(h.data(), h.size() * sizeof(T), p, s);
     }
     ~DevVec() {
         if (p) cudaFreeAsync(p, s);

@@ -36,7 +36,10 @@ public:
         release();
         s_ = s;
         n_ = n;
-        if (n) H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(double), s));
+        if (n) {
+            ensure_mem_pool();
+            H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(double), s));
+        }
     }
     void zero() {
         if (n_) H2B_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(double), s_));

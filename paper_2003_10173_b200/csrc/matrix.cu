@@ -74,7 +74,6 @@ std::unique_ptr<H2Dev> make_h2(std::shared_ptr<const BlockTree> bt, bool symmetr
     h->col.xfer.zero();
     h->S.zero();
     h->D.zero();
-    H2B_CUDA(cudaDeviceSynchronize());
     return h;
 }
 
