@@ -168,6 +168,33 @@ int h2c_peel_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config
 /* estimate_relative_error(op, h, op_norm) (construction.hpp:537-546) */
 int h2c_estimate_relative_error(h2c_operator op, h2c_matrix h, double op_norm, double* out);
 
+/* ---- row-subtree sharded hgemv (one process per GPU) ------
+ * Rank r of P (power of two) owns the subtree under the r-th node of tree level
+ * log2 P; levels above are replicated. One hgemv = begin (owned upsweep, pack
+ * the send buffer) -> an all-to-all of send/recv buffers by the caller's
+ * collective layer (NCCL via torch.distributed) -> end (unpack, couplings,
+ * downsweep, near-field for the owned rows of y). Buffer sizes are rows per
+ * vector column: send_rows[q] * b doubles go to peer q, peers in rank order. */
+typedef struct h2c_dist_plan_s* h2c_dist_plan;
+int h2c_dist_plan_create(h2c_matrix h, int transpose, int nranks, int rank, h2c_dist_plan* out);
+void h2c_dist_plan_destroy(h2c_dist_plan p);
+/* send_rows / recv_rows: nranks entries each; owned internal row range [begin, begin + rows) */
+int h2c_dist_plan_counts(h2c_dist_plan p, int64_t* send_rows, int64_t* recv_rows, int64_t* owned_begin,
+                         int64_t* owned_rows);
+/* x: full n x b user-order device matrix (only owned rows are read) */
+int h2c_dist_hgemv_begin(h2c_dist_plan p, int64_t b, const double* x, int64_t ldx, double* sendbuf, void* stream);
+/* y: full n x b user-order device matrix (only owned rows are written: y = alpha H x + beta y) */
+int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha,
+                       double beta, void* stream);
+/* host-only partition metadata (no device needed): owner rank per cluster node
+ * (-1 = replicated top level) and the exchange items rank dst receives from
+ * rank src for a matrix with the given upsweep-basis ranks (arr 0 = x rows of
+ * leaf `node`, 1 = x-hat of `node`; rows per vector column). Call with
+ * arr == NULL to get *count. */
+int h2c_partition_owner(h2c_block_tree b, int nranks, int* owner);
+int h2c_partition_exchange(h2c_block_tree b, int symmetric, int transpose, const int* up_ranks, int nranks, int src,
+                           int dst, int64_t* count, int* arr, int* node, int64_t* rows);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,3 +116,11 @@ _sig("h2c_recompress", i32, H, f64, P(H))
 _sig("h2c_peel_config_default", None, P(PeelConfigC))
 _sig("h2c_peel_construct", i32, H, H, P(PeelConfigC), P(H), P(i64), P(LevelStatsC), i32, P(i32), P(f64), P(f64))
 _sig("h2c_estimate_relative_error", i32, H, H, f64, P(f64))
+
+_sig("h2c_dist_plan_create", i32, H, i32, i32, i32, P(H))
+_sig("h2c_dist_plan_destroy", None, H)
+_sig("h2c_dist_plan_counts", i32, H, vp, vp, P(i64), P(i64))
+_sig("h2c_dist_hgemv_begin", i32, H, i64, vp, i64, vp, vp)
+_sig("h2c_dist_hgemv_end", i32, H, i64, vp, vp, i64, f64, f64, vp)
+_sig("h2c_partition_owner", i32, H, i32, vp)
+_sig("h2c_partition_exchange", i32, H, i32, i32, vp, i32, i32, i32, P(i64), vp, vp, vp)

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/h2c.h) over the C++ host layer and CUDA kernels.
 #include "../../include/h2c.h"
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -17,6 +18,9 @@ struct h2c_block_tree_s {
 struct h2c_matrix_s {
     std::unique_ptr<h2b::H2Dev> h;
     h2b::Workspace ws;
+};
+struct h2c_dist_plan_s {
+    std::shared_ptr<h2b::DistPlan> p;
 };
 struct h2c_operator_s {
     std::unique_ptr<h2b::DevOperator> op;
@@ -430,6 +434,86 @@ int h2c_estimate_relative_error(h2c_operator op, h2c_matrix h, double op_norm, d
     return guard([&] {
         need(op != nullptr && h != nullptr && out != nullptr, "null argument");
         *out = h2b::estimate_relative_error(*op->op, *h->h, op_norm, nullptr);
+    });
+}
+
+// ---- sharded hgemv ----------------------------------------------------------
+int h2c_dist_plan_create(h2c_matrix h, int transpose, int nranks, int rank, h2c_dist_plan* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        *out = new h2c_dist_plan_s{h2b::make_dist_plan(*h->h, transpose != 0, nranks, rank)};
+    });
+}
+
+void h2c_dist_plan_destroy(h2c_dist_plan p) {
+    if (p) cudaDeviceSynchronize();
+    delete p;
+}
+
+int h2c_dist_plan_counts(h2c_dist_plan p, int64_t* send_rows, int64_t* recv_rows, int64_t* owned_begin,
+                         int64_t* owned_rows) {
+    return guard([&] {
+        need(p != nullptr, "null argument");
+        std::vector<int64_t> s, r;
+        h2b::dist_counts(*p->p, s, r);
+        for (size_t i = 0; i < s.size(); ++i) {
+            if (send_rows) send_rows[i] = s[i];
+            if (recv_rows) recv_rows[i] = r[i];
+        }
+        int64_t beg = 0;
+        const int64_t rows = h2b::dist_owned_rows(*p->p, &beg);
+        if (owned_begin) *owned_begin = beg;
+        if (owned_rows) *owned_rows = rows;
+    });
+}
+
+int h2c_dist_hgemv_begin(h2c_dist_plan p, int64_t b, const double* x, int64_t ldx, double* sendbuf, void* stream) {
+    return guard([&] {
+        need(p != nullptr && x != nullptr, "null argument");
+        need(b >= 1, "matvec: need at least one column");
+        h2b::dist_hgemv_begin(*p->p, b, x, ldx, sendbuf, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha,
+                       double beta, void* stream) {
+    return guard([&] {
+        need(p != nullptr && y != nullptr, "null argument");
+        need(b >= 1, "matvec: need at least one column");
+        h2b::dist_hgemv_end(*p->p, b, recvbuf, y, ldy, alpha, beta, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_partition_owner(h2c_block_tree b, int nranks, int* owner) {
+    return guard([&] {
+        need(b != nullptr && owner != nullptr, "null argument");
+        const h2b::DistSpec d = h2b::make_dist_spec(*b->b->tree, nranks, 0);
+        std::copy(d.owner.begin(), d.owner.end(), owner);
+    });
+}
+
+int h2c_partition_exchange(h2c_block_tree b, int symmetric, int transpose, const int* up_ranks, int nranks, int src,
+                           int dst, int64_t* count, int* arr, int* node, int64_t* rows) {
+    return guard([&] {
+        need(b != nullptr && up_ranks != nullptr && count != nullptr, "null argument");
+        need(src >= 0 && src < nranks && dst >= 0 && dst < nranks, "rank out of range");
+        const h2b::ClusterTree& ct = *b->b->tree;
+        const h2b::DistSpec d = h2b::make_dist_spec(ct, nranks, dst);
+        std::vector<int> ur(up_ranks, up_ranks + ct.num_nodes());
+        std::vector<int64_t> cu(size_t(ct.num_nodes()));
+        int64_t o = 0;
+        for (int v = 0; v < ct.num_nodes(); ++v) {
+            cu[size_t(v)] = o;
+            o += ur[size_t(v)];
+        }
+        const auto items = h2b::exchange_items(*b->b, symmetric != 0, transpose != 0, ur, d, src, dst, cu);
+        *count = int64_t(items.size());
+        if (arr)
+            for (size_t i = 0; i < items.size(); ++i) {
+                arr[i] = items[i].arr;
+                if (node) node[i] = items[i].node;
+                if (rows) rows[i] = items[i].rows;
+            }
     });
 }
 

@@ -74,4 +74,44 @@ void hgemv_timed(const H2Dev& h, bool transpose, bool user_order, int64_t n, int
 // kernel launches one hgemv issues (for the bench's gpu_launches claim)
 int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b);
 
+// ---- row-subtree sharded hgemv ------------------------------
+// Rank r of P (a power of two) owns the subtree under the r-th node of level
+// lp = log2 P: its leaves' rows of x and y, its nodes' x-hat / y-hat and every
+// block whose target (row) lies in it. Levels < lp are replicated (computed
+// redundantly by every rank). One exchange per hgemv moves, to each rank, the
+// x-hat of remote nodes its couplings / top upsweep read and the x rows of
+// remote near-field leaves its dense blocks read.
+struct DistSpec {
+    int nranks = 1, rank = 0, lp = 0;
+    std::vector<int> owner;   // per node: owning rank, -1 for the replicated top levels
+};
+DistSpec make_dist_spec(const ClusterTree& ct, int nranks, int rank);
+
+// one exchange item: `rows` rows (times b columns, contiguous) of array
+// `arr` (0 = blocked x, 1 = x-hat) at row offset `unit`, packed at `buf` rows
+struct XItem {
+    int arr;
+    int node;
+    int64_t unit, rows, buf;
+};
+// items rank `dst` must receive from rank `src` (identical on every rank)
+std::vector<XItem> exchange_items(const H2Dev& h, bool transpose, const DistSpec& all, int src, int dst,
+                                  const std::vector<int64_t>& cu);
+// host-only form (block tree + ranks of the basis the upsweep uses; cu = x-hat offsets)
+std::vector<XItem> exchange_items(const BlockTree& bt, bool symmetric, bool transpose, const std::vector<int>& up_rank,
+                                  const DistSpec& all, int src, int dst, const std::vector<int64_t>& cu);
+
+struct DistPlan;
+std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nranks, int rank);
+// rows (per column) this rank sends to / receives from each peer
+void dist_counts(const DistPlan& p, std::vector<int64_t>& send_rows, std::vector<int64_t>& recv_rows);
+// phase A: gather owned x rows, owned upsweep, pack the send buffer
+// (peers in rank order, each peer's items contiguous; b columns per row)
+void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, double* sendbuf, cudaStream_t s);
+// phase B: unpack the receive buffer, replicated top upsweep, couplings,
+// downsweep, leaf + near-field for owned rows of y (user order)
+void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha, double beta,
+                    cudaStream_t s);
+int64_t dist_owned_rows(const DistPlan& p, int64_t* begin);
+
 }  // namespace h2b

@@ -295,6 +295,7 @@ struct LaunchDesc {
     // column of B operands read / outputs written
     double flops_per_col = 0, payload_bytes = 0, bsrc_per_col = 0, out_per_col = 0;
     int stage = 0;            // 1 leaf up, 2 transfer up, 3 coupling, 4 downsweep, 5 leaf+dense
+    int phase = 0;            // sharded hgemv: 0 before the exchange, 1 after
 };
 
 struct HgemvPlan {
@@ -306,6 +307,7 @@ struct HgemvPlan {
     DeviceArray<int> leaf_m;
     int num_leaves = 0;
     int64_t coef_up = 0, coef_down = 0;
+    std::vector<int64_t> cu;   // per node: x-hat offset (units of b)
 };
 
 namespace {
@@ -322,8 +324,10 @@ struct PlanBuilder {
         std::vector<SegEntry> es;
     };
 
+    int phase = 0;
     void emit(std::vector<Pending>& outs, int mode, int out, int stage, bool zero_yhat = false) {
         LaunchDesc ld;
+        ld.phase = phase;
         ld.stage = stage;
         ld.mode = mode;
         ld.out = out;
@@ -414,8 +418,12 @@ SegEntry make_entry(const double* A, int lda, int k, bool trans, int src, int64_
     return e;
 }
 
-std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
+std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const DistSpec* ds = nullptr) {
     const ClusterTree& ct = h.tree();
+    // sharded plans keep only this rank's outputs: its subtree (owner == rank)
+    // plus the replicated top levels (owner < 0)
+    auto own = [&](int v) { return !ds || ds->owner[size_t(v)] == ds->rank; };
+    auto local = [&](int v) { return !ds || ds->owner[size_t(v)] == ds->rank || ds->owner[size_t(v)] < 0; };
     const BlockTree& bt = *h.bt;
     const int nn = ct.num_nodes();
     const bool swap = transpose && !h.symmetric;
@@ -435,6 +443,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
     {
         std::vector<P> outs;
         for (int t : ct.leaves) {
+            if (!own(t)) continue;
             const int k = up.rank[size_t(t)], m = int(ct.size(t));
             P p{k, k, cu[size_t(t)], {}};
             p.es.push_back(make_entry(up.leaf.data() + up.leaf_off[size_t(t)], m, m, true, 0, ct.begin[size_t(t)], m));
@@ -445,8 +454,9 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
     // stage 1b: transfers bottom-up
     for (int l = ct.depth - 1; l >= 0; --l) {
         std::vector<P> outs;
+        pb.phase = (ds && l < ds->lp) ? 1 : 0;
         for (int v : ct.levels[size_t(l)]) {
-            if (ct.is_leaf(v)) continue;
+            if (ct.is_leaf(v) || !local(v)) continue;
             const int kv = up.rank[size_t(v)];
             P p{kv, kv, cu[size_t(v)], {}};
             for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]}) {
@@ -474,8 +484,9 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
             }
         }
         std::vector<P> outs;
+        pb.phase = 1;
         for (int v = 0; v < nn; ++v) {
-            if (by_target[size_t(v)].empty()) continue;
+            if (by_target[size_t(v)].empty() || !local(v)) continue;
             const int k = down.rank[size_t(v)];
             outs.push_back(P{k, k, cd[size_t(v)], std::move(by_target[size_t(v)])});
         }
@@ -488,6 +499,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
             if (ct.is_leaf(v)) continue;
             const int kv = down.rank[size_t(v)];
             for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]}) {
+                if (!local(c)) continue;
                 const int kc = down.rank[size_t(c)];
                 P p{kc, kc, cd[size_t(c)], {}};
                 p.es.push_back(make_entry(down.xfer.data() + down.xfer_off[size_t(c)], kc, kv, false, 2, cd[size_t(v)], kv));
@@ -518,6 +530,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
         }
         std::vector<P> outs;
         for (int t : ct.leaves) {
+            if (!own(t)) continue;
             const int m = int(ct.size(t));
             outs.push_back(P{m, m, ct.begin[size_t(t)], std::move(by_leaf[size_t(t)])});
         }
@@ -531,10 +544,12 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose) {
     std::vector<int64_t> lb;
     std::vector<int> lm;
     for (int t : ct.leaves) {
+        if (!own(t)) continue;
         lb.push_back(ct.begin[size_t(t)]);
         lm.push_back(int(ct.size(t)));
     }
     plan->num_leaves = int(lb.size());
+    plan->cu = std::move(cu);
     plan->leaf_begin.upload(lb);
     plan->leaf_m.upload(lm);
     H2B_CUDA(cudaDeviceSynchronize());
@@ -629,7 +644,7 @@ struct EventTimer {
 };
 void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
                 double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
-                EventTimer* timer);
+                EventTimer* timer, const HgemvPlan* dplan = nullptr, int phases = 3);
 }  // namespace
 
 void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
@@ -656,25 +671,30 @@ void hgemv_timed(const H2Dev& h, bool transpose, bool user_order, int64_t n, int
 namespace {
 void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
                 double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
-                EventTimer* timer) {
+                EventTimer* timer, const HgemvPlan* dplan, int phases) {
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
     if (b < 1) throw std::invalid_argument("matvec: need at least one column");
     if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
-    auto plan = get_plan(h, transpose);
+    std::shared_ptr<HgemvPlan> own_plan;
+    if (!dplan) own_plan = get_plan(h, transpose);
+    const HgemvPlan* plan = dplan ? dplan : own_plan.get();
     const size_t need_x = size_t(n * b), need_u = size_t(plan->coef_up * b), need_d = size_t(plan->coef_down * b);
     if (ws.xint.size() < need_x) ws.xint.resize(need_x, stream);
     if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1), stream);
     if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
     const int* perm = user_order ? plan->perm.data() : nullptr;
-    if (timer) timer->mark(stream);
-    gather_blocked_kernel<<<plan->num_leaves, 256, 0, stream>>>(x, ldx, perm, plan->leaf_begin.data(), plan->leaf_m.data(), b,
-                                                               ws.xint.data());
-    H2B_LAUNCH();
-    if (timer) {
-        timer->mark(stream);
-        timer->out->push_back({0, 0.f, 0.0, 16.0 * double(n * b)});
+    if ((phases & 1) && plan->num_leaves > 0) {
+        if (timer) timer->mark(stream);
+        gather_blocked_kernel<<<plan->num_leaves, 256, 0, stream>>>(x, ldx, perm, plan->leaf_begin.data(),
+                                                                   plan->leaf_m.data(), b, ws.xint.data());
+        H2B_LAUNCH();
+        if (timer) {
+            timer->mark(stream);
+            timer->out->push_back({0, 0.f, 0.0, 16.0 * double(n * b)});
+        }
     }
     for (const LaunchDesc& ld : plan->launches) {
+        if (!(phases & (1 << ld.phase))) continue;
         if (ld.zero_yhat && need_d) H2B_CUDA(cudaMemsetAsync(ws.yhat.data(), 0, need_d * sizeof(double), stream));
         const int ntasks = ld.task_end - ld.task_begin;
         if (ntasks == 0) continue;
@@ -702,6 +722,189 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     }
 }
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// row-subtree sharded hgemv
+// ---------------------------------------------------------------------------
+DistSpec make_dist_spec(const ClusterTree& ct, int nranks, int rank) {
+    if (nranks < 1 || (nranks & (nranks - 1)) != 0) throw std::invalid_argument("dist: nranks must be a power of two");
+    if (rank < 0 || rank >= nranks) throw std::invalid_argument("dist: rank out of range");
+    DistSpec d;
+    d.nranks = nranks;
+    d.rank = rank;
+    while ((1 << d.lp) < nranks) ++d.lp;
+    if (d.lp > ct.depth || int(ct.levels[size_t(d.lp)].size()) != nranks)
+        throw std::invalid_argument("dist: the cluster tree has fewer than nranks nodes at level log2(nranks)");
+    for (int l = 0; l < d.lp; ++l)
+        for (int v : ct.levels[size_t(l)])
+            if (ct.is_leaf(v)) throw std::invalid_argument("dist: leaf above the partition level");
+    d.owner.assign(size_t(ct.num_nodes()), -1);
+    const auto& roots = ct.levels[size_t(d.lp)];
+    for (int r = 0; r < nranks; ++r) {
+        std::vector<int> st{roots[size_t(r)]};
+        while (!st.empty()) {
+            const int v = st.back();
+            st.pop_back();
+            d.owner[size_t(v)] = r;
+            if (!ct.is_leaf(v)) {
+                st.push_back(ct.child0[size_t(v)]);
+                st.push_back(ct.child1[size_t(v)]);
+            }
+        }
+    }
+    return d;
+}
+
+std::vector<XItem> exchange_items(const H2Dev& h, bool transpose, const DistSpec& all, int src, int dst,
+                                  const std::vector<int64_t>& cu) {
+    const bool swap = transpose && !h.symmetric;
+    return exchange_items(*h.bt, h.symmetric, transpose, (swap ? h.row : h.vbasis()).rank, all, src, dst, cu);
+}
+
+std::vector<XItem> exchange_items(const BlockTree& bt, bool symmetric, bool transpose, const std::vector<int>& up_rank,
+                                  const DistSpec& all, int src, int dst, const std::vector<int64_t>& cu) {
+    const ClusterTree& ct = *bt.tree;
+    const bool swap = transpose && !symmetric;
+    auto stores = [&](int b) { return !symmetric || bt.canonical(b); };
+    auto local = [&](int v) { return all.owner[size_t(v)] == dst || all.owner[size_t(v)] < 0; };
+    std::vector<char> need_hat(size_t(ct.num_nodes()), 0), need_x(size_t(ct.num_nodes()), 0);
+    // replicated top upsweep reads the partition roots
+    if (all.lp > 0)
+        for (int v : ct.levels[size_t(all.lp - 1)])
+            for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]})
+                if (all.owner[size_t(c)] == src) need_hat[size_t(c)] = 1;
+    auto orient = [&](int b, auto&& f) {
+        const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
+        if (!swap) {
+            f(r, c);
+            if (symmetric && r != c) f(c, r);
+        } else {
+            f(c, r);
+        }
+    };
+    for (size_t i = 0; i < bt.adm.size(); ++i) {
+        const int b = bt.adm[i];
+        if (!stores(b)) continue;
+        orient(b, [&](int tgt, int srcn) {
+            if (local(tgt) && all.owner[size_t(srcn)] == src) need_hat[size_t(srcn)] = 1;
+        });
+    }
+    for (size_t i = 0; i < bt.dense.size(); ++i) {
+        const int b = bt.dense[i];
+        if (!stores(b)) continue;
+        orient(b, [&](int tgt, int srcn) {
+            if (all.owner[size_t(tgt)] == dst && all.owner[size_t(srcn)] == src) need_x[size_t(srcn)] = 1;
+        });
+    }
+    std::vector<XItem> items;
+    if (src == dst) return items;
+    int64_t at = 0;
+    for (int v = 0; v < ct.num_nodes(); ++v)
+        if (need_x[size_t(v)]) {
+            items.push_back(XItem{0, v, ct.begin[size_t(v)], ct.size(v), at});
+            at += ct.size(v);
+        }
+    for (int v = 0; v < ct.num_nodes(); ++v)
+        if (need_hat[size_t(v)] && up_rank[size_t(v)] > 0) {
+            items.push_back(XItem{1, v, cu[size_t(v)], up_rank[size_t(v)], at});
+            at += up_rank[size_t(v)];
+        }
+    return items;
+}
+
+struct DistPlan {
+    const H2Dev* h = nullptr;
+    bool transpose = false;
+    DistSpec spec;
+    std::shared_ptr<HgemvPlan> plan;
+    std::vector<int64_t> send_rows, recv_rows;
+    DeviceArray<XItem> send_items, recv_items;   // buffer offsets already global (peer blocks concatenated)
+    int nsend = 0, nrecv = 0;
+    Workspace ws;
+};
+
+namespace {
+// pack (dir 0: arrays -> buf) or unpack (dir 1: buf -> arrays) b columns per item
+__global__ void exchange_kernel(const XItem* __restrict__ items, int64_t b, double* xint, double* xhat, double* buf,
+                                int dir) {
+    const XItem it = items[blockIdx.x];
+    double* arr = it.arr == 0 ? xint : xhat;
+    double* a = arr + it.unit * b;
+    double* p = buf + it.buf * b;
+    const int64_t cnt = it.rows * b;
+    if (dir == 0)
+        for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) p[e] = a[e];
+    else
+        for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) a[e] = p[e];
+}
+}  // namespace
+
+std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nranks, int rank) {
+    auto p = std::make_shared<DistPlan>();
+    p->h = &h;
+    p->transpose = transpose;
+    p->spec = make_dist_spec(h.tree(), nranks, rank);
+    p->plan = build_plan(h, transpose, &p->spec);
+    const std::vector<int64_t>& cu = p->plan->cu;
+    p->send_rows.assign(size_t(nranks), 0);
+    p->recv_rows.assign(size_t(nranks), 0);
+    std::vector<XItem> snd, rcv;
+    int64_t so = 0, ro = 0;
+    for (int q = 0; q < nranks; ++q) {
+        auto out = exchange_items(h, transpose, p->spec, rank, q, cu);   // what q needs from me
+        for (XItem it : out) {
+            it.buf += so;
+            snd.push_back(it);
+            p->send_rows[size_t(q)] += it.rows;
+        }
+        so += p->send_rows[size_t(q)];
+        auto in = exchange_items(h, transpose, p->spec, q, rank, cu);    // what I need from q
+        for (XItem it : in) {
+            it.buf += ro;
+            rcv.push_back(it);
+            p->recv_rows[size_t(q)] += it.rows;
+        }
+        ro += p->recv_rows[size_t(q)];
+    }
+    p->nsend = int(snd.size());
+    p->nrecv = int(rcv.size());
+    p->send_items.upload(snd);
+    p->recv_items.upload(rcv);
+    H2B_CUDA(cudaDeviceSynchronize());
+    return p;
+}
+
+void dist_counts(const DistPlan& p, std::vector<int64_t>& send_rows, std::vector<int64_t>& recv_rows) {
+    send_rows = p.send_rows;
+    recv_rows = p.recv_rows;
+}
+
+int64_t dist_owned_rows(const DistPlan& p, int64_t* begin) {
+    const ClusterTree& ct = p.h->tree();
+    const int root = ct.levels[size_t(p.spec.lp)][size_t(p.spec.rank)];
+    if (begin) *begin = ct.begin[size_t(root)];
+    return ct.size(root);
+}
+
+void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, double* sendbuf, cudaStream_t s) {
+    const int64_t n = p.h->tree().n;
+    hgemv_impl(*p.h, p.transpose, true, n, b, x, ldx, nullptr, n, 1.0, 0.0, s, p.ws, nullptr, p.plan.get(), 1);
+    if (p.nsend) {
+        exchange_kernel<<<p.nsend, 256, 0, s>>>(p.send_items.data(), b, p.ws.xint.data(), p.ws.xhat.data(), sendbuf, 0);
+        H2B_LAUNCH();
+    }
+}
+
+void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha, double beta,
+                    cudaStream_t s) {
+    const int64_t n = p.h->tree().n;
+    if (p.nrecv) {
+        exchange_kernel<<<p.nrecv, 256, 0, s>>>(p.recv_items.data(), b, p.ws.xint.data(), p.ws.xhat.data(),
+                                                const_cast<double*>(recvbuf), 1);
+        H2B_LAUNCH();
+    }
+    hgemv_impl(*p.h, p.transpose, true, n, b, nullptr, n, y, ldy, alpha, beta, s, p.ws, nullptr, p.plan.get(), 2);
+}
 
 int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
     (void)b;

@@ -1,0 +1,104 @@
+"""Row-subtree sharded hgemv across GPUs: one process per GPU,
+torch.distributed (NCCL over NVLink) for the single all-to-all exchange per
+hgemv; every compute step runs in lib/libh2b200.so.
+
+Rank r of P owns the subtree under the r-th node of level log2 P (its rows of
+x and y); the top log2 P levels are replicated. The exchange carries the
+x-hat of remote clusters that owned couplings / the replicated top upsweep read
+and the x rows of remote near-field leaves (h2c.h, h2c_dist_*)."""
+import ctypes as C
+
+import numpy as np
+
+from ._lib import H, check, lib
+
+
+def partition_owner(bt, nranks):
+    """Owning rank per cluster node (-1 = replicated top level); host only."""
+    out = np.empty(bt.tree.num_nodes, np.int32)
+    check(lib.h2c_partition_owner(bt._h, int(nranks), out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def partition_exchange(bt, symmetric, up_ranks, nranks, src, dst, transpose=False):
+    """Items rank dst receives from rank src: list of (arr, node, rows); host only."""
+    ur = np.ascontiguousarray(up_ranks, np.int32)
+    cnt = C.c_int64()
+    check(lib.h2c_partition_exchange(bt._h, int(symmetric), int(transpose), ur.ctypes.data_as(C.c_void_p),
+                                     int(nranks), int(src), int(dst), C.byref(cnt), None, None, None))
+    arr = np.empty(cnt.value, np.int32)
+    node = np.empty(cnt.value, np.int32)
+    rows = np.empty(cnt.value, np.int64)
+    if cnt.value:
+        check(lib.h2c_partition_exchange(bt._h, int(symmetric), int(transpose), ur.ctypes.data_as(C.c_void_p),
+                                         int(nranks), int(src), int(dst), C.byref(cnt),
+                                         arr.ctypes.data_as(C.c_void_p), node.ctypes.data_as(C.c_void_p),
+                                         rows.ctypes.data_as(C.c_void_p)))
+    return list(zip(arr.tolist(), node.tolist(), rows.tolist()))
+
+
+class DistPlan:
+    """h2c_dist_plan: this rank's share of y = H x."""
+
+    def __init__(self, m, nranks, rank, transpose=False):
+        h = H()
+        check(lib.h2c_dist_plan_create(m._h, int(transpose), int(nranks), int(rank), C.byref(h)))
+        self._h = h
+        self.matrix = m
+        self.nranks, self.rank = int(nranks), int(rank)
+        s = np.zeros(nranks, np.int64)
+        r = np.zeros(nranks, np.int64)
+        ob, orows = C.c_int64(), C.c_int64()
+        check(lib.h2c_dist_plan_counts(h, s.ctypes.data_as(C.c_void_p), r.ctypes.data_as(C.c_void_p),
+                                       C.byref(ob), C.byref(orows)))
+        self.send_rows, self.recv_rows = s, r
+        self.owned_begin, self.owned_rows = ob.value, orows.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.h2c_dist_plan_destroy(self._h)
+            self._h = None
+
+    def begin(self, x, sendbuf, b, stream=None):
+        check(lib.h2c_dist_hgemv_begin(self._h, int(b), x.data_ptr(), x.stride(1) if x.dim() == 2 else x.shape[0],
+                                       sendbuf.data_ptr(), stream))
+
+    def end(self, recvbuf, y, b, alpha=1.0, beta=0.0, stream=None):
+        check(lib.h2c_dist_hgemv_end(self._h, int(b), recvbuf.data_ptr(), y.data_ptr(),
+                                     y.stride(1) if y.dim() == 2 else y.shape[0], float(alpha), float(beta), stream))
+
+
+class ShardedHgemv:
+    """y = alpha H x + beta y for this rank's rows, exchange over torch.distributed.
+
+    x, y: column-major (n x b, stride(0) == 1) float64 CUDA tensors holding the
+    full user-ordered vectors; only owned rows of x are read and of y written."""
+
+    def __init__(self, m, group=None, transpose=False):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.plan = DistPlan(m, world, rank, transpose)
+        self._bufs = {}
+
+    def _buffers(self, b, device):
+        import torch
+        key = (b, str(device))
+        if key not in self._bufs:
+            self._bufs[key] = (torch.empty(max(1, int(self.plan.send_rows.sum()) * b), dtype=torch.float64, device=device),
+                               torch.empty(max(1, int(self.plan.recv_rows.sum()) * b), dtype=torch.float64, device=device))
+        return self._bufs[key]
+
+    def __call__(self, x, y, alpha=1.0, beta=0.0):
+        import torch
+        b = x.shape[1] if x.dim() == 2 else 1
+        send, recv = self._buffers(b, x.device)
+        s = torch.cuda.current_stream(x.device).cuda_stream
+        self.plan.begin(x, send, b, s)
+        if self.plan.nranks > 1:
+            self.dist.all_to_all_single(recv[:int(self.plan.recv_rows.sum()) * b], send[:int(self.plan.send_rows.sum()) * b],
+                                        output_split_sizes=[int(v) * b for v in self.plan.recv_rows],
+                                        input_split_sizes=[int(v) * b for v in self.plan.send_rows], group=self.group)
+        self.plan.end(recv, y, b, alpha, beta, s)
