@@ -1,0 +1,338 @@
+// h2b200.hpp — C++ host API of the B200 H^2 hot path, mirroring the reference's
+// header API (proj/include/h2/*.hpp) over the C ABI in h2c.h. Header-only; link
+// with paper_2003_10173_b200/lib/libh2b200.so.
+//
+// Names, argument meaning and exception types follow the reference:
+//   build_cluster_tree / build_block_tree   cluster_tree.hpp:186-188, block_tree.hpp:120-124
+//   H2Matrix::matvec / matvec_transpose     h2_matrix.hpp:108-124 (user and internal ordering)
+//   LinearOperator, DenseOperator,          linear_operator.hpp:20-115
+//   H2Operator, make_operator
+//   pnorm_estimate(op, 2)                   linear_operator.hpp:127-153
+//   orthogonalize / recompress              algebra.hpp:72-226
+//   PeelConfig / peel_construct /           construction.hpp:23-382, 537-546
+//   estimate_relative_error, max_rank_error
+// Matrices are any column-major type with rows(), cols() and data() (e.g.
+// Eigen::MatrixXd, or h2::Matrix below); results come back as the same type.
+// Everything numeric runs on the current CUDA device; nothing falls back to
+// the CPU.
+#ifndef H2B200_HPP
+#define H2B200_HPP
+
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "h2c.h"
+
+namespace h2 {
+inline namespace b200 {
+
+using Index = std::int64_t;
+
+enum class Ordering { user, internal };      // types.hpp:19
+enum class Admissibility { strong, weak };   // block_tree.hpp:18-27
+
+// construction.hpp:61-66
+class max_rank_error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == H2C_OK) return;
+    const std::string msg = h2c_last_error();
+    switch (rc) {
+        case H2C_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case H2C_LOGIC_ERROR: throw std::logic_error(msg);
+        case H2C_MAX_RANK_ERROR: throw max_rank_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+}  // namespace detail
+
+// minimal column-major matrix (stands in for Eigen::MatrixXd when Eigen is absent)
+class Matrix {
+public:
+    Matrix() = default;
+    Matrix(Index r, Index c) : r_(r), c_(c), d_(static_cast<size_t>(r * c), 0.0) {}
+    static Matrix Identity(Index n, Index m) {
+        Matrix a(n, m);
+        for (Index i = 0; i < std::min(n, m); ++i) a(i, i) = 1.0;
+        return a;
+    }
+    Index rows() const { return r_; }
+    Index cols() const { return c_; }
+    double* data() { return d_.data(); }
+    const double* data() const { return d_.data(); }
+    double& operator()(Index i, Index j) { return d_[static_cast<size_t>(i + j * r_)]; }
+    double operator()(Index i, Index j) const { return d_[static_cast<size_t>(i + j * r_)]; }
+
+private:
+    Index r_ = 0, c_ = 0;
+    std::vector<double> d_;
+};
+
+// PointSet (point_set.hpp:18-63): n points of dimension d <= 3, column-major n x d
+struct PointSet {
+    Index n = 0;
+    int dim = 0;
+    std::vector<double> coords;
+    PointSet(Index n_, int d, std::vector<double> c) : n(n_), dim(d), coords(std::move(c)) {}
+};
+
+class ClusterTree {
+public:
+    ClusterTree(const PointSet& p, Index leaf) {
+        detail::check(h2c_cluster_tree_create(p.coords.data(), p.n, p.dim, leaf, &h_));
+        int dim = 0, nn = 0, nl = 0;
+        detail::check(h2c_cluster_tree_info(h_, &n_, &dim, &depth_, &nn, &nl));
+        nodes_ = nn;
+    }
+    ~ClusterTree() { h2c_cluster_tree_destroy(h_); }
+    ClusterTree(const ClusterTree&) = delete;
+    ClusterTree& operator=(const ClusterTree&) = delete;
+    Index n() const { return n_; }
+    int depth() const { return depth_; }
+    int num_nodes() const { return nodes_; }
+    h2c_cluster_tree handle() const { return h_; }
+
+private:
+    h2c_cluster_tree h_ = nullptr;
+    int64_t n_ = 0;
+    int depth_ = 0, nodes_ = 0;
+};
+
+inline std::shared_ptr<const ClusterTree> build_cluster_tree(const PointSet& p, Index leaf) {
+    return std::make_shared<const ClusterTree>(p, leaf);
+}
+
+class BlockTree {
+public:
+    BlockTree(std::shared_ptr<const ClusterTree> t, double eta, Admissibility mode) : tree_(std::move(t)) {
+        detail::check(h2c_block_tree_create(tree_->handle(), eta, mode == Admissibility::weak ? 1 : 0, &h_));
+    }
+    ~BlockTree() { h2c_block_tree_destroy(h_); }
+    BlockTree(const BlockTree&) = delete;
+    BlockTree& operator=(const BlockTree&) = delete;
+    Index n() const { return tree_->n(); }
+    const ClusterTree& row_tree() const { return *tree_; }
+    h2c_block_tree handle() const { return h_; }
+
+private:
+    std::shared_ptr<const ClusterTree> tree_;
+    h2c_block_tree h_ = nullptr;
+};
+
+inline std::shared_ptr<const BlockTree> build_block_tree(std::shared_ptr<const ClusterTree> rows,
+                                                         std::shared_ptr<const ClusterTree> cols, double eta,
+                                                         Admissibility mode = Admissibility::strong) {
+    if (rows != cols) throw std::invalid_argument("block tree: the B200 path requires identical row and column trees");
+    return std::make_shared<const BlockTree>(std::move(rows), eta, mode);
+}
+
+// device-resident H^2 matrix (h2_matrix.hpp:40-306); value semantics via shared ownership
+class H2Matrix {
+public:
+    H2Matrix() = default;
+    H2Matrix(h2c_matrix h, std::shared_ptr<const BlockTree> bt)
+        : blocks(std::move(bt)), h_(h, [](h2c_matrix p) { h2c_matrix_destroy(p); }) {}
+    static H2Matrix zero(std::shared_ptr<const BlockTree> bt, bool symmetric) {   // :53-75
+        h2c_matrix h = nullptr;
+        detail::check(h2c_matrix_create(bt->handle(), symmetric ? 1 : 0, nullptr, nullptr, &h));
+        return H2Matrix(h, std::move(bt));
+    }
+    Index n() const { return blocks->n(); }
+    bool symmetric() const {
+        int64_t n = 0;
+        int s = 0, o = 0;
+        detail::check(h2c_matrix_info(h_.get(), &n, &s, &o));
+        return s != 0;
+    }
+    // y = op(H) x by value (:112-124); M: rows()/cols()/data() column-major
+    template <class M>
+    M matvec(const M& x) const { return apply(x, false, Ordering::user); }
+    template <class M>
+    M matvec_transpose(const M& x) const { return apply(x, true, Ordering::user); }
+    template <class M>
+    M matvec_internal(const M& x) const { return apply(x, false, Ordering::internal); }
+    template <class M>
+    M matvec_transpose_internal(const M& x) const { return apply(x, true, Ordering::internal); }
+    // device buffers: y = alpha op(H) x + beta y (the hot path, no host copies)
+    void hgemv(bool transpose, Ordering ord, Index b, const double* x_dev, Index ldx, double* y_dev, Index ldy,
+               double alpha = 1.0, double beta = 0.0, void* stream = nullptr) const {
+        detail::check(h2c_hgemv(h_.get(), transpose ? 1 : 0, ord == Ordering::internal ? 1 : 0, n(), b, x_dev, ldx,
+                                y_dev, ldy, alpha, beta, stream));
+    }
+    std::vector<int> row_ranks() const {
+        std::vector<int> r(static_cast<size_t>(blocks->row_tree().num_nodes()));
+        detail::check(h2c_matrix_ranks(h_.get(), r.data(), nullptr));
+        return r;
+    }
+    h2c_matrix handle() const { return h_.get(); }
+
+    std::shared_ptr<const BlockTree> blocks;
+
+private:
+    template <class M>
+    M apply(const M& x, bool t, Ordering ord) const {
+        if (x.rows() != n() || x.cols() < 1) throw std::invalid_argument("matvec: dimension mismatch");
+        M y(x.rows(), x.cols());
+        detail::check(h2c_matvec_host(h_.get(), t ? 1 : 0, ord == Ordering::internal ? 1 : 0, x.rows(), x.cols(),
+                                      x.data(), y.data()));
+        return y;
+    }
+    std::shared_ptr<h2c_matrix_s> h_;
+};
+
+inline H2Matrix orthogonalize(const H2Matrix& h) {   // algebra.hpp:72-113
+    h2c_matrix o = nullptr;
+    detail::check(h2c_orthogonalize(h.handle(), &o));
+    return H2Matrix(o, h.blocks);
+}
+inline H2Matrix recompress(const H2Matrix& h, double eps) {   // algebra.hpp:144-226
+    h2c_matrix o = nullptr;
+    detail::check(h2c_recompress(h.handle(), eps, &o));
+    return H2Matrix(o, h.blocks);
+}
+
+// LinearOperator (linear_operator.hpp:20-55): apply on host matrices (user order)
+class LinearOperator {
+public:
+    explicit LinearOperator(h2c_operator h, Index n, bool sym, std::shared_ptr<void> keep = {})
+        : h_(h, [](h2c_operator p) { h2c_operator_destroy(p); }), n_(n), sym_(sym), keep_(std::move(keep)) {}
+    Index dim() const { return n_; }
+    bool symmetric() const { return sym_; }
+    long columns_applied() const {
+        int64_t c = 0;
+        detail::check(h2c_operator_columns_applied(h_.get(), &c));
+        return long(c);
+    }
+    void reset_counter() const { detail::check(h2c_operator_reset_counter(h_.get())); }
+    h2c_operator handle() const { return h_.get(); }
+
+private:
+    std::shared_ptr<h2c_operator_s> h_;
+    Index n_;
+    bool sym_;
+    std::shared_ptr<void> keep_;
+};
+
+// DenseOperator (linear_operator.hpp:86-101)
+template <class M>
+LinearOperator DenseOperator(const M& a, bool sym = false) {
+    if (a.rows() != a.cols()) throw std::invalid_argument("dense operator: square only");
+    h2c_operator h = nullptr;
+    detail::check(h2c_operator_dense(a.data(), a.rows(), sym ? 1 : 0, &h));
+    return LinearOperator(h, a.rows(), sym);
+}
+// H2Operator (linear_operator.hpp:104-115)
+inline LinearOperator H2Operator(const H2Matrix& m) {
+    h2c_operator h = nullptr;
+    detail::check(h2c_operator_h2(m.handle(), &h));
+    return LinearOperator(h, m.n(), m.symmetric(), std::make_shared<H2Matrix>(m));
+}
+// make_operator (linear_operator.hpp:80-84): host functions on h2::Matrix (n x b, user order)
+using HostFn = std::function<Matrix(const Matrix&)>;
+inline LinearOperator make_operator(Index n, bool sym, HostFn f, HostFn t = nullptr) {
+    struct Ctx {
+        Index n;
+        HostFn f, t;
+    };
+    auto ctx = std::make_shared<Ctx>(Ctx{n, std::move(f), std::move(t)});
+    auto cb = [](void* c, int transpose, int64_t b, const double* x, double* y, void*) -> int {
+        try {
+            auto* cx = static_cast<Ctx*>(c);
+            Matrix xm(cx->n, b);
+            std::copy(x, x + cx->n * b, xm.data());
+            const Matrix ym = transpose ? cx->t(xm) : cx->f(xm);
+            if (ym.rows() != cx->n || ym.cols() != b) return 1;
+            std::copy(ym.data(), ym.data() + cx->n * b, y);
+            return 0;
+        } catch (...) {
+            return 1;
+        }
+    };
+    h2c_operator h = nullptr;
+    detail::check(h2c_operator_host_callback(n, sym ? 1 : 0, ctx->t ? 1 : 0, cb, ctx.get(), &h));
+    return LinearOperator(h, n, sym, ctx);
+}
+
+struct NormEstimate {
+    double value = 0;
+    int iterations = 0;
+};
+inline NormEstimate pnorm_estimate(const LinearOperator& op, double p) {   // linear_operator.hpp:127-153
+    if (p != 2.0) throw std::invalid_argument("pnorm_estimate: the B200 path implements p = 2");
+    NormEstimate e;
+    detail::check(h2c_pnorm2_estimate(op.handle(), &e.value, &e.iterations));
+    return e;
+}
+
+struct PeelConfig {   // construction.hpp:23-31
+    double eps = 1e-4;
+    Index sample_block_size = 16;
+    Index oversampling = 10;
+    Index max_rank = 0;
+    std::uint64_t seed = 42;
+    double norm_scale = 0;
+    Index crossover_rank_cap = 128;
+    int rng = 0;   // B200 extension: 0 reference host stream, 1 device Philox
+};
+struct LevelStats {
+    int level = 0;
+    Index blocks = 0, max_rank = 0;
+    long samples = 0;
+};
+struct SampleStats {   // construction.hpp:40-59
+    long total = 0;
+    std::vector<LevelStats> levels;
+    bool consistent() const {
+        long s = 0;
+        for (const auto& l : levels) s += l.samples;
+        return s == total;
+    }
+};
+struct PeelResult {   // construction.hpp:295-298
+    H2Matrix matrix;
+    SampleStats stats;
+};
+
+inline PeelResult peel_construct(const LinearOperator& op, std::shared_ptr<const BlockTree> bt,
+                                 const PeelConfig& cfg) {   // construction.hpp:300-382
+    h2c_peel_config c;
+    c.eps = cfg.eps;
+    c.sample_block_size = cfg.sample_block_size;
+    c.oversampling = cfg.oversampling;
+    c.max_rank = cfg.max_rank;
+    c.seed = cfg.seed;
+    c.norm_scale = cfg.norm_scale;
+    c.crossover_rank_cap = cfg.crossover_rank_cap;
+    c.rng = cfg.rng;
+    h2c_matrix h = nullptr;
+    int64_t total = 0;
+    std::vector<h2c_level_stats> lv(128);
+    int nl = 0;
+    detail::check(h2c_peel_construct(op.handle(), bt->handle(), &c, &h, &total, lv.data(), int(lv.size()), &nl,
+                                     nullptr, nullptr));
+    PeelResult r{H2Matrix(h, bt), {}};
+    r.stats.total = long(total);
+    for (int i = 0; i < nl; ++i) r.stats.levels.push_back({lv[size_t(i)].level, lv[size_t(i)].blocks,
+                                                           lv[size_t(i)].max_rank, long(lv[size_t(i)].samples)});
+    return r;
+}
+
+inline double estimate_relative_error(const LinearOperator& op, const H2Matrix& h, double op_norm = 0) {
+    double v = 0;   // construction.hpp:537-546
+    detail::check(h2c_estimate_relative_error(op.handle(), h.handle(), op_norm, &v));
+    return v;
+}
+
+}  // namespace b200
+}  // namespace h2
+
+#endif  // H2B200_HPP
