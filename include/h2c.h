@@ -102,6 +102,12 @@ int h2c_hgemv(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, c
 /* the same with HOST buffers: H2D copy, hgemv, D2H copy (the drop-in for the
  * by-value Matrix H2Matrix::matvec(const Matrix&)) */
 int h2c_matvec_host(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, double* y);
+/* asynchronous host-buffer matvec on `stream`: H2D of x (pinned host memory
+ * for overlap), hgemv, D2H of y, all enqueued without waiting; the caller
+ * synchronises the stream. Workspace is per stream, so successive calls on
+ * alternating streams overlap one call's copies with another's compute. */
+int h2c_matvec_host_async(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, double* y,
+                          void* stream);
 /* number of kernel launches one hgemv issues (gather + stage launches) */
 int h2c_hgemv_launches(h2c_matrix h, int transpose, int64_t b, int* launches);
 /* one hgemv (alpha 1, beta 0) with a CUDA event around every launch on `stream`:

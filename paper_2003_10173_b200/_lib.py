@@ -68,6 +68,7 @@ _sig("h2c_matrix_download", i32, H, vp, vp, vp, vp, vp, vp)
 _sig("h2c_matrix_kernel", i32, H, vp, i32, f64, i32, P(H))
 _sig("h2c_hgemv", i32, H, i32, i32, i64, i64, vp, i64, vp, i64, f64, f64, vp)
 _sig("h2c_matvec_host", i32, H, i32, i32, i64, i64, vp, vp)
+_sig("h2c_matvec_host_async", i32, H, i32, i32, i64, i64, vp, vp, vp)
 _sig("h2c_hgemv_launches", i32, H, i32, i64, P(i32))
 
 def check(rc):

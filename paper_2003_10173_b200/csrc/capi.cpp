@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "h2dev.hpp"
@@ -17,7 +19,18 @@ struct h2c_block_tree_s {
 };
 struct h2c_matrix_s {
     std::unique_ptr<h2b::H2Dev> h;
-    h2b::Workspace ws;
+    h2b::Workspace ws;   // legacy-stream calls and timing
+    // hgemv workspace per stream: the matrix and its plans are immutable and
+    // shared, scratch (x blocked, x-hat, y-hat, host staging) is per stream
+    std::mutex mu;
+    std::map<cudaStream_t, std::unique_ptr<h2b::Workspace>> per_stream;
+    h2b::Workspace& ws_for(cudaStream_t s) {
+        if (s == nullptr) return ws;
+        std::lock_guard<std::mutex> g(mu);
+        auto& w = per_stream[s];
+        if (!w) w = std::make_unique<h2b::Workspace>();
+        return *w;
+    }
 };
 struct h2c_dist_plan_s {
     std::shared_ptr<h2b::DistPlan> p;
@@ -161,6 +174,10 @@ int h2c_matrix_create(h2c_block_tree b, int symmetric, const int* row_ranks, con
 }
 void h2c_matrix_destroy(h2c_matrix h) {
     if (h) cudaDeviceSynchronize();   // device work on any stream may still read it
+    if (h) {
+        // per-stream scratch is freed on its own stream; drop it while those streams still exist
+        for (auto& kv : h->per_stream) kv.second.reset();
+    }
     delete h;
 }
 
@@ -239,7 +256,7 @@ int h2c_hgemv(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, c
         need(ordering == 0 || ordering == 1, "ordering must be 0 (user) or 1 (internal)");
         need(x != nullptr && y != nullptr, "null vector pointer");
         h2b::hgemv(*h->h, transpose != 0, ordering == 0, n, b, x, ldx, y, ldy, alpha, beta,
-                   static_cast<cudaStream_t>(stream), h->ws);
+                   static_cast<cudaStream_t>(stream), h->ws_for(static_cast<cudaStream_t>(stream)));
     });
 }
 
@@ -257,6 +274,24 @@ int h2c_matvec_host(h2c_matrix h, int transpose, int ordering, int64_t n, int64_
                    nullptr, h->ws);
         H2B_CUDA(cudaMemcpyAsync(y, h->ws.hy.data(), cnt * sizeof(double), cudaMemcpyDeviceToHost, nullptr));
         H2B_CUDA(cudaStreamSynchronize(nullptr));
+    });
+}
+
+int h2c_matvec_host_async(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, double* y,
+                          void* stream) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        need(x != nullptr && y != nullptr, "null vector pointer");
+        if (n != h->h->tree().n) throw std::invalid_argument("matvec: dimension mismatch");
+        if (b < 1) throw std::invalid_argument("matvec: need at least one column");
+        auto s = static_cast<cudaStream_t>(stream);
+        h2b::Workspace& w = h->ws_for(s);
+        const size_t cnt = size_t(n * b);
+        if (w.hx.size() < cnt) w.hx.resize(cnt, s);
+        if (w.hy.size() < cnt) w.hy.resize(cnt, s);
+        H2B_CUDA(cudaMemcpyAsync(w.hx.data(), x, cnt * sizeof(double), cudaMemcpyHostToDevice, s));
+        h2b::hgemv(*h->h, transpose != 0, ordering == 0, n, b, w.hx.data(), n, w.hy.data(), n, 1.0, 0.0, s, w);
+        H2B_CUDA(cudaMemcpyAsync(y, w.hy.data(), cnt * sizeof(double), cudaMemcpyDeviceToHost, s));
     });
 }
 
