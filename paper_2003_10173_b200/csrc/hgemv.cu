@@ -364,6 +364,10 @@ struct PlanBuilder {
                 tasks.push_back(tk);
             }
         }
+        // longest tasks first (stable: equal-cost tasks keep tree order for L2 locality)
+        // so the last wave is made of short tasks
+        std::stable_sort(tasks.begin() + ld.task_begin, tasks.end(),
+                         [](const SegTask& a, const SegTask& b) { return a.nsteps > b.nsteps; });
         ld.vec = vec;
         ld.units_even = ue;
         ld.task_end = int(tasks.size());
