@@ -145,6 +145,26 @@ def dist_setup(args):
     return world, rank, local, pg
 
 
+def algorithmic_flops(m, bt, b):
+    """Reference flop count of one hgemv: F = 2b(2 sum_leaf m k + 2 sum_nonroot k k_par
+    + sum_adm k_r k_c + sum_dense m_r m_c), both orientations of every block; also the stage-5 part
+    (dense near-field + leaf expansion)."""
+    ct = bt.tree
+    r, _ = m.ranks()
+    r = r.astype(np.float64)
+    size = (ct.end - ct.begin).astype(np.float64)
+    leaves = ct.leaves
+    nonroot = np.nonzero(ct.parent >= 0)[0]
+    adm, dense = bt.admissible_leaves, bt.dense_leaves
+    leaf_t = float(np.sum(size[leaves] * r[leaves]))
+    xfer = float(np.sum(r[nonroot] * r[ct.parent[nonroot]]))
+    coup = float(np.sum(r[bt.row[adm]] * r[bt.col[adm]]))
+    dns = float(np.sum(size[bt.row[dense]] * size[bt.col[dense]]))
+    total = 2.0 * b * (2 * leaf_t + 2 * xfer + coup + dns)
+    stage5 = 2.0 * b * (leaf_t + dns)
+    return total, stage5
+
+
 def algorithmic_work(m, b, launches_stats=None):
     """F (flops) and B (bytes) of one hgemv per SURVEY §8(d)."""
     sizes = m.packed_sizes()   # U, E, V, F, S, D (doubles)
@@ -216,7 +236,7 @@ def run_b200(args, cfg, world, rank, local, dist):
     nrep = max(3, min(args.steps, 10)) - 1
     stages = {k: {"ms": v[0] / nrep, "gflop": v[1] / nrep / 1e9, "gbytes": v[2] / nrep / 1e9,
                   "launches": v[3] // nrep} for k, v in agg.items()}
-    F = sum(v[1] for v in agg.values()) / nrep
+    F, F5 = algorithmic_flops(m, bt, b)
     Bbytes = algorithmic_work(m, b)
     launches = m.launches(b)
 
@@ -241,8 +261,11 @@ def run_b200(args, cfg, world, rank, local, dist):
     value = F / t_step / 1e9          # one hgemv of the whole matrix per step (all ranks together)
     gbs = Bbytes / t_step / 1e9
 
-    # dominant kernel roofline: leaf expansion + dense near-field (stage 5)
-    dom = stages[5]
+    # dominant kernel roofline: leaf expansion + dense near-field (stage 5); algorithmic flops of the
+    # reference for that stage (the kernel also applies U_t E_t, the folded finest downsweep step)
+    dom = dict(stages[5])
+    dom["kernel_gflop"] = dom["gflop"]
+    dom["gflop"] = F5 / 1e9
     hbm, hbm_src = hbm_peak()
     ai = dom["gflop"] / max(dom["gbytes"], 1e-30)
     ridge = FP64_PEAK_TFLOPS * 1e3 / hbm
@@ -295,6 +318,8 @@ def run_b200(args, cfg, world, rank, local, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
     # the synchronous by-value call (H2D, hgemv, D2H, wait) for reference
+    for _ in range(3):
+        check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
     t0 = time.perf_counter()
     for _ in range(3):
         check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
@@ -500,11 +525,16 @@ def main():
     ap.add_argument("--hara-rng", default="device", choices=["device", "reference"],
                     help="cfg3 Gaussian panels: device Philox (perf) or the reference host stream")
     ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes/launch of the dominant kernel from an ncu --set full capture")
+                    help="dram bytes/launch of the dominant kernel from an ncu --set full capture "
+                         "(default for cfg2: the committed capture, profiles/ncu_full_cfg2_r01_v1.txt)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.traffic is None and args.config == "cfg2":
+        # ncu --set full of the stage-5 kernel (dram__bytes_read.sum + dram__bytes_write.sum):
+        # 10.639 GB + 0.266 GB per launch, profiles/ncu_full_cfg2_r01_v1.txt
+        args.traffic = 10.638945e9 + 0.266123e9
     world, rank, local, dist = dist_setup(args)
     if cfg.get("hara"):
         if args.impl == "reference":

@@ -51,9 +51,34 @@ struct H2Dev {
 };
 
 // per-call scratch (x in internal blocked layout, upsweep / downsweep coefficients)
+// A repeated hgemv with identical arguments replays a captured CUDA graph of
+// its ~30 launches (captured on the second identical call)
+struct HgemvGraph {
+    struct Key {
+        uint64_t plan = 0;
+        bool transpose = false, user = false;
+        int64_t n = 0, b = 0, ldx = 0, ldy = 0;
+        const double* x = nullptr;
+        double* y = nullptr;
+        double alpha = 0, beta = 0;
+        bool operator==(const Key& o) const {
+            return plan == o.plan && transpose == o.transpose && user == o.user && n == o.n && b == o.b &&
+                   ldx == o.ldx && ldy == o.ldy && x == o.x && y == o.y && alpha == o.alpha && beta == o.beta;
+        }
+    };
+    Key key, last;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cap = nullptr;
+    ~HgemvGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (cap) cudaStreamDestroy(cap);
+    }
+};
+
 struct Workspace {
     DeviceArray<double> xint, xhat, yhat;
     DeviceArray<double> hx, hy;   // staging of the host-buffer entry point
+    HgemvGraph graph;
 };
 
 void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,

@@ -44,7 +44,7 @@ def test_hgemv_matches_oracle(cuda, tree, sym, kmax):
     kmax = min(kmax, leaf)
     ora, m, _ = pair(pts, leaf, weak, sym, kmax, seed=2)
     n = pts.shape[0]
-    for b in (1, 5, 16, 33):
+    for b in (1, 5, 16, 32, 33, 64, 70):
         x = O.gaussian(100 + b, n, b)
         for transpose in (False, True):
             for ordering in (0, 1):

@@ -63,6 +63,16 @@ int main() {
         fl = 2.0 * 8 * 256 * iters * (double)blocks * (threads / 32);
         printf("DMMA threads=%d: %.2f TFLOP/s\n", threads, fl / ms / 1e9);
     }
+    // DMMA throughput vs resident warps per SM (8 independent accumulators per warp)
+    for (int w : {1, 2, 4, 8, 12, 16, 24, 32}) {
+        const int blocks = sms * w, iters = 4096;
+        dmma_kernel<<<blocks, 32>>>(out, 64);
+        cudaEventRecord(e0);
+        dmma_kernel<<<blocks, 32>>>(out, iters);
+        cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+        const double fl = 2.0 * 8 * 256 * iters * (double)blocks;
+        printf("DMMA warps/SM=%d: %.2f TFLOP/s\n", w, fl / ms / 1e9);
+    }
     size_t n = (size_t)1 << 28;  // 2 GiB of doubles per buffer
     double2 *a, *b; CK(cudaMalloc(&a, n * 8)); CK(cudaMalloc(&b, n * 8));
     cudaMemset(a, 0, n * 8);

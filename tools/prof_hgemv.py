@@ -22,7 +22,14 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=list(bench.CONFIGS))
     ap.add_argument("--b", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--tune", default="", help="h2b_tune values for slots 0,1,2 (e.g. 0,0,2)")
     a = ap.parse_args()
+    if a.tune:
+        import ctypes as C
+        from paper_2003_10173_b200._lib import lib
+        lib.h2b_tune.argtypes = [C.c_int, C.c_int]
+        for i, v in enumerate(a.tune.split(",")):
+            lib.h2b_tune(i, int(v))
     cfg = bench.CONFIGS[a.config]
     b = a.b or cfg["b"]
     pts = bench.grid_points(cfg["grid"])

@@ -47,8 +47,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2", choices=list(bench.CONFIGS))
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--dense", default="0,1,2,3,4,5")
-    ap.add_argument("--coupling", default="0,1,2,3,4,5")
+    ap.add_argument("--dense", default="0,1")
+    ap.add_argument("--coupling", default="0,1")
+    ap.add_argument("--ws", default="", help="warp-specialised kernel variants (h2b_tune(2, v)); 0 = off")
     a = ap.parse_args()
     lib.h2b_tune.argtypes = [C.c_int, C.c_int]
     lib.h2b_tune.restype = C.c_int
@@ -63,8 +64,20 @@ def main():
     y = torch.empty(b, n, dtype=torch.float64, device="cuda").t()
     lib.h2b_tune(0, 0)
     lib.h2b_tune(1, 0)
+    lib.h2b_tune(2, 0)
     m.hgemv(x, y)
     y0 = y.clone()
+    for v in [int(q) for q in a.ws.split(",") if q]:
+        lib.h2b_tune(2, v)
+        m.hgemv(x, y)
+        torch.cuda.synchronize()
+        diff = float((y - y0).abs().max() / y0.abs().max())
+        agg = stage_times(m, x, y, n, b, a.reps)
+        tot = sum(s_[0] for s_ in agg.values())
+        line = " ".join(f"s{k}={agg[k][0]:.3f}ms({agg[k][1] / agg[k][0] / 1e9:.1f}TF)" for k in sorted(agg)
+                        if agg[k][1] > 0)
+        print(f"ws v{v}: total {tot:.3f} ms  {line}  maxdiff {diff:.1e}", flush=True)
+    lib.h2b_tune(2, 0)
     for which, vals in ((0, a.dense), (1, a.coupling)):
         for v in [int(s) for s in vals.split(",")]:
             lib.h2b_tune(0, 0)
