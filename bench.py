@@ -451,11 +451,16 @@ def run_hara(args, cfg, world, rank, local, dist):
     if dist:
         dist.barrier()
     steps = max(1, min(args.steps, 3))
+    import ctypes as C
+    from paper_2003_10173_b200._lib import lib as _l
+    _l.h2b_plan_build_ms.restype = C.c_double
+    _l.h2b_plan_build_ms.argtypes = [C.c_int]
     times, opms = [], []
     with ClockSampler(local) as clk:
         for _ in range(steps):
             op.reset_counter()
             torch.cuda.synchronize()
+            _l.h2b_plan_build_ms(1)
             t0 = time.perf_counter()
             res = peel_construct(op, bt, pc)
             torch.cuda.synchronize()
@@ -466,12 +471,13 @@ def run_hara(args, cfg, world, rank, local, dist):
         tt = torch.tensor([t], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    import ctypes as C
-    from paper_2003_10173_b200._lib import lib as _l
+    plan_ms = _l.h2b_plan_build_ms(0)
     ph = (C.c_double * 8)()
     _l.h2b_hara_phase_ms(ph, 8)
     phases = dict(zip(["rng", "op_apply", "residual_hgemv", "absorb", "transposed_pass", "local_updates",
                        "recompress", "dense_leaves"], [round(v / 1e3, 4) for v in ph]))
+    phases["hgemv_plan_builds"] = round(plan_ms / 1e3, 4)
+    phases["all_steps_s"] = [round(v, 4) for v in times]
     err = estimate_relative_error(op, res.matrix)
     prof = [int(v) for v in res.matrix.rank_profile()]
     out = {"metric": "HARA build time (N=2^18, tol 1e-6)", "value": t, "unit": "s", "n_gpus": world,

@@ -6,6 +6,9 @@
 // leaf/dense epilogue together with alpha/beta.
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <chrono>
 #include <cstring>
 #include <unordered_set>
 
@@ -474,9 +477,13 @@ struct LaunchDesc {
 struct HgemvPlan {
     uint64_t id = 0;   // unique per plan (graph cache key)
     std::vector<LaunchDesc> launches;
+    // host copies for the (lazy) byte accounting of timed runs
+    std::vector<SegTask> htasks;
+    std::vector<SegEntry> hentries;
+    std::once_flag accounted;
     DeviceArray<SegTask> tasks;
     DeviceArray<SegEntry> entries;
-    DeviceArray<int> perm;
+    std::shared_ptr<const DeviceArray<int>> perm;   // shared by every plan on the same cluster tree
     DeviceArray<int64_t> leaf_begin;
     DeviceArray<int> leaf_m;
     int num_leaves = 0;
@@ -542,46 +549,27 @@ struct PlanBuilder {
             }
         }
         // longest tasks first (stable: equal-cost tasks keep tree order for L2 locality)
-        // so the last wave is made of short tasks
-        std::stable_sort(tasks.begin() + ld.task_begin, tasks.end(),
-                         [](const SegTask& a, const SegTask& b) { return a.nsteps > b.nsteps; });
+        // so the last wave is made of short tasks; counting sort on the chunk count
+        {
+            const int t0 = ld.task_begin, t1 = int(tasks.size());
+            int maxs = 0;
+            for (int i = t0; i < t1; ++i) maxs = std::max(maxs, tasks[size_t(i)].nsteps);
+            std::vector<int> cnt(size_t(maxs) + 2, 0);
+            for (int i = t0; i < t1; ++i) ++cnt[size_t(maxs - tasks[size_t(i)].nsteps) + 1];
+            for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+            std::vector<SegTask> sorted(size_t(t1 - t0));
+            for (int i = t0; i < t1; ++i)
+                sorted[size_t(cnt[size_t(maxs - tasks[size_t(i)].nsteps)]++)] = tasks[size_t(i)];
+            std::copy(sorted.begin(), sorted.end(), tasks.begin() + t0);
+        }
         ld.vec = vec;
         ld.units_even = ue;
         ld.task_end = int(tasks.size());
-        {
-            std::vector<const double*> as;
-            std::vector<int64_t> bs;
-            for (auto& p : outs) {
-                if (p.rows <= 0) continue;
-                ld.out_per_col += p.rows;
-                for (auto& e : p.es) {
-                    if (e.k <= 0) continue;
-                    ld.flops_per_col += 2.0 * p.rows * e.k;
-                    as.push_back(e.A);
-                    bs.push_back((int64_t(e.src) << 56) ^ e.b_unit);
-                }
-            }
-            // each distinct stored block is read once; each distinct B operand block once per column
-            std::vector<std::pair<const double*, double>> ab;
-            for (auto& p : outs) {
-                if (p.rows <= 0) continue;
-                for (auto& e : p.es)
-                    if (e.k > 0) ab.emplace_back(e.A, 8.0 * double(p.rows) * e.k);
-            }
-            std::sort(ab.begin(), ab.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
-            for (size_t i = 0; i < ab.size(); ++i)
-                if (i == 0 || ab[i].first != ab[i - 1].first) ld.payload_bytes += ab[i].second;
-            std::vector<std::pair<int64_t, int>> bk;
-            for (auto& p : outs) {
-                if (p.rows <= 0) continue;
-                for (auto& e : p.es)
-                    if (e.k > 0) bk.emplace_back((int64_t(e.src) << 56) ^ e.b_unit, e.k);
-            }
-            std::sort(bk.begin(), bk.end());
-            for (size_t i = 0; i < bk.size(); ++i)
-                if (i == 0 || bk[i].first != bk[i - 1].first) ld.bsrc_per_col += bk[i].second;
-            (void)as;
-            (void)bs;
+        for (auto& p : outs) {
+            if (p.rows <= 0) continue;
+            ld.out_per_col += p.rows;
+            for (auto& e : p.es)
+                if (e.k > 0) ld.flops_per_col += 2.0 * p.rows * e.k;
         }
         if (ld.task_end > ld.task_begin || zero_yhat) launches.push_back(ld);
     }
@@ -597,6 +585,26 @@ SegEntry make_entry(const double* A, int lda, int k, bool trans, int src, int64_
     e.b_unit = b_unit;
     e.ldb = ldb;
     return e;
+}
+
+// device copy of a cluster tree's permutation, cached per tree (HARA builds many
+// matrices on one tree; each plan would otherwise upload the same n indices)
+std::shared_ptr<const DeviceArray<int>> tree_perm(const std::shared_ptr<const ClusterTree>& t) {
+    static std::mutex mu;
+    static std::map<const ClusterTree*, std::pair<std::weak_ptr<const ClusterTree>,
+                                                  std::shared_ptr<const DeviceArray<int>>>> cache;
+    std::lock_guard<std::mutex> g(mu);
+    for (auto it = cache.begin(); it != cache.end();) {   // drop trees that no longer exist
+        if (it->second.first.expired()) it = cache.erase(it);
+        else ++it;
+    }
+    auto it = cache.find(t.get());
+    if (it != cache.end() && it->second.first.lock() == t) return it->second.second;
+    auto d = std::make_shared<DeviceArray<int>>();
+    std::vector<int> p32(t->perm.begin(), t->perm.end());
+    d->upload(p32);
+    cache[t.get()] = {t, d};
+    return d;
 }
 
 std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const DistSpec* ds = nullptr) {
@@ -749,8 +757,9 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     plan->launches = std::move(pb.launches);
     plan->tasks.upload(pb.tasks);
     plan->entries.upload(pb.entries);
-    std::vector<int> perm32(ct.perm.begin(), ct.perm.end());
-    plan->perm.upload(perm32);
+    plan->htasks = std::move(pb.tasks);
+    plan->hentries = std::move(pb.entries);
+    plan->perm = tree_perm(h.bt->tree);
     std::vector<int64_t> lb;
     std::vector<int> lm;
     for (int t : ct.leaves) {
@@ -766,10 +775,17 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     return plan;
 }
 
+double g_plan_build_ms = 0;   // host wall time spent building plans (diagnostics)
+
 std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
     std::lock_guard<std::mutex> g(h.plan_mu);
+    if (h.symmetric) transpose = false;   // op(H) = H: one plan serves both
     auto& p = h.plan[transpose ? 1 : 0];
-    if (!p) p = build_plan(h, transpose);
+    if (!p) {
+        const auto t0 = std::chrono::steady_clock::now();
+        p = build_plan(h, transpose);
+        g_plan_build_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
     return p;
 }
 
@@ -954,9 +970,42 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     H2B_CUDA(cudaGraphLaunch(g.exec, stream));
 }
 
+namespace {
+// distinct stored-payload bytes and B-operand rows per launch (the roofline
+// numerators of timed runs), computed once per plan from its host copies
+void account(HgemvPlan& p) {
+    std::call_once(p.accounted, [&p] {
+        for (LaunchDesc& ld : p.launches) {
+            std::vector<std::pair<const double*, double>> ab;
+            std::vector<std::pair<int64_t, int>> bk;
+            int last_e0 = -1;
+            for (int t = ld.task_begin; t < ld.task_end; ++t) {
+                const SegTask& tk = p.htasks[size_t(t)];
+                if (tk.e_begin == last_e0) continue;   // row tiles of one output share entries
+                last_e0 = tk.e_begin;
+                for (int e = tk.e_begin; e < tk.e_end; ++e) {
+                    const SegEntry& en = p.hentries[size_t(e)];
+                    ab.emplace_back(en.A, 8.0 * double(tk.rows) * en.k);
+                    bk.emplace_back((int64_t(en.src) << 56) ^ en.b_unit, en.k);
+                }
+            }
+            std::sort(ab.begin(), ab.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+            ld.payload_bytes = 0;
+            for (size_t i = 0; i < ab.size(); ++i)
+                if (i == 0 || ab[i].first != ab[i - 1].first) ld.payload_bytes += ab[i].second;
+            std::sort(bk.begin(), bk.end());
+            ld.bsrc_per_col = 0;
+            for (size_t i = 0; i < bk.size(); ++i)
+                if (i == 0 || bk[i].first != bk[i - 1].first) ld.bsrc_per_col += bk[i].second;
+        }
+    });
+}
+}  // namespace
+
 void hgemv_timed(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
                  double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
                  std::vector<StageRecord>& records) {
+    account(*get_plan(h, transpose));
     EventTimer t;
     std::vector<StageRecord> recs;
     t.out = &recs;
@@ -984,7 +1033,7 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     if (ws.xint.size() < need_x) ws.xint.resize(need_x, stream);
     if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1), stream);
     if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
-    const int* perm = user_order ? plan->perm.data() : nullptr;
+    const int* perm = user_order ? plan->perm->data() : nullptr;
     if ((phases & 1) && plan->num_leaves > 0) {
         if (timer) timer->mark(stream);
         gather_blocked_kernel<<<plan->num_leaves, 256, 0, stream>>>(x, ldx, perm, plan->leaf_begin.data(),
@@ -1224,4 +1273,11 @@ extern "C" int h2b_tune(int which, int value) {
     if (which < 0 || which > 3) return -1;
     h2b::g_tune[which] = value;
     return 0;
+}
+
+// diagnostics hook: accumulated plan-build host time (ms); reset when `reset` != 0
+extern "C" double h2b_plan_build_ms(int reset) {
+    const double v = h2b::g_plan_build_ms;
+    if (reset) h2b::g_plan_build_ms = 0;
+    return v;
 }
