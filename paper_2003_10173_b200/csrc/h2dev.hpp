@@ -42,11 +42,12 @@ struct H2Dev {
     void layout_blocks();              // s_off / d_off from ranks
 
     mutable std::mutex plan_mu;
-    mutable std::shared_ptr<HgemvPlan> plan[2];   // [transpose]
+    mutable std::shared_ptr<HgemvPlan> plan[3];   // [transpose], [2]: symmetric few-vector plan
     void invalidate_plans() {
         std::lock_guard<std::mutex> g(plan_mu);
         plan[0].reset();
         plan[1].reset();
+        plan[2].reset();
     }
 };
 
@@ -77,6 +78,7 @@ struct HgemvGraph {
 
 struct Workspace {
     DeviceArray<double> xint, xhat, yhat;
+    DeviceArray<double> scratch;   // per-block products of the symmetric few-vector path
     DeviceArray<double> hx, hy;   // staging of the host-buffer entry point
     HgemvGraph graph;
 };

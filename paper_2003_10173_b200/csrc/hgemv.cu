@@ -436,6 +436,279 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB) ws_gemm_kernel(SegAr
     }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric few-vector path (b <= 2): the product is HBM-bound, so every
+// canonical block is streamed ONCE and used for both orientations:
+//   u_b = A x_s  (row side)   and   w_b = A^T x_t  (column side)
+// are written to a per-block scratch slot; a second pass sums each output's
+// slots in a fixed order (deterministic, no atomics). One warp per block: lanes
+// own rows r and r+32; the column partials of A^T x_t are reduced 32 columns
+// at a time by a butterfly (31 shuffles per 32 columns).
+// ---------------------------------------------------------------------------
+struct SymBlock {
+    const double* A;
+    int lda, R, C;
+    int64_t xs_unit, xt_unit;   // rows (times b) of the source array: x_s (C x b), x_t (R x b)
+    int64_t u_off, w_off;       // scratch rows (times b); w_off < 0: diagonal block (no transpose part)
+};
+struct CsrUnit {
+    int rows;
+    int s0, s1;         // slot range
+    int64_t out_unit;   // y-hat offset / leaf begin (times b / rows)
+};
+
+template <int B>
+__global__ void __launch_bounds__(256) sym_pass_kernel(const SymBlock* __restrict__ blocks, int nblocks,
+                                                       const double* __restrict__ src, double* __restrict__ scratch,
+                                                       int64_t b) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (wid >= nblocks) return;
+    const SymBlock d = blocks[wid];
+    const int R = d.R, C = d.C;
+    const double* xs = src + d.xs_unit * b;
+    const double* xt = src + d.xt_unit * b;
+    const int r0 = lane, r1 = lane + 32;
+    const bool v0 = r0 < R, v1 = r1 < R;
+    double xt0[B], xt1[B], u0[B], u1[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+        xt0[q] = v0 ? xt[r0 + q * R] : 0.0;
+        xt1[q] = v1 ? xt[r1 + q * R] : 0.0;
+        u0[q] = u1[q] = 0.0;
+    }
+    const bool want_w = d.w_off >= 0;
+    double* w = want_w ? scratch + d.w_off * b : nullptr;
+    // 8 columns at a time: 16 independent loads per lane in flight, and the 8
+    // column partials of A^T x_t reduced across the warp with 9 shuffles
+#pragma unroll 2
+    for (int j0 = 0; j0 < C; j0 += 8) {
+        double p[8][B];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int j = j0 + jj;
+            const bool vj = j < C;
+            const double* col = d.A + int64_t(j) * d.lda;
+            const double a0 = (v0 && vj) ? __ldg(col + r0) : 0.0;
+            const double a1 = (v1 && vj) ? __ldg(col + r1) : 0.0;
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const double xj = vj ? __ldg(xs + j + q * C) : 0.0;
+                u0[q] = fma(a0, xj, u0[q]);
+                u1[q] = fma(a1, xj, u1[q]);
+                p[jj][q] = fma(a0, xt0[q], a1 * xt1[q]);
+            }
+        }
+        if (want_w) {
+            // butterfly on lane bits 2..0 halves the column set (4 + 2 + 1 shuffles),
+            // leaving column (lane & 7); lane bits 3..4 are then summed (2 shuffles)
+#pragma unroll
+            for (int sft = 4; sft >= 1; sft >>= 1) {
+                const bool up = lane & sft;
+#pragma unroll
+                for (int k = 0; k < sft; ++k)
+#pragma unroll
+                    for (int q = 0; q < B; ++q) {
+                        const double send = up ? p[k][q] : p[k + sft][q];
+                        const double keep = up ? p[k + sft][q] : p[k][q];
+                        p[k][q] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+                    }
+            }
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 8);
+                p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 16);
+            }
+            const int j = j0 + lane;
+            if (lane < 8 && j < C)
+#pragma unroll
+                for (int q = 0; q < B; ++q) w[j + q * C] = p[0][q];
+        }
+    }
+    double* u = scratch + d.u_off * b;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+        if (v0) u[r0 + q * R] = u0[q];
+        if (v1) u[r1 + q * R] = u1[q];
+    }
+}
+
+// blocks of <= 32 rows (couplings at rank <= 32): a half-warp covers one
+// column with 16-byte loads (lane: rows 2i, 2i+1), so one warp instruction
+// reads two columns; column partials are reduced 16 columns at a time
+// (butterfly over lane bits 0..2, then bit 3: 8 shuffles per 16 columns)
+template <int B>
+__global__ void __launch_bounds__(256) sym_pass32_kernel(const SymBlock* __restrict__ blocks, int nblocks,
+                                                         const double* __restrict__ src,
+                                                         double* __restrict__ scratch, int64_t b) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (wid >= nblocks) return;
+    const SymBlock d = blocks[wid];
+    const int R = d.R, C = d.C;
+    const double* xs = src + d.xs_unit * b;
+    const double* xt = src + d.xt_unit * b;
+    const int half = lane >> 4, rr = (lane & 15) * 2;
+    const bool vr = rr < R;   // R even: rows rr and rr + 1 valid together
+    double xa[B], xb[B], ua[B], ub[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+        xa[q] = vr ? xt[rr + q * R] : 0.0;
+        xb[q] = vr ? xt[rr + 1 + q * R] : 0.0;
+        ua[q] = ub[q] = 0.0;
+    }
+    const bool want_w = d.w_off >= 0;
+    double* w = want_w ? scratch + d.w_off * b : nullptr;
+    for (int j0 = 0; j0 < C; j0 += 16) {
+        double p[8][B];   // p[k]: partial of column j0 + 2k + half
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = j0 + 2 * k + half;
+            const bool vj = j < C;
+            double2 a = make_double2(0.0, 0.0);
+            if (vr && vj) a = __ldg(reinterpret_cast<const double2*>(d.A + int64_t(j) * d.lda + rr));
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const double xj = vj ? __ldg(xs + j + q * C) : 0.0;
+                ua[q] = fma(a.x, xj, ua[q]);
+                ub[q] = fma(a.y, xj, ub[q]);
+                p[k][q] = fma(a.x, xa[q], a.y * xb[q]);
+            }
+        }
+        if (want_w) {
+#pragma unroll
+            for (int sft = 4; sft >= 1; sft >>= 1) {
+                const bool up = lane & sft;
+#pragma unroll
+                for (int k = 0; k < sft; ++k)
+#pragma unroll
+                    for (int q = 0; q < B; ++q) {
+                        const double send = up ? p[k][q] : p[k + sft][q];
+                        const double keep = up ? p[k + sft][q] : p[k][q];
+                        p[k][q] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+                    }
+            }
+#pragma unroll
+            for (int q = 0; q < B; ++q) p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 8);
+            // lane now holds column pair index (lane & 7) of its half: column j0 + 2 (lane & 7) + half
+            const int j = j0 + 2 * (lane & 7) + half;
+            if ((lane & 8) == 0 && j < C)
+#pragma unroll
+                for (int q = 0; q < B; ++q) w[j + q * C] = p[0][q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+        ua[q] += __shfl_xor_sync(0xffffffffu, ua[q], 16);
+        ub[q] += __shfl_xor_sync(0xffffffffu, ub[q], 16);
+    }
+    if (half == 0 && vr) {
+        double* u = scratch + d.u_off * b;
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            u[rr + q * R] = ua[q];
+            u[rr + 1 + q * R] = ub[q];
+        }
+    }
+}
+
+// blocks of <= 64 even rows (dense near-field leaves): each lane loads rows
+// 2l, 2l+1 of a column with one 16-byte load (512 B per warp instruction)
+template <int B>
+__global__ void __launch_bounds__(256) sym_pass64_kernel(const SymBlock* __restrict__ blocks, int nblocks,
+                                                         const double* __restrict__ src,
+                                                         double* __restrict__ scratch, int64_t b) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (wid >= nblocks) return;
+    const SymBlock d = blocks[wid];
+    const int R = d.R, C = d.C;
+    const double* xs = src + d.xs_unit * b;
+    const double* xt = src + d.xt_unit * b;
+    const int rr = lane * 2;
+    const bool vr = rr < R;
+    double xa[B], xb[B], ua[B], ub[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+        xa[q] = vr ? xt[rr + q * R] : 0.0;
+        xb[q] = vr ? xt[rr + 1 + q * R] : 0.0;
+        ua[q] = ub[q] = 0.0;
+    }
+    const bool want_w = d.w_off >= 0;
+    double* w = want_w ? scratch + d.w_off * b : nullptr;
+#pragma unroll 2
+    for (int j0 = 0; j0 < C; j0 += 8) {
+        double p[8][B];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int j = j0 + jj;
+            const bool vj = j < C;
+            double2 a = make_double2(0.0, 0.0);
+            if (vr && vj) a = __ldg(reinterpret_cast<const double2*>(d.A + int64_t(j) * d.lda + rr));
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const double xj = vj ? __ldg(xs + j + q * C) : 0.0;
+                ua[q] = fma(a.x, xj, ua[q]);
+                ub[q] = fma(a.y, xj, ub[q]);
+                p[jj][q] = fma(a.x, xa[q], a.y * xb[q]);
+            }
+        }
+        if (want_w) {
+#pragma unroll
+            for (int sft = 4; sft >= 1; sft >>= 1) {
+                const bool up = lane & sft;
+#pragma unroll
+                for (int k = 0; k < sft; ++k)
+#pragma unroll
+                    for (int q = 0; q < B; ++q) {
+                        const double send = up ? p[k][q] : p[k + sft][q];
+                        const double keep = up ? p[k + sft][q] : p[k][q];
+                        p[k][q] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+                    }
+            }
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 8);
+                p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 16);
+            }
+            const int j = j0 + lane;
+            if (lane < 8 && j < C)
+#pragma unroll
+                for (int q = 0; q < B; ++q) w[j + q * C] = p[0][q];
+        }
+    }
+    if (vr) {
+        double* u = scratch + d.u_off * b;
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            u[rr + q * R] = ua[q];
+            u[rr + 1 + q * R] = ub[q];
+        }
+    }
+}
+
+// per output unit, the fixed-order sum of its slots: mode 0 sets y-hat, mode 1
+// adds alpha * sum into the rows of y (user order through perm)
+__global__ void __launch_bounds__(256) csr_sum_kernel(const CsrUnit* __restrict__ units, int nunits,
+                                                      const int64_t* __restrict__ slots,
+                                                      const double* __restrict__ scratch, int64_t b, int mode,
+                                                      double* __restrict__ out, const int* __restrict__ perm,
+                                                      int64_t ldy, double alpha) {
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (wid >= nunits) return;
+    const CsrUnit u = units[wid];
+    const int64_t cnt = int64_t(u.rows) * b;
+    for (int64_t e = lane; e < cnt; e += 32) {
+        double acc = 0.0;
+        for (int s = u.s0; s < u.s1; ++s) acc += scratch[slots[s] * b + e];
+        if (mode == 0) {
+            out[u.out_unit * b + e] = acc;
+        } else {
+            const int64_t i = e % u.rows, c = e / u.rows;
+            const int64_t r = u.out_unit + i;
+            const int64_t ur = perm ? perm[r] : r;
+            out[ur + c * ldy] += alpha * acc;
+        }
+    }
+}
+
 // x (n x b, user or internal ordering, ld) -> blocked internal layout: leaf t
 // occupies [begin_t*b, (begin_t+m_t)*b) as an m_t x b column-major block
 __global__ void gather_blocked_kernel(const double* __restrict__ x, int64_t ldx, const int* __restrict__ perm,
@@ -472,6 +745,10 @@ struct LaunchDesc {
     double flops_per_col = 0, payload_bytes = 0, bsrc_per_col = 0, out_per_col = 0;
     int stage = 0;            // 1 leaf up, 2 transfer up, 3 coupling, 4 downsweep, 5 leaf+dense
     int phase = 0;            // sharded hgemv: 0 before the exchange, 1 after
+    // 0 segmented GEMM; symmetric few-vector path: 1 block pass over couplings,
+    // 2 slot sums into y-hat, 3 block pass over dense blocks, 4 slot sums into y
+    int kind = 0;
+    int item_begin = 0, item_end = 0;   // blocks / units of kinds 1-4
 };
 
 struct HgemvPlan {
@@ -480,6 +757,13 @@ struct HgemvPlan {
     // host copies for the (lazy) byte accounting of timed runs
     std::vector<SegTask> htasks;
     std::vector<SegEntry> hentries;
+    // symmetric few-vector path
+    DeviceArray<SymBlock> sym_blocks;
+    DeviceArray<CsrUnit> csr_units;
+    DeviceArray<int64_t> csr_slots;
+    int64_t scratch_rows = 0;
+    bool sym32 = false;   // every coupling block has <= 32 even rows, 16-byte aligned
+    bool sym64 = false;   // every dense block has <= 64 even rows, 16-byte aligned
     std::once_flag accounted;
     DeviceArray<SegTask> tasks;
     DeviceArray<SegEntry> entries;
@@ -607,7 +891,8 @@ std::shared_ptr<const DeviceArray<int>> tree_perm(const std::shared_ptr<const Cl
     return d;
 }
 
-std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const DistSpec* ds = nullptr) {
+std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const DistSpec* ds = nullptr,
+                                      bool small = false) {
     const ClusterTree& ct = h.tree();
     // sharded plans keep only this rank's outputs: its subtree (owner == rank)
     // plus the replicated top levels (owner < 0)
@@ -658,8 +943,84 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         }
         pb.emit(outs, kModeSet, 1, 2);
     }
+    // symmetric few-vector path: block passes (kinds 1, 3) + slot sums (kinds 2, 4)
+    std::vector<SymBlock> sblocks;
+    std::vector<CsrUnit> sunits;
+    std::vector<int64_t> sslots;
+    int64_t srows = 0;
+    // canonical stored blocks of one kind -> block pass + per-output slot lists
+    auto sym_stage = [&](const std::vector<int>& list, const std::vector<int64_t>& offs, const double* base,
+                         bool coupling, std::vector<int>& outputs, std::vector<int>& out_rows,
+                         std::vector<int64_t>& out_unit) {
+        std::vector<std::vector<int64_t>> by_out(static_cast<size_t>(nn));
+        LaunchDesc lb;
+        lb.kind = coupling ? 1 : 3;
+        lb.stage = coupling ? 3 : 5;
+        lb.phase = 1;
+        lb.item_begin = int(sblocks.size());
+        for (size_t i = 0; i < list.size(); ++i) {
+            const int b = list[i];
+            if (offs[i] < 0) continue;
+            const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
+            const int R = coupling ? h.row.rank[size_t(r)] : int(ct.size(r));
+            const int C = coupling ? h.row.rank[size_t(c)] : int(ct.size(c));
+            if (R == 0 || C == 0) continue;
+            SymBlock sb{};
+            sb.A = base + offs[i];
+            sb.lda = R;
+            sb.R = R;
+            sb.C = C;
+            sb.xs_unit = coupling ? cu[size_t(c)] : ct.begin[size_t(c)];
+            sb.xt_unit = coupling ? cu[size_t(r)] : ct.begin[size_t(r)];
+            sb.u_off = srows;
+            srows += R;
+            by_out[size_t(r)].push_back(sb.u_off);
+            sb.w_off = -1;
+            if (r != c) {
+                sb.w_off = srows;
+                srows += C;
+                by_out[size_t(c)].push_back(sb.w_off);
+            }
+            sblocks.push_back(sb);
+        }
+        lb.item_end = int(sblocks.size());
+        LaunchDesc ls;
+        ls.kind = coupling ? 2 : 4;
+        ls.stage = coupling ? 3 : 5;
+        ls.phase = 1;
+        ls.item_begin = int(sunits.size());
+        for (size_t q = 0; q < outputs.size(); ++q) {
+            const int v = outputs[q];
+            CsrUnit un{};
+            un.rows = out_rows[q];
+            un.out_unit = out_unit[q];
+            un.s0 = int(sslots.size());
+            for (int64_t o : by_out[size_t(v)]) sslots.push_back(o);
+            un.s1 = int(sslots.size());
+            sunits.push_back(un);
+        }
+        ls.item_end = int(sunits.size());
+        if (lb.item_end > lb.item_begin) pb.launches.push_back(lb);
+        if (ls.item_end > ls.item_begin) pb.launches.push_back(ls);
+    };
+    if (small) {
+        std::vector<int> outs_v, outs_r;
+        std::vector<int64_t> outs_u;
+        for (int v = 0; v < nn; ++v)
+            if (down.rank[size_t(v)] > 0) {
+                outs_v.push_back(v);
+                outs_r.push_back(down.rank[size_t(v)]);
+                outs_u.push_back(cd[size_t(v)]);
+            }
+        sym_stage(bt.adm, h.s_off, h.S.data(), true, outs_v, outs_r, outs_u);
+        bool ok32 = true;
+        for (const SymBlock& sb : sblocks)
+            ok32 = ok32 && sb.R <= 32 && sb.R % 2 == 0 && sb.lda % 2 == 0 &&
+                   (reinterpret_cast<uintptr_t>(sb.A) % 16) == 0;
+        plan->sym32 = ok32;
+    }
     // stage 2: couplings, row-CSR over target nodes (yhat zeroed first)
-    {
+    if (!small) {
         std::vector<std::vector<SegEntry>> by_target(static_cast<size_t>(nn));
         for (size_t i = 0; i < bt.adm.size(); ++i) {
             const int b = bt.adm[i];
@@ -733,7 +1094,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
                 by_leaf[size_t(t)].push_back(make_entry(plan->ue.data() + ue_off[size_t(t)], m, kp, false, 2, cd[size_t(p)], kp));
             }
         }
-        for (size_t i = 0; i < bt.dense.size(); ++i) {
+        for (size_t i = 0; i < bt.dense.size() && !small; ++i) {
             const int b = bt.dense[i];
             if (!h.stores(b)) continue;
             const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
@@ -753,6 +1114,28 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
             outs.push_back(P{m, m, ct.begin[size_t(t)], std::move(by_leaf[size_t(t)])});
         }
         pb.emit(outs, kModeY, 3, 5);
+    }
+    if (small) {
+        std::vector<int> lv, lr;
+        std::vector<int64_t> lu;
+        for (int t : ct.leaves) {
+            lv.push_back(t);
+            lr.push_back(int(ct.size(t)));
+            lu.push_back(ct.begin[size_t(t)]);
+        }
+        const size_t first_dense = sblocks.size();
+        sym_stage(bt.dense, h.d_off, h.D.data(), false, lv, lr, lu);
+        bool ok64 = true;
+        for (size_t q = first_dense; q < sblocks.size(); ++q) {
+            const SymBlock& sb = sblocks[q];
+            ok64 = ok64 && sb.R <= 64 && sb.R % 2 == 0 && sb.lda % 2 == 0 &&
+                   (reinterpret_cast<uintptr_t>(sb.A) % 16) == 0;
+        }
+        plan->sym64 = ok64;
+        plan->sym_blocks.upload(sblocks);
+        plan->csr_units.upload(sunits);
+        plan->csr_slots.upload(sslots);
+        plan->scratch_rows = srows;
     }
     plan->launches = std::move(pb.launches);
     plan->tasks.upload(pb.tasks);
@@ -776,6 +1159,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
 }
 
 double g_plan_build_ms = 0;   // host wall time spent building plans (diagnostics)
+int g_small_b = 2;            // symmetric few-vector path for b <= this (0 = off)
 
 std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
     std::lock_guard<std::mutex> g(h.plan_mu);
@@ -787,6 +1171,27 @@ std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
         g_plan_build_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     return p;
+}
+
+// symmetric matrices with few vectors: stream every canonical block once (HBM-bound regime)
+std::shared_ptr<HgemvPlan> select_plan(const H2Dev& h, bool transpose, int64_t b) {
+    if (h.symmetric && b <= g_small_b) {
+        const ClusterTree& ct = h.tree();
+        bool ok = ct.max_leaf_size() <= 64;
+        for (int k : h.row.rank) ok = ok && k <= 64;
+        if (ok) {
+            std::lock_guard<std::mutex> g(h.plan_mu);
+            auto& p = h.plan[2];
+            if (!p) {
+                const auto t0 = std::chrono::steady_clock::now();
+                p = build_plan(h, false, nullptr, true);
+                g_plan_build_ms +=
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            }
+            return p;
+        }
+    }
+    return get_plan(h, transpose);
 }
 
 template <int MT, int NB, int WM, int WN, int STAGES, int KC, bool VEC, int MODE>
@@ -925,7 +1330,7 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
     if (b < 1) throw std::invalid_argument("matvec: need at least one column");
     if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
-    auto plan = get_plan(h, transpose);
+    auto plan = select_plan(h, transpose, b);
     HgemvGraph& g = ws.graph;
     HgemvGraph::Key k;
     k.plan = plan->id;
@@ -1005,7 +1410,7 @@ void account(HgemvPlan& p) {
 void hgemv_timed(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
                  double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
                  std::vector<StageRecord>& records) {
-    account(*get_plan(h, transpose));
+    account(*select_plan(h, transpose, b));
     EventTimer t;
     std::vector<StageRecord> recs;
     t.out = &recs;
@@ -1027,7 +1432,7 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     if (b < 1) throw std::invalid_argument("matvec: need at least one column");
     if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
     std::shared_ptr<HgemvPlan> own_plan;
-    if (!dplan) own_plan = get_plan(h, transpose);
+    if (!dplan) own_plan = select_plan(h, transpose, b);
     const HgemvPlan* plan = dplan ? dplan : own_plan.get();
     const size_t need_x = size_t(n * b), need_u = size_t(plan->coef_up * b), need_d = size_t(plan->coef_down * b);
     if (ws.xint.size() < need_x) ws.xint.resize(need_x, stream);
@@ -1044,8 +1449,37 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
             timer->out->push_back({0, 0.f, 0.0, 16.0 * double(n * b)});
         }
     }
+    if (plan->scratch_rows > 0 && ws.scratch.size() < size_t(plan->scratch_rows * b))
+        ws.scratch.resize(size_t(plan->scratch_rows * b), stream);
     for (const LaunchDesc& ld : plan->launches) {
         if (!(phases & (1 << ld.phase))) continue;
+        if (ld.kind != 0) {
+            const int nitems = ld.item_end - ld.item_begin;
+            if (nitems == 0) continue;
+            if (timer) {
+                timer->mark(stream);
+                timer->out->push_back({ld.stage, 0.f, 0.0, 0.0});
+            }
+            const unsigned grid = unsigned((nitems + 7) / 8);
+            if (ld.kind == 1 && plan->sym32) {
+                if (b == 1) sym_pass32_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
+                else sym_pass32_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
+            } else if (ld.kind == 3 && plan->sym64) {
+                if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
+                else sym_pass64_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
+            } else if (ld.kind == 1 || ld.kind == 3) {
+                const double* src = ld.kind == 1 ? ws.xhat.data() : ws.xint.data();
+                if (b == 1) sym_pass_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
+                else sym_pass_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
+            } else {
+                csr_sum_kernel<<<grid, 256, 0, stream>>>(plan->csr_units.data() + ld.item_begin, nitems, plan->csr_slots.data(),
+                                                         ws.scratch.data(), b, ld.kind == 2 ? 0 : 1,
+                                                         ld.kind == 2 ? ws.yhat.data() : y, perm, ldy, alpha);
+            }
+            H2B_LAUNCH();
+            if (timer) timer->mark(stream);
+            continue;
+        }
         if (ld.zero_yhat && need_d) H2B_CUDA(cudaMemsetAsync(ws.yhat.data(), 0, need_d * sizeof(double), stream));
         const int ntasks = ld.task_end - ld.task_begin;
         if (ntasks == 0) continue;
@@ -1270,6 +1704,10 @@ int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
 
 // tuning hook (not part of the public ABI): select a tile-shape variant
 extern "C" int h2b_tune(int which, int value) {
+    if (which == 4) {   // symmetric few-vector path threshold (0 = off)
+        h2b::g_small_b = value;
+        return 0;
+    }
     if (which < 0 || which > 3) return -1;
     h2b::g_tune[which] = value;
     return 0;
