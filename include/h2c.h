@@ -31,6 +31,7 @@ extern "C" {
 #define H2C_RUNTIME_ERROR (-4)    /* std::runtime_error */
 #define H2C_CUDA_ERROR (-5)       /* CUDA failure (no reference counterpart) */
 #define H2C_CALLBACK_ERROR (-6)   /* user operator callback returned non-zero */
+#define H2C_DIVERGENCE_ERROR (-7) /* h2::divergence_error    (inversion.hpp:41-46) */
 
 typedef struct h2c_cluster_tree_s* h2c_cluster_tree;
 typedef struct h2c_block_tree_s* h2c_block_tree;
@@ -200,6 +201,38 @@ int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double
 int h2c_partition_owner(h2c_block_tree b, int nranks, int* owner);
 int h2c_partition_exchange(h2c_block_tree b, int symmetric, int transpose, const int* up_ranks, int nranks, int src,
                            int dst, int64_t* count, int* arr, int* node, int64_t* rows);
+
+/* ---- iterative inversion (inversion.hpp; SURVEY §8(f) "next") ------------
+ * Each iterate is rebuilt by h2c_peel_construct from a sampler of hgemvs. */
+/* H2Matrix::scaled_identity(bt, value) (h2_matrix.hpp:90-93) */
+int h2c_scaled_identity(h2c_block_tree b, double value, h2c_matrix* out);
+/* scaled_identity_start(a) = I / ||A||_inf (inversion.hpp:124-130) */
+int h2c_scaled_identity_start(h2c_matrix a, h2c_matrix* out);
+/* pnorm_estimate(op, p) for p = 1, 2 or +inf (linear_operator.hpp:127-178) */
+int h2c_pnorm_estimate(h2c_operator op, double p, double* value, int* iterations);
+/* ns_sampler / hyperpower_sampler / unrolled_sampler (inversion.hpp:137-208) as operators:
+ * kind 0 NS, 1 hyperpower (arg = order), 2 unrolled (arg = k); xk and a must outlive it */
+int h2c_sampler_operator(h2c_matrix xk, h2c_matrix a, int kind, int arg, h2c_operator* out);
+/* residual_norm(a, x) = ||A X - I||_2 estimate (inversion.hpp:213-225) */
+int h2c_residual_norm(h2c_matrix a, h2c_matrix x, double* out);
+/* the same for two black-box operators (inversion.hpp:213-220) */
+int h2c_residual_norm_op(h2c_operator a, h2c_operator x, double* out);
+typedef struct {
+    int iter;
+    double residual, eps_k;
+    int64_t samples;
+    double wall_seconds;
+} h2c_trace_row;   /* TraceRow (inversion.hpp:19-25) */
+/* h_newton_schulz (method 0), h_hyperpower (1, arg = order), h_unrolled (2, arg = k)
+ * (inversion.hpp:281-311); schedule: dynamic 0/1 + eps_initial (ThresholdSchedule :50-54).
+ * On H2C_DIVERGENCE_ERROR the trace so far is still returned. */
+int h2c_h_inverse(h2c_matrix a, h2c_matrix x0, int method, int arg, int dynamic_schedule, double eps_initial,
+                  double eps, const h2c_peel_config* cfg, int max_iter, h2c_matrix* out, h2c_trace_row* rows,
+                  int max_rows, int* num_rows, double* final_residual, int* converged);
+/* low_rank_update(h, {X, Y}, eps) (algebra.hpp:334-346); X, Y device n x k user order */
+int h2c_low_rank_update(h2c_matrix h, int64_t k, const double* X, const double* Y, double eps, h2c_matrix* out);
+/* desymmetrized() (h2_matrix.hpp:200-216) */
+int h2c_desymmetrized(h2c_matrix h, h2c_matrix* out);
 
 #ifdef __cplusplus
 }

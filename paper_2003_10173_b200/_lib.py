@@ -28,6 +28,7 @@ H2C_MAX_RANK_ERROR = -3
 H2C_RUNTIME_ERROR = -4
 H2C_CUDA_ERROR = -5
 H2C_CALLBACK_ERROR = -6
+H2C_DIVERGENCE_ERROR = -7
 
 
 class CudaError(RuntimeError):
@@ -36,6 +37,14 @@ class CudaError(RuntimeError):
 
 class max_rank_error(RuntimeError):
     """Mirror of h2::max_rank_error (construction.hpp:61-66)."""
+
+
+class divergence_error(RuntimeError):
+    """Mirror of h2::divergence_error (inversion.hpp:41-46); .trace holds the rows so far."""
+
+    def __init__(self, msg, trace=None):
+        super().__init__(msg)
+        self.trace = trace
 
 
 def _sig(name, res, *args):
@@ -82,6 +91,8 @@ def check(rc):
         raise NotImplementedError(msg)
     if rc == H2C_MAX_RANK_ERROR:
         raise max_rank_error(msg)
+    if rc == H2C_DIVERGENCE_ERROR:
+        raise divergence_error(msg)
     if rc == H2C_CUDA_ERROR:
         raise CudaError(msg)
     raise RuntimeError(f"h2c error {rc}: {msg}")
@@ -125,3 +136,20 @@ _sig("h2c_dist_hgemv_begin", i32, H, i64, vp, i64, vp, vp)
 _sig("h2c_dist_hgemv_end", i32, H, i64, vp, vp, i64, f64, f64, vp)
 _sig("h2c_partition_owner", i32, H, i32, vp)
 _sig("h2c_partition_exchange", i32, H, i32, i32, vp, i32, i32, i32, P(i64), vp, vp, vp)
+
+
+class TraceRowC(C.Structure):
+    _fields_ = [("iter", C.c_int), ("residual", C.c_double), ("eps_k", C.c_double), ("samples", C.c_int64),
+                ("wall_seconds", C.c_double)]
+
+
+_sig("h2c_scaled_identity", i32, H, f64, P(H))
+_sig("h2c_scaled_identity_start", i32, H, P(H))
+_sig("h2c_pnorm_estimate", i32, H, f64, P(f64), P(i32))
+_sig("h2c_sampler_operator", i32, H, H, i32, i32, P(H))
+_sig("h2c_residual_norm", i32, H, H, P(f64))
+_sig("h2c_residual_norm_op", i32, H, H, P(f64))
+_sig("h2c_h_inverse", i32, H, H, i32, i32, i32, f64, f64, P(PeelConfigC), i32, P(H), P(TraceRowC), i32, P(i32),
+     P(f64), P(i32))
+_sig("h2c_low_rank_update", i32, H, i64, vp, vp, f64, P(H))
+_sig("h2c_desymmetrized", i32, H, P(H))

@@ -96,11 +96,9 @@ def make_operator(n, symmetric, f, t=None):
 
 
 def pnorm_estimate(op, p=2):
-    """pnorm_estimate(op, 2) (linear_operator.hpp:127-153) -> (value, iterations)."""
-    if p != 2:
-        raise ValueError("pnorm_estimate: the B200 path implements p = 2")
+    """pnorm_estimate(op, p), p in {1, 2, inf} (linear_operator.hpp:127-178) -> (value, iterations)."""
     v, it = C.c_double(), C.c_int()
-    check(lib.h2c_pnorm2_estimate(op._h, C.byref(v), C.byref(it)))
+    check(lib.h2c_pnorm_estimate(op._h, float(p), C.byref(v), C.byref(it)))
     return v.value, it.value
 
 

@@ -2,6 +2,7 @@
 #include "../../include/h2c.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -9,6 +10,7 @@
 
 #include "h2dev.hpp"
 #include "hara.hpp"
+#include "inversion.hpp"
 #include "matrix.hpp"
 
 struct h2c_cluster_tree_s {
@@ -50,6 +52,9 @@ int guard(F&& f) {
     } catch (const h2b::cuda_error& e) {
         g_err = e.what();
         return H2C_CUDA_ERROR;
+    } catch (const h2b::divergence_error& e) {
+        g_err = e.what();
+        return H2C_DIVERGENCE_ERROR;
     } catch (const h2b::max_rank_error& e) {
         g_err = e.what();
         return H2C_MAX_RANK_ERROR;
@@ -549,6 +554,121 @@ int h2c_partition_exchange(h2c_block_tree b, int symmetric, int transpose, const
                 if (node) node[i] = items[i].node;
                 if (rows) rows[i] = items[i].rows;
             }
+    });
+}
+
+// ---- inversion ------------------------------------------------------------------
+int h2c_scaled_identity(h2c_block_tree b, double value, h2c_matrix* out) {
+    return guard([&] {
+        need(b != nullptr && out != nullptr, "null argument");
+        *out = wrap_matrix(h2b::scaled_identity(b->b, value, nullptr));
+    });
+}
+
+int h2c_scaled_identity_start(h2c_matrix a, h2c_matrix* out) {
+    return guard([&] {
+        need(a != nullptr && out != nullptr, "null argument");
+        *out = wrap_matrix(h2b::scaled_identity_start(*a->h, nullptr));
+    });
+}
+
+int h2c_pnorm_estimate(h2c_operator op, double p, double* value, int* iterations) {
+    return guard([&] {
+        need(op != nullptr && value != nullptr, "null argument");
+        h2b::NormEstimate e;
+        if (p == 2.0) e = h2b::pnorm2_estimate(*op->op, nullptr);
+        else if (p == 1.0) e = h2b::pnorm_1inf_estimate(*op->op, false, nullptr);
+        else if (std::isinf(p)) e = h2b::pnorm_1inf_estimate(*op->op, true, nullptr);
+        else throw std::invalid_argument("pnorm_estimate: p must be 1, 2 or inf");
+        *value = e.value;
+        if (iterations) *iterations = e.iterations;
+    });
+}
+
+int h2c_sampler_operator(h2c_matrix xk, h2c_matrix a, int kind, int arg, h2c_operator* out) {
+    return guard([&] {
+        need(xk != nullptr && a != nullptr && out != nullptr, "null argument");
+        std::unique_ptr<h2b::DevOperator> op;
+        if (kind == 0) op = h2b::ns_sampler(*xk->h, *a->h);
+        else if (kind == 1) op = h2b::hyperpower_sampler(*xk->h, *a->h, arg);
+        else if (kind == 2) op = h2b::unrolled_sampler(*xk->h, *a->h, arg);
+        else throw std::invalid_argument("sampler kind must be 0, 1 or 2");
+        *out = new h2c_operator_s{std::move(op)};
+    });
+}
+
+int h2c_residual_norm(h2c_matrix a, h2c_matrix x, double* out) {
+    return guard([&] {
+        need(a != nullptr && x != nullptr && out != nullptr, "null argument");
+        *out = h2b::residual_norm(*a->h, *x->h, nullptr);
+    });
+}
+
+int h2c_residual_norm_op(h2c_operator a, h2c_operator x, double* out) {
+    return guard([&] {
+        need(a != nullptr && x != nullptr && out != nullptr, "null argument");
+        *out = h2b::residual_norm(*a->op, *x->op, nullptr);
+    });
+}
+
+namespace {
+void export_trace(const h2b::ConvergenceTrace& t, h2c_trace_row* rows, int max_rows, int* num_rows,
+                  double* final_residual, int* converged) {
+    if (num_rows) *num_rows = int(t.rows.size());
+    if (rows)
+        for (int i = 0; i < int(t.rows.size()) && i < max_rows; ++i) {
+            const h2b::TraceRow& r = t.rows[size_t(i)];
+            rows[i] = h2c_trace_row{r.iter, r.residual, r.eps_k, r.samples, r.wall_seconds};
+        }
+    if (final_residual) *final_residual = t.final_residual;
+    if (converged) *converged = t.converged ? 1 : 0;
+}
+}  // namespace
+
+int h2c_h_inverse(h2c_matrix a, h2c_matrix x0, int method, int arg, int dynamic_schedule, double eps_initial,
+                  double eps, const h2c_peel_config* cfg, int max_iter, h2c_matrix* out, h2c_trace_row* rows,
+                  int max_rows, int* num_rows, double* final_residual, int* converged) {
+    return guard([&] {
+        need(a != nullptr && x0 != nullptr && out != nullptr, "null argument");
+        h2b::PeelConfig c;
+        if (cfg) {
+            c.eps = cfg->eps;
+            c.sample_block_size = cfg->sample_block_size;
+            c.oversampling = cfg->oversampling;
+            c.max_rank = cfg->max_rank;
+            c.seed = cfg->seed;
+            c.norm_scale = cfg->norm_scale;
+            c.crossover_rank_cap = cfg->crossover_rank_cap;
+            c.rng = cfg->rng;
+        }
+        h2b::ThresholdSchedule sched;
+        sched.dynamic = dynamic_schedule != 0;
+        sched.eps_initial = eps_initial;
+        try {
+            h2b::InverseResult r = method == 2 ? h2b::h_unrolled(*a->h, *x0->h, arg, eps, c, nullptr)
+                                               : h2b::h_iterative_inverse(*a->h, *x0->h, sched, eps, c, method, arg,
+                                                                          max_iter, nullptr);
+            export_trace(r.trace, rows, max_rows, num_rows, final_residual, converged);
+            *out = wrap_matrix(std::move(r.X));
+        } catch (const h2b::divergence_error& e) {
+            export_trace(e.trace, rows, max_rows, num_rows, final_residual, converged);
+            throw;
+        }
+    });
+}
+
+int h2c_low_rank_update(h2c_matrix h, int64_t k, const double* X, const double* Y, double eps, h2c_matrix* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        need(k == 0 || (X != nullptr && Y != nullptr), "null factor");
+        *out = wrap_matrix(h2b::low_rank_update(*h->h, X, Y, int(k), eps, nullptr));
+    });
+}
+
+int h2c_desymmetrized(h2c_matrix h, h2c_matrix* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        *out = wrap_matrix(h2b::desymmetrized(*h->h, nullptr));
     });
 }
 

@@ -528,11 +528,16 @@ std::unique_ptr<H2Dev> apply_local_updates(const H2Dev& h, const std::vector<Loc
     for (size_t u = 0; u < ups.size(); ++u) {
         const LocalUpdate& up = ups[u];
         if (up.k == 0) continue;
-        if (h.symmetric && up.t == up.s)
-            throw std::invalid_argument("local update: diagonal update on a symmetric matrix needs X == Y");
+        // a symmetric diagonal update (t == s) must have X == Y (algebra.hpp:242-243);
+        // the caller guarantees it (low_rank_update desymmetrizes otherwise): the
+        // region is augmented once with X and every (row, col) pair inside it
+        // gets the identity coupling and X_r X_c^T dense contributions
         mark(mrow, up.t, int(u), 0);
-        if (h.symmetric) mark(mrow, up.s, int(u), 1);
-        else mark(mcol, up.s, int(u), 1);
+        if (h.symmetric) {
+            if (up.s != up.t) mark(mrow, up.s, int(u), 1);
+        } else {
+            mark(mcol, up.s, int(u), 1);
+        }
     }
     std::vector<Mark>& mc = h.symmetric ? mrow : mcol;
     auto newr = [&](const BasisDev& b, const std::vector<Mark>& m) {
@@ -585,8 +590,9 @@ std::unique_ptr<H2Dev> apply_local_updates(const H2Dev& h, const std::vector<Loc
         const int nr = rr[size_t(r)];
         if (kr && kc) cp.push_back(CopyDesc{Sp(h, i), Sp(*out, i), kr, kc, ld1(kr), ld1(nr), 0});
         const Mark a = mrow[size_t(r)], bm = mc[size_t(c)];
+        const bool self = a.u >= 0 && h.symmetric && ups[size_t(a.u)].t == ups[size_t(a.u)].s;
         const bool ident = a.u >= 0 && a.u == bm.u &&
-                           ((a.side == 0 && bm.side == 1) || (h.symmetric && a.side == 1 && bm.side == 0));
+                           (self || (a.side == 0 && bm.side == 1) || (h.symmetric && a.side == 1 && bm.side == 0));
         if (ident) {
             const int kp = ups[size_t(a.u)].k;
             cp.push_back(CopyDesc{nullptr, Sp(*out, i) + kr + int64_t(kc) * nr, kp, kp, 1, ld1(nr), 2});
@@ -600,7 +606,8 @@ std::unique_ptr<H2Dev> apply_local_updates(const H2Dev& h, const std::vector<Loc
         if (a.u < 0 || a.u != bm.u) continue;
         const LocalUpdate& up = ups[size_t(a.u)];
         const int mr = int(ct.size(r)), mcn = int(ct.size(c));
-        if (a.side == 0 && bm.side == 1) {
+        const bool self = h.symmetric && up.t == up.s;
+        if (self || (a.side == 0 && bm.side == 1)) {
             auto x = factor_rows(up, 0, r);
             auto y = factor_rows(up, 1, c);
             gm.push_back(GemmDesc{x.first, y.first, Dp(*out, i), mr, mcn, up.k, int(x.second), int(y.second), mr, 0, 1,
