@@ -44,6 +44,14 @@ CONFIGS = {
                           "weak admissibility, leaf 32, eps 1e-6, PeelConfig defaults (b=16, p=10)",
                  grid=(262144,), kind="gaussian", ell=0.05, rank=32, leaf=32, eps=1e-6, hara=True,
                  sample_n=16384),
+    # BASELINE.json configs[4]: recompression + low-rank update, then hierarchical Newton-Schulz on a
+    # regularised Hessian proxy: the cfg3 diffusion proxy (Gaussian heat kernel F^T F) at N=2^16 plus a
+    # Tikhonov shift alpha I, updated by a rank-8 symmetric term (a quasi-Newton-style correction)
+    "cfg5": dict(workload="recompress(1e-8) + rank-8 low_rank_update + hierarchical Newton-Schulz (dynamic threshold "
+                          "schedule, residual 1e-6) of a regularised 1D diffusion-Hessian proxy (Gaussian heat kernel "
+                          "ell=0.05, lambda_max ~ 2.9e3, + 1000 I: kappa ~ 4, rank-32 H^2), N=2^16, weak admissibility, leaf 32",
+                 grid=(65536,), kind="gaussian", ell=0.05, rank=32, leaf=32, alpha=1000.0, eps=1e-6, inversion=True,
+                 update_rank=8),
     # BASELINE.json configs[3] at P=1
     "cfg4": dict(workload="3D Matern-3/2 H2 hgemv N=2^21 (128^3 grid), leaf 64, rank 32, 64 vectors",
                  grid=(128, 128, 128), kind="matern32", ell=0.1, rank=32, b=64, leaf=64),
@@ -497,6 +505,64 @@ def run_hara(args, cfg, world, rank, local, dist):
     return out
 
 
+def run_inversion(args, cfg, world, rank, local, dist):
+    """cfg5: one step = recompress + low-rank update + hierarchical Newton-Schulz to residual eps."""
+    import torch
+    from paper_2003_10173_b200 import (PeelConfig, ThresholdSchedule, h_newton_schulz, low_rank_update,
+                                       recompress, residual_norm, scaled_identity_start)
+    torch.cuda.set_device(local)
+    n = cfg["grid"][0]
+    pts, ct, bt, a = hara_problem(cfg, n)
+    a.add_diagonal(cfg["alpha"])
+    X = 0.1 * np.random.default_rng(7).standard_normal((n, cfg["update_rank"]))
+    pc = PeelConfig(eps=cfg["eps"], rng=1)
+
+    def step():
+        t = {}
+        t0 = time.perf_counter()
+        ar = recompress(a, 1e-8)
+        t["recompress"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        au = low_rank_update(ar, X, X, 1e-8)
+        t["low_rank_update"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        x0 = scaled_identity_start(au)
+        try:
+            res = h_newton_schulz(au, x0, ThresholdSchedule(dynamic=True), cfg["eps"], pc)
+        except Exception as e:
+            tr = getattr(e, "trace", None)
+            rows = [(r.iter, r.residual, r.eps_k, r.samples) for r in tr.rows] if tr else []
+            raise RuntimeError(f"NS failed: {e}; trace {rows}") from e
+        torch.cuda.synchronize()
+        t["newton_schulz"] = time.perf_counter() - t0
+        return t, res, au
+
+    step()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(max(1, min(args.steps, 2))):
+            t, res, au = step()
+            times.append(t)
+    tot = [sum(t.values()) for t in times]
+    i = int(np.argsort(tot)[len(tot) // 2])
+    rows = res.trace.rows
+    return {"metric": "NS inversion time (N=2^16, residual 1e-6)", "value": tot[i], "unit": "s", "n_gpus": world,
+            "steps": len(tot), "warmup": 1, "ms_per_step": tot[i] * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated kernel H^2 + shift, random rank-8 update)",
+            "config": {"workload": cfg["workload"], "n": n, "parallelism": "single GPU"},
+            "inversion": {"phases_s": {k: round(v, 4) for k, v in times[i].items()},
+                          "iterations": len(rows), "converged": res.trace.converged,
+                          "final_residual": res.trace.final_residual,
+                          "residual_check": residual_norm(au, res.X),
+                          "samples": res.trace.total_samples(),
+                          "rows": [(r.iter, r.residual, r.eps_k, r.samples, round(r.wall_seconds, 4)) for r in rows],
+                          "rank_profile": [int(v) for v in res.X.rank_profile()]},
+            "cpu_baseline": {"value": None, "reason": "the oracle restates the hot path (hgemv, HARA, algebra); the "
+                                                      "inversion drivers are SURVEY §8(f) 'next' and have no CPU port"},
+            "clocks": clk.summary()}
+
+
 def cpu_baseline_hara(args, cfg):
     """The oracle (restated reference, 1 thread) on a bounded sample: the same
     problem at N = sample_n, next to the B200 on the same sample."""
@@ -547,6 +613,16 @@ def main():
         # 10.639 GB + 0.266 GB per launch, profiles/ncu_full_cfg2_r01_v1.txt
         args.traffic = 10.638945e9 + 0.266123e9
     world, rank, local, dist = dist_setup(args)
+    if cfg.get("inversion"):
+        if args.impl == "reference":
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "no CPU port of the inversion drivers "
+                                                                      "(SURVEY §8(f) 'next')"}))
+            return
+        out = run_inversion(args, cfg, world, rank, local, dist)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
     if cfg.get("hara"):
         if args.impl == "reference":
             if rank == 0:

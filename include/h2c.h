@@ -206,6 +206,8 @@ int h2c_partition_exchange(h2c_block_tree b, int symmetric, int transpose, const
  * Each iterate is rebuilt by h2c_peel_construct from a sampler of hgemvs. */
 /* H2Matrix::scaled_identity(bt, value) (h2_matrix.hpp:90-93) */
 int h2c_scaled_identity(h2c_block_tree b, double value, h2c_matrix* out);
+/* in place: H <- H + value I (diagonal dense leaves; e.g. a Tikhonov shift of a Hessian) */
+int h2c_matrix_add_diagonal(h2c_matrix h, double value);
 /* scaled_identity_start(a) = I / ||A||_inf (inversion.hpp:124-130) */
 int h2c_scaled_identity_start(h2c_matrix a, h2c_matrix* out);
 /* pnorm_estimate(op, p) for p = 1, 2 or +inf (linear_operator.hpp:127-178) */

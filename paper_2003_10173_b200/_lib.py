@@ -145,6 +145,7 @@ class TraceRowC(C.Structure):
 
 _sig("h2c_scaled_identity", i32, H, f64, P(H))
 _sig("h2c_scaled_identity_start", i32, H, P(H))
+_sig("h2c_matrix_add_diagonal", i32, H, f64)
 _sig("h2c_pnorm_estimate", i32, H, f64, P(f64), P(i32))
 _sig("h2c_sampler_operator", i32, H, H, i32, i32, P(H))
 _sig("h2c_residual_norm", i32, H, H, P(f64))

@@ -565,6 +565,13 @@ int h2c_scaled_identity(h2c_block_tree b, double value, h2c_matrix* out) {
     });
 }
 
+int h2c_matrix_add_diagonal(h2c_matrix h, double value) {
+    return guard([&] {
+        need(h != nullptr, "null argument");
+        h2b::add_diagonal(*h->h, value, nullptr);
+    });
+}
+
 int h2c_scaled_identity_start(h2c_matrix a, h2c_matrix* out) {
     return guard([&] {
         need(a != nullptr && out != nullptr, "null argument");

@@ -121,12 +121,35 @@ __global__ void fill_kernel(int64_t n, double v, double* __restrict__ o) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         o[i] = v;
 }
-// diagonal dense leaves of a zero matrix set to value * I (scaled_identity)
+// diagonal of the diagonal dense leaves: set to (add == 0) or add `value`
 __global__ void diag_set_kernel(const int64_t* __restrict__ off, const int* __restrict__ m, double value,
-                                double* __restrict__ D) {
+                                double* __restrict__ D, int add) {
     const int64_t o = off[blockIdx.x];
     const int mm = m[blockIdx.x];
-    for (int i = threadIdx.x; i < mm; i += blockDim.x) D[o + int64_t(i) * mm + i] = value;
+    for (int i = threadIdx.x; i < mm; i += blockDim.x) {
+        double* p = D + o + int64_t(i) * mm + i;
+        *p = add ? *p + value : value;
+    }
+}
+void diag_apply(H2Dev& h, double value, int add, cudaStream_t s) {
+    const BlockTree& bt = *h.bt;
+    const ClusterTree& ct = *bt.tree;
+    std::vector<int64_t> off;
+    std::vector<int> m;
+    for (size_t i = 0; i < bt.dense.size(); ++i) {
+        const int b = bt.dense[i];
+        if (h.d_off[i] < 0 || bt.row[size_t(b)] != bt.col[size_t(b)]) continue;
+        off.push_back(h.d_off[i]);
+        m.push_back(int(ct.size(bt.row[size_t(b)])));
+    }
+    if (off.empty()) return;
+    DeviceArray<int64_t> doff;
+    DeviceArray<int> dm;
+    doff.upload(off, s);
+    dm.upload(m, s);
+    diag_set_kernel<<<unsigned(off.size()), 128, 0, s>>>(doff.data(), dm.data(), value, h.D.data(), add);
+    H2B_LAUNCH();
+    H2B_CUDA(cudaStreamSynchronize(s));
 }
 
 // hgemv of one matrix with its own workspace (samplers own one per matrix)
@@ -143,25 +166,12 @@ struct Apply {
 
 std::unique_ptr<H2Dev> scaled_identity(std::shared_ptr<const BlockTree> bt, double value, cudaStream_t s) {
     auto h = make_h2(bt, true, nullptr, nullptr);
-    const ClusterTree& ct = *bt->tree;
-    std::vector<int64_t> off;
-    std::vector<int> m;
-    for (size_t i = 0; i < bt->dense.size(); ++i) {
-        const int b = bt->dense[i];
-        if (h->d_off[i] < 0 || bt->row[size_t(b)] != bt->col[size_t(b)]) continue;
-        off.push_back(h->d_off[i]);
-        m.push_back(int(ct.size(bt->row[size_t(b)])));
-    }
-    if (!off.empty()) {
-        DeviceArray<int64_t> doff;
-        DeviceArray<int> dm;
-        doff.upload(off, s);
-        dm.upload(m, s);
-        diag_set_kernel<<<unsigned(off.size()), 128, 0, s>>>(doff.data(), dm.data(), value, h->D.data());
-        H2B_LAUNCH();
-    }
-    H2B_CUDA(cudaStreamSynchronize(s));
+    diag_apply(*h, value, 0, s);
     return h;
+}
+
+void add_diagonal(H2Dev& h, double value, cudaStream_t s) {
+    diag_apply(h, value, 1, s);   // values only: plans (pointers, structure) stay valid
 }
 
 NormEstimate pnorm_1inf_estimate(DevOperator& op, bool inf, cudaStream_t s, int max_iter) {

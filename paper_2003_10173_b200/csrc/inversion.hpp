@@ -37,6 +37,8 @@ public:
 
 // H2Matrix::diagonal / scaled_identity (h2_matrix.hpp:78-93)
 std::unique_ptr<H2Dev> scaled_identity(std::shared_ptr<const BlockTree> bt, double value, cudaStream_t s);
+// H <- H + value I on the diagonal dense leaves (regularisation shift; in place)
+void add_diagonal(H2Dev& h, double value, cudaStream_t s);
 // pnorm_estimate(op, 1 / inf) (linear_operator.hpp:155-178)
 NormEstimate pnorm_1inf_estimate(DevOperator& op, bool inf, cudaStream_t s, int max_iter = 100);
 // X0 = I / ||A||_inf (inversion.hpp:124-130)

@@ -291,6 +291,10 @@ class H2Matrix:
         check(lib.h2c_hgemv(self._h, int(transpose), int(ordering), x.shape[0], b, x.data_ptr(), ldx,
                             y.data_ptr(), ldy, float(alpha), float(beta), s))
 
+    def add_diagonal(self, value):
+        """In place H <- H + value I (diagonal dense leaves)."""
+        check(lib.h2c_matrix_add_diagonal(self._h, float(value)))
+
     def launches(self, b, transpose=False):
         n = C.c_int()
         check(lib.h2c_hgemv_launches(self._h, int(transpose), int(b), C.byref(n)))
