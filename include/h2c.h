@@ -236,6 +236,22 @@ int h2c_low_rank_update(h2c_matrix h, int64_t k, const double* X, const double* 
 /* desymmetrized() (h2_matrix.hpp:200-216) */
 int h2c_desymmetrized(h2c_matrix h, h2c_matrix* out);
 
+/* ---- global randomized low-rank and the hybrid constructor
+ *      (construction.hpp:386-534; SURVEY §8(f) "next") ------------------ */
+typedef struct h2c_lowrank_s* h2c_lowrank;
+/* randomized_lowrank(op, eps, max_rank, cfg) (construction.hpp:484-491) */
+int h2c_randomized_lowrank(h2c_operator op, double eps, int64_t max_rank, const h2c_peel_config* cfg,
+                           h2c_lowrank* out);
+int h2c_lowrank_info(h2c_lowrank f, int64_t* n, int64_t* rank, int* symmetric_form, double* residual_estimate,
+                     int* max_rank_reached, int64_t* total_samples);
+/* factor X Y^T to host buffers (n x rank, column-major, user ordering) */
+int h2c_lowrank_download(h2c_lowrank f, double* X, double* Y);
+void h2c_lowrank_destroy(h2c_lowrank f);
+/* hybrid_construct(op, bt, cfg) (construction.hpp:506-534) */
+int h2c_hybrid_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config* cfg, h2c_matrix* out,
+                         int64_t* global_rank, int64_t* total_samples, h2c_level_stats* levels, int max_levels,
+                         int* num_levels);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,8 +6,9 @@ lib/libh2b200.so (sm_100a CUDA kernels behind the C ABI in include/h2c.h).
 from .h2 import (Admissibility, BlockTree, ClusterTree, H2Matrix, Ordering, build_block_tree,
                  build_cluster_tree)
 from ._lib import CudaError, LIB_PATH, divergence_error, max_rank_error
-from .construction import (DenseOperator, H2Operator, LinearOperator, PeelConfig, PeelResult, SampleStats,
-                           estimate_relative_error, make_operator, orthogonalize, peel_construct, pnorm_estimate,
+from .construction import (DenseOperator, H2Operator, HybridResult, LinearOperator, LowRankFactor, LowRankResult,
+                           PeelConfig, PeelResult, SampleStats, estimate_relative_error, hybrid_construct,
+                           make_operator, orthogonalize, peel_construct, pnorm_estimate, randomized_lowrank,
                            recompress)
 from .inversion import (ConvergenceTrace, HInverseResult, ThresholdSchedule, desymmetrized, h_hyperpower,
                         h_newton_schulz, h_unrolled, hyperpower_sampler, low_rank_update, ns_sampler,
@@ -20,4 +21,5 @@ __all__ = ["Admissibility", "BlockTree", "ClusterTree", "H2Matrix", "Ordering", 
            "orthogonalize", "peel_construct", "pnorm_estimate", "recompress", "divergence_error", "ConvergenceTrace",
            "HInverseResult", "ThresholdSchedule", "desymmetrized", "h_hyperpower", "h_newton_schulz", "h_unrolled",
            "hyperpower_sampler", "low_rank_update", "ns_sampler", "residual_norm", "scaled_identity",
-           "scaled_identity_start", "threshold_schedule", "unrolled_sampler"]
+           "scaled_identity_start", "threshold_schedule", "unrolled_sampler", "HybridResult", "LowRankFactor",
+           "LowRankResult", "hybrid_construct", "randomized_lowrank"]

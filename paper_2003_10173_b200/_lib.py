@@ -154,3 +154,9 @@ _sig("h2c_h_inverse", i32, H, H, i32, i32, i32, f64, f64, P(PeelConfigC), i32, P
      P(f64), P(i32))
 _sig("h2c_low_rank_update", i32, H, i64, vp, vp, f64, P(H))
 _sig("h2c_desymmetrized", i32, H, P(H))
+
+_sig("h2c_randomized_lowrank", i32, H, f64, i64, P(PeelConfigC), P(H))
+_sig("h2c_lowrank_info", i32, H, P(i64), P(i64), P(i32), P(f64), P(i32), P(i64))
+_sig("h2c_lowrank_download", i32, H, vp, vp)
+_sig("h2c_lowrank_destroy", None, H)
+_sig("h2c_hybrid_construct", i32, H, H, P(PeelConfigC), P(H), P(i64), P(i64), P(LevelStatsC), i32, P(i32))

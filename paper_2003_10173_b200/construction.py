@@ -174,3 +174,68 @@ def estimate_relative_error(op, m, op_norm=0.0):
     v = C.c_double()
     check(lib.h2c_estimate_relative_error(op._h, m._h, float(op_norm), C.byref(v)))
     return v.value
+
+
+def _cfg_c(cfg):
+    return PeelConfigC(float(cfg.eps), int(cfg.sample_block_size), int(cfg.oversampling), int(cfg.max_rank),
+                       int(cfg.seed), float(cfg.norm_scale), int(cfg.crossover_rank_cap), int(cfg.rng))
+
+
+@dataclasses.dataclass
+class LowRankFactor:   # algebra.hpp:323-331 (LowRankFactor)
+    X: np.ndarray
+    Y: np.ndarray
+
+    def rank(self):
+        return self.X.shape[1]
+
+
+@dataclasses.dataclass
+class LowRankResult:   # construction.hpp:386-391
+    factor: LowRankFactor
+    stats: SampleStats
+    residual_estimate: float
+    max_rank_reached: bool
+    symmetric_form: bool
+
+
+def randomized_lowrank(op, eps, max_rank=0, cfg=None):
+    """Adaptive global randomized range finder (construction.hpp:484-491) on the B200."""
+    cfg = cfg or PeelConfig()
+    c = _cfg_c(cfg)
+    h = H()
+    check(lib.h2c_randomized_lowrank(op._h, float(eps), int(max_rank), C.byref(c), C.byref(h)))
+    try:
+        n, k, tot = C.c_int64(), C.c_int64(), C.c_int64()
+        sym, mr = C.c_int(), C.c_int()
+        res = C.c_double()
+        check(lib.h2c_lowrank_info(h, C.byref(n), C.byref(k), C.byref(sym), C.byref(res), C.byref(mr), C.byref(tot)))
+        X = np.zeros((n.value, k.value), order="F")
+        Y = np.zeros((n.value, k.value), order="F")
+        if k.value:
+            check(lib.h2c_lowrank_download(h, X.ctypes.data_as(C.c_void_p), Y.ctypes.data_as(C.c_void_p)))
+    finally:
+        lib.h2c_lowrank_destroy(h)
+    return LowRankResult(LowRankFactor(X, Y), SampleStats(tot.value, [LevelStats(0, 1, k.value, tot.value)]),
+                         res.value, bool(mr.value), bool(sym.value))
+
+
+@dataclasses.dataclass
+class HybridResult:   # construction.hpp:495-499
+    matrix: H2Matrix
+    stats: SampleStats
+    global_rank: int
+
+
+def hybrid_construct(op, bt, cfg=None):
+    """Global low-rank capture, peel of the residual, global update back (construction.hpp:506-534)."""
+    cfg = cfg or PeelConfig()
+    c = _cfg_c(cfg)
+    h = H()
+    gr, tot = C.c_int64(), C.c_int64()
+    lv = (LevelStatsC * 128)()
+    nl = C.c_int()
+    check(lib.h2c_hybrid_construct(op._h, bt._h, C.byref(c), C.byref(h), C.byref(gr), C.byref(tot), lv, 128,
+                                   C.byref(nl)))
+    levels = [LevelStats(lv[i].level, lv[i].blocks, lv[i].max_rank, lv[i].samples) for i in range(nl.value)]
+    return HybridResult(H2Matrix(h, bt), SampleStats(tot.value, levels), gr.value)

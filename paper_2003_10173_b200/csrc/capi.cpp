@@ -37,6 +37,10 @@ struct h2c_matrix_s {
 struct h2c_dist_plan_s {
     std::shared_ptr<h2b::DistPlan> p;
 };
+struct h2c_lowrank_s {
+    h2b::LowRankResultDev r;
+    int64_t n = 0;
+};
 struct h2c_operator_s {
     std::unique_ptr<h2b::DevOperator> op;
 };
@@ -676,6 +680,86 @@ int h2c_desymmetrized(h2c_matrix h, h2c_matrix* out) {
     return guard([&] {
         need(h != nullptr && out != nullptr, "null argument");
         *out = wrap_matrix(h2b::desymmetrized(*h->h, nullptr));
+    });
+}
+
+// ---- randomized low-rank / hybrid ---------------------------------------------------
+namespace {
+h2b::PeelConfig to_cfg(const h2c_peel_config* cfg) {
+    h2b::PeelConfig c;
+    if (cfg) {
+        c.eps = cfg->eps;
+        c.sample_block_size = cfg->sample_block_size;
+        c.oversampling = cfg->oversampling;
+        c.max_rank = cfg->max_rank;
+        c.seed = cfg->seed;
+        c.norm_scale = cfg->norm_scale;
+        c.crossover_rank_cap = cfg->crossover_rank_cap;
+        c.rng = cfg->rng;
+    }
+    return c;
+}
+}  // namespace
+
+int h2c_randomized_lowrank(h2c_operator op, double eps, int64_t max_rank, const h2c_peel_config* cfg,
+                           h2c_lowrank* out) {
+    return guard([&] {
+        need(op != nullptr && out != nullptr, "null argument");
+        auto f = new h2c_lowrank_s;
+        try {
+            f->r = h2b::randomized_lowrank(*op->op, eps, max_rank, to_cfg(cfg), 0, nullptr);
+            f->n = op->op->dim();
+        } catch (...) {
+            delete f;
+            throw;
+        }
+        *out = f;
+    });
+}
+
+int h2c_lowrank_info(h2c_lowrank f, int64_t* n, int64_t* rank, int* symmetric_form, double* residual_estimate,
+                     int* max_rank_reached, int64_t* total_samples) {
+    return guard([&] {
+        need(f != nullptr, "null argument");
+        if (n) *n = f->n;
+        if (rank) *rank = f->r.rank;
+        if (symmetric_form) *symmetric_form = f->r.X == f->r.Y ? 1 : 0;
+        if (residual_estimate) *residual_estimate = f->r.residual_estimate;
+        if (max_rank_reached) *max_rank_reached = f->r.max_rank_reached ? 1 : 0;
+        if (total_samples) *total_samples = f->r.stats.total;
+    });
+}
+
+int h2c_lowrank_download(h2c_lowrank f, double* X, double* Y) {
+    return guard([&] {
+        need(f != nullptr, "null argument");
+        const size_t cnt = size_t(f->n * f->r.rank);
+        if (cnt == 0) return;
+        if (X) H2B_CUDA(cudaMemcpy(X, f->r.X->data(), cnt * sizeof(double), cudaMemcpyDeviceToHost));
+        if (Y) H2B_CUDA(cudaMemcpy(Y, f->r.Y->data(), cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+void h2c_lowrank_destroy(h2c_lowrank f) {
+    if (f) cudaDeviceSynchronize();
+    delete f;
+}
+
+int h2c_hybrid_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config* cfg, h2c_matrix* out,
+                         int64_t* global_rank, int64_t* total_samples, h2c_level_stats* levels, int max_levels,
+                         int* num_levels) {
+    return guard([&] {
+        need(op != nullptr && bt != nullptr && out != nullptr, "null argument");
+        h2b::HybridResultDev r = h2b::hybrid_construct(*op->op, bt->b, to_cfg(cfg), nullptr);
+        if (global_rank) *global_rank = r.global_rank;
+        if (total_samples) *total_samples = r.stats.total;
+        if (num_levels) *num_levels = int(r.stats.levels.size());
+        if (levels)
+            for (int i = 0; i < int(r.stats.levels.size()) && i < max_levels; ++i) {
+                const h2b::LevelStats& l = r.stats.levels[size_t(i)];
+                levels[i] = h2c_level_stats{l.level, l.blocks, l.max_rank, l.samples};
+            }
+        *out = wrap_matrix(std::move(r.matrix));
     });
 }
 

@@ -163,6 +163,27 @@ struct PeelResult {
 PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, const PeelConfig& cfg,
                           cudaStream_t s);
 
+// global randomized low-rank (construction.hpp:386-491): factor X Y^T (n x k
+// device arrays, user ordering; X == Y for symmetric operators)
+struct LowRankResultDev {
+    int64_t rank = 0;
+    std::shared_ptr<DeviceArray<double>> X, Y;   // Y aliases X for the symmetric form
+    SampleStats stats;
+    double residual_estimate = 0;
+    bool max_rank_reached = false;
+};
+LowRankResultDev randomized_lowrank(DevOperator& op, double eps, int64_t max_rank, const PeelConfig& cfg,
+                                    int stagnation_window, cudaStream_t s);
+// hybrid_construct (construction.hpp:506-534): global low-rank capture, peel of
+// the residual, global update back
+struct HybridResultDev {
+    std::unique_ptr<H2Dev> matrix;
+    SampleStats stats;
+    int64_t global_rank = 0;
+};
+HybridResultDev hybrid_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, const PeelConfig& cfg,
+                                 cudaStream_t s);
+
 // estimate_relative_error (construction.hpp:537-546)
 double estimate_relative_error(DevOperator& op, const H2Dev& h, double op_norm, cudaStream_t s);
 

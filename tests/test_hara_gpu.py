@@ -263,3 +263,53 @@ def test_peel_matches_oracle(cuda, case):
     for g_s, o_s in zip(gl, st["level_samples"]):
         assert abs(g_s - o_s) <= 16 * (1 if sym else 2), (gl, st["level_samples"])
     assert res.stats.consistent() and res.stats.total == op.columns_applied()
+
+
+# ---- global randomized low-rank and hybrid (test_construction.cpp:180-224) -----
+
+def test_randomized_lowrank_exact_rank8(cuda):
+    from paper_2003_10173_b200 import randomized_lowrank
+    b8 = O.gaussian(58, 100, 8)
+    a = b8 @ b8.T
+    op = DenseOperator(a, True)
+    cfg = PeelConfig(norm_scale=n2(a))   # no estimation samples in this budget check
+    op.reset_counter()
+    lr = randomized_lowrank(op, 1e-10, 0, cfg)
+    assert lr.factor.rank() == 8
+    assert op.columns_applied() <= 8 + cfg.sample_block_size + cfg.oversampling
+    assert not lr.max_rank_reached
+    assert rel(lr.factor.X @ lr.factor.Y.T, a) < 1e-9
+    assert lr.symmetric_form and np.array_equal(lr.factor.X, lr.factor.Y)
+
+
+def test_randomized_lowrank_identity_stalls_at_max_rank(cuda):
+    from paper_2003_10173_b200 import randomized_lowrank
+    op = make_operator(64, True, lambda x: x)
+    lr = randomized_lowrank(op, 1e-4, 16, PeelConfig(norm_scale=1.0))
+    assert lr.max_rank_reached
+    assert lr.factor.rank() <= 16
+    assert abs(lr.residual_estimate - 1.0) <= 0.4 * 1.0 + 1e-12
+
+
+def test_randomized_lowrank_nonsymmetric(cuda):
+    from paper_2003_10173_b200 import randomized_lowrank
+    u = O.gaussian(70, 90, 6)
+    v = O.gaussian(71, 90, 6)
+    a = u @ v.T
+    lr = randomized_lowrank(DenseOperator(a, False), 1e-10, 0, PeelConfig())
+    assert lr.factor.rank() == 6 and not lr.symmetric_form
+    assert rel(lr.factor.X @ lr.factor.Y.T, a) < 1e-9
+
+
+def test_hybrid_low_rank_operator(cuda):
+    from paper_2003_10173_b200 import hybrid_construct
+    b20 = O.gaussian(59, 128, 20)
+    a = b20 @ b20.T
+    bt, ref = tree1d(128, 16)
+    cfg = PeelConfig(eps=1e-8)
+    hy = hybrid_construct(DenseOperator(a, True), bt, cfg)
+    assert hy.global_rank == 20
+    assert n2(dense(hy.matrix, ref) - a) <= 3e-8 * n2(a)
+    assert hy.stats.consistent()
+    pr = peel_construct(DenseOperator(a, True), bt, cfg)
+    assert hy.stats.total <= pr.stats.total
