@@ -173,6 +173,53 @@ def algorithmic_flops(m, bt, b):
     return total, stage5
 
 
+def algorithmic_bytes(m, bt, b):
+    """Compulsory HBM bytes of one hgemv: stored payload once, bases and transfers twice
+    (up and down), x read and y written; from the structure, so it holds for sharded matrices too."""
+    ct = bt.tree
+    r, _ = m.ranks()
+    r = r.astype(np.float64)
+    size = (ct.end - ct.begin).astype(np.float64)
+    leaves = ct.leaves
+    nonroot = np.nonzero(ct.parent >= 0)[0]
+    adm, dense = bt.admissible_leaves, bt.dense_leaves
+    canon_a = adm[bt.row[adm] <= bt.col[adm]]
+    canon_d = dense[bt.row[dense] <= bt.col[dense]]
+    U = float(np.sum(size[leaves] * r[leaves]))
+    E = float(np.sum(r[nonroot] * r[ct.parent[nonroot]]))
+    S = float(np.sum(r[bt.row[canon_a]] * r[bt.col[canon_a]]))
+    D = float(np.sum(size[bt.row[canon_d]] * size[bt.col[canon_d]]))
+    return 8.0 * (2 * U + 2 * E + S + D + 2 * ct.n * b)
+
+
+def stage5_roofline(args, m, n, b, F5, stages):
+    """Roofline of the dominant launch (leaf expansion + dense near-field, stage 5): algorithmic flops of
+    the reference for that stage (the kernel also applies U_t E_t, the folded finest downsweep step)."""
+    dom = dict(stages[5])
+    dom["kernel_gflop"] = dom["gflop"]
+    dom["gflop"] = F5 / 1e9
+    sizes = m.packed_sizes()
+    dom["gbytes"] = (8.0 * (sizes[5] + sizes[0]) + 16.0 * n * b) / 1e9   # D and U once, x read, y written
+    hbm, hbm_src = hbm_peak()
+    ai = dom["gflop"] / max(dom["gbytes"], 1e-30)
+    ridge = FP64_PEAK_TFLOPS * 1e3 / hbm
+    if ai >= ridge:
+        achieved = dom["gflop"] / (dom["ms"] / 1e3) / 1e3
+        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE}
+    else:
+        achieved = dom["gbytes"] / (dom["ms"] / 1e3)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": hbm_src}
+    kname = ("seg_gemm_kernel<64,32,2,2,2,32,VEC,kModeY> (leaf expansion + dense near-field)" if b > 2 else
+             "sym_pass64_kernel (dense near-field, each canonical block streamed once) + seg_gemm leaf expansion "
+             "+ csr_sum")
+    roof.update({"kernel": kname, "share_of_step": dom["ms"] / sum(s["ms"] for s in stages.values()),
+                 "traffic": args.traffic, "algorithmic_gflop": dom["gflop"], "algorithmic_gbytes": dom["gbytes"],
+                 "ms": dom["ms"]})
+    return roof
+
+
 def algorithmic_work(m, b, launches_stats=None):
     """F (flops) and B (bytes) of one hgemv per SURVEY §8(d)."""
     sizes = m.packed_sizes()   # U, E, V, F, S, D (doubles)
@@ -197,7 +244,9 @@ def run_b200(args, cfg, world, rank, local, dist):
     bt = build_block_tree(ct, ct, 1.0)
     t_tree = time.perf_counter() - t0
     t0 = time.perf_counter()
-    m = H2Matrix.kernel(bt, pts, cfg["kind"], cfg["ell"], cfg["rank"])
+    # N > 1: every rank generates only its row-subtree shard's payload
+    shard_mode = world > 1 or args.force_shard
+    m = H2Matrix.kernel(bt, pts, cfg["kind"], cfg["ell"], cfg["rank"], shard=(world, rank) if shard_mode else None)
     t_gen = time.perf_counter() - t0
     rng = np.random.default_rng(42)
     x_host = torch.from_numpy(rng.standard_normal((b, n)))      # column-major n x b == row-major b x n
@@ -206,7 +255,7 @@ def run_b200(args, cfg, world, rank, local, dist):
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     sharded = None
-    if world > 1:
+    if shard_mode:
         # row-subtree sharding: each rank computes its subtree's rows; one NCCL all-to-all per hgemv
         from paper_2003_10173_b200.dist import ShardedHgemv
         sharded = ShardedHgemv(m)
@@ -229,7 +278,7 @@ def run_b200(args, cfg, world, rank, local, dist):
     fl = np.zeros(maxrec)
     by = np.zeros(maxrec)
     agg = {}
-    for rep in range(max(3, min(args.steps, 10))):
+    for rep in range(max(3, min(args.steps, 10)) if sharded is None else 0):
         check(lib.h2c_hgemv_stage_times(m._h, 0, 0, n, b, X.data_ptr(), n, Y.data_ptr(), n, sh, maxrec,
                                         C.byref(cnt), st.ctypes.data_as(C.c_void_p), ms.ctypes.data_as(C.c_void_p),
                                         fl.ctypes.data_as(C.c_void_p), by.ctypes.data_as(C.c_void_p)))
@@ -245,8 +294,8 @@ def run_b200(args, cfg, world, rank, local, dist):
     stages = {k: {"ms": v[0] / nrep, "gflop": v[1] / nrep / 1e9, "gbytes": v[2] / nrep / 1e9,
                   "launches": v[3] // nrep} for k, v in agg.items()}
     F, F5 = algorithmic_flops(m, bt, b)
-    Bbytes = algorithmic_work(m, b)
-    launches = m.launches(b)
+    Bbytes = algorithmic_bytes(m, bt, b)
+    launches = m.launches(b) if sharded is None else sharded.plan.launches()
 
     # main timed region
     if dist:
@@ -269,31 +318,15 @@ def run_b200(args, cfg, world, rank, local, dist):
     value = F / t_step / 1e9          # one hgemv of the whole matrix per step (all ranks together)
     gbs = Bbytes / t_step / 1e9
 
-    # dominant kernel roofline: leaf expansion + dense near-field (stage 5); algorithmic flops of the
-    # reference for that stage (the kernel also applies U_t E_t, the folded finest downsweep step)
-    dom = dict(stages[5])
-    dom["kernel_gflop"] = dom["gflop"]
-    dom["gflop"] = F5 / 1e9
-    sizes = m.packed_sizes()
-    dom["gbytes"] = (8.0 * (sizes[5] + sizes[0]) + 16.0 * n * b) / 1e9   # D and U once, x read, y written
-    hbm, hbm_src = hbm_peak()
-    ai = dom["gflop"] / max(dom["gbytes"], 1e-30)
-    ridge = FP64_PEAK_TFLOPS * 1e3 / hbm
-    if ai >= ridge:
-        achieved = dom["gflop"] / (dom["ms"] / 1e3) / 1e3
-        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE}
+    if sharded is not None:
+        # per-GPU roofline of the whole sharded step (stage timers run on the single-GPU path only)
+        per_gpu = F / world / t_step / 1e12
+        roof = {"bound": "tensor", "achieved": per_gpu, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": per_gpu / FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
+                "kernel": "whole sharded hgemv step per GPU (algorithmic flops / world / step time)",
+                "traffic": None}
     else:
-        achieved = dom["gbytes"] / (dom["ms"] / 1e3)
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "peak_source": hbm_src}
-    kname = ("seg_gemm_kernel<64,32,2,2,2,32,VEC,kModeY> (leaf expansion + dense near-field)" if b > 2 else
-             "sym_pass64_kernel (dense near-field, each canonical block streamed once) + seg_gemm leaf expansion "
-             "+ csr_sum")
-    roof.update({"kernel": kname,
-                 "share_of_step": dom["ms"] / sum(s["ms"] for s in stages.values()),
-                 "traffic": args.traffic, "algorithmic_gflop": dom["gflop"], "algorithmic_gbytes": dom["gbytes"],
-                 "ms": dom["ms"]})
+        roof = stage5_roofline(args, m, n, b, F5, stages)
 
     # end-to-end through the public host-buffer API (pinned x in, y out)
     xp = x_host.pin_memory()
@@ -330,20 +363,22 @@ def run_b200(args, cfg, world, rank, local, dist):
         t = torch.tensor([te], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
-    # the synchronous by-value call (H2D, hgemv, D2H, wait) for reference
-    for _ in range(3):
-        check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
-    t0 = time.perf_counter()
-    for _ in range(3):
-        check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
-    ts = (time.perf_counter() - t0) / 3
+    # the synchronous by-value call (H2D, hgemv, D2H, wait) for reference (single-GPU matrix only)
+    ts = None
+    if sharded is None:
+        for _ in range(3):
+            check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
+        t0 = time.perf_counter()
+        for _ in range(3):
+            check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
+        ts = (time.perf_counter() - t0) / 3
     e2e = {"value": F / te / 1e9, "unit": "GFLOP/s", "ms_per_step": te * 1e3,
            "h2d_bytes_per_step": 8 * n * b, "d2h_bytes_per_step": 8 * n * b,
            "path": ("h2c_matvec_host_async on 3 rotating streams: per step pinned host x -> HBM, hgemv, "
                     "HBM -> pinned host y (copies of one step overlap the hgemv of the next)") if sharded is None else
                    "per rank: pinned host x -> HBM, sharded hgemv (NCCL all-to-all), HBM -> pinned host y",
-           "sync_call": {"value": F / ts / 1e9, "ms_per_step": ts * 1e3,
-                         "path": "h2c_matvec_host (H2D, hgemv, D2H, wait; no overlap)"}}
+           "sync_call": None if ts is None else {"value": F / ts / 1e9, "ms_per_step": ts * 1e3,
+                                                 "path": "h2c_matvec_host (H2D, hgemv, D2H, wait; no overlap)"}}
 
     out = {
         "metric": "hgemv GFLOP/s (N=2^20, 32 vectors, fp64)" if args.config == "cfg2" else f"hgemv GFLOP/s ({args.config})",
@@ -599,6 +634,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=list(CONFIGS))
     ap.add_argument("--b", type=int, default=0, help="override the vector count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-shard", action="store_true", help="use the sharded path even at N=1 (testing)")
     ap.add_argument("--hara-rng", default="device", choices=["device", "reference"],
                     help="cfg3 Gaussian panels: device Philox (perf) or the reference host stream")
     ap.add_argument("--traffic", type=float, default=None,
@@ -650,7 +686,7 @@ def main():
             print(json.dumps(out), flush=True)
         return
     out, ctx = run_b200(args, cfg, world, rank, local, dist)
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline_sample(args, ctx)
         except Exception as e:  # the baseline is reported, never fatal

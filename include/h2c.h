@@ -92,6 +92,11 @@ int h2c_matrix_download(h2c_matrix h, double* U, double* E, double* V, double* F
 int h2c_matrix_kernel(h2c_block_tree b, const double* coords /* user order, n x dim */, int kind, double ell,
                       int rank, h2c_matrix* out);
 
+/* the same matrix, but only the payload rank `shard` of `nranks` needs for the
+ * row-subtree sharded hgemv (h2c_dist_*): memory per rank ~ 1/nranks + top levels */
+int h2c_matrix_kernel_sharded(h2c_block_tree b, const double* coords, int kind, double ell, int rank, int nranks,
+                              int shard, h2c_matrix* out);
+
 /* ---- hgemv: replaces H2Matrix::matvec / matvec_transpose (user ordering)
  *      and matvec_internal / matvec_transpose_internal (h2_matrix.hpp:108-124)
  *   y = alpha * op(H) x + beta * y  with x, y DEVICE pointers (n x b, col-major).
@@ -188,6 +193,8 @@ void h2c_dist_plan_destroy(h2c_dist_plan p);
 /* send_rows / recv_rows: nranks entries each; owned internal row range [begin, begin + rows) */
 int h2c_dist_plan_counts(h2c_dist_plan p, int64_t* send_rows, int64_t* recv_rows, int64_t* owned_begin,
                          int64_t* owned_rows);
+/* kernel launches of one sharded hgemv on this rank (begin + end) */
+int h2c_dist_plan_launches(h2c_dist_plan p, int* launches);
 /* x: full n x b user-order device matrix (only owned rows are read) */
 int h2c_dist_hgemv_begin(h2c_dist_plan p, int64_t b, const double* x, int64_t ldx, double* sendbuf, void* stream);
 /* y: full n x b user-order device matrix (only owned rows are written: y = alpha H x + beta y) */

@@ -75,6 +75,7 @@ _sig("h2c_matrix_ranks", i32, H, vp, vp)
 _sig("h2c_matrix_upload", i32, H, vp, vp, vp, vp, vp, vp)
 _sig("h2c_matrix_download", i32, H, vp, vp, vp, vp, vp, vp)
 _sig("h2c_matrix_kernel", i32, H, vp, i32, f64, i32, P(H))
+_sig("h2c_matrix_kernel_sharded", i32, H, vp, i32, f64, i32, i32, i32, P(H))
 _sig("h2c_hgemv", i32, H, i32, i32, i64, i64, vp, i64, vp, i64, f64, f64, vp)
 _sig("h2c_matvec_host", i32, H, i32, i32, i64, i64, vp, vp)
 _sig("h2c_matvec_host_async", i32, H, i32, i32, i64, i64, vp, vp, vp)
@@ -132,6 +133,7 @@ _sig("h2c_estimate_relative_error", i32, H, H, f64, P(f64))
 _sig("h2c_dist_plan_create", i32, H, i32, i32, i32, P(H))
 _sig("h2c_dist_plan_destroy", None, H)
 _sig("h2c_dist_plan_counts", i32, H, vp, vp, P(i64), P(i64))
+_sig("h2c_dist_plan_launches", i32, H, P(i32))
 _sig("h2c_dist_hgemv_begin", i32, H, i64, vp, i64, vp, vp)
 _sig("h2c_dist_hgemv_end", i32, H, i64, vp, vp, i64, f64, f64, vp)
 _sig("h2c_partition_owner", i32, H, i32, vp)

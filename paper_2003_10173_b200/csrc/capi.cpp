@@ -258,6 +258,22 @@ int h2c_matrix_kernel(h2c_block_tree b, const double* coords, int kind, double e
     });
 }
 
+int h2c_matrix_kernel_sharded(h2c_block_tree b, const double* coords, int kind, double ell, int rank, int nranks,
+                              int shard, h2c_matrix* out) {
+    return guard([&] {
+        need(b != nullptr && coords != nullptr && out != nullptr, "null argument");
+        need(kind >= 0 && kind <= 2 && rank >= 1, "kernel: bad kind or rank");
+        auto m = new h2c_matrix_s;
+        try {
+            m->h = h2b::make_kernel_h2(b->b, coords, kind, ell, rank, nranks, shard);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
 int h2c_hgemv(h2c_matrix h, int transpose, int ordering, int64_t n, int64_t b, const double* x, int64_t ldx,
               double* y, int64_t ldy, double alpha, double beta, void* stream) {
     return guard([&] {
@@ -508,6 +524,13 @@ int h2c_dist_plan_counts(h2c_dist_plan p, int64_t* send_rows, int64_t* recv_rows
         const int64_t rows = h2b::dist_owned_rows(*p->p, &beg);
         if (owned_begin) *owned_begin = beg;
         if (owned_rows) *owned_rows = rows;
+    });
+}
+
+int h2c_dist_plan_launches(h2c_dist_plan p, int* launches) {
+    return guard([&] {
+        need(p != nullptr && launches != nullptr, "null argument");
+        *launches = h2b::dist_launch_count(*p->p);
     });
 }
 

@@ -24,6 +24,8 @@ struct BasisDev {
     std::vector<int64_t> xfer_off;    // per node, -1 for the root
     DeviceArray<double> leaf, xfer;
     void layout(const ClusterTree& t);   // offsets from ranks
+    // only the marked leaves / transfers get storage (offset -1 otherwise)
+    void layout(const ClusterTree& t, const std::vector<char>* need_leaf, const std::vector<char>* need_xfer);
 };
 
 struct HgemvPlan;
@@ -40,6 +42,10 @@ struct H2Dev {
     const BasisDev& vbasis() const { return symmetric ? row : col; }
     bool stores(int b) const { return !symmetric || bt->canonical(b); }
     void layout_blocks();              // s_off / d_off from ranks
+    void layout_blocks(const std::vector<char>* need_s, const std::vector<char>* need_d);
+    // row-subtree shard: only the payload rank `shard_rank` of `shard_nranks`
+    // needs for its sharded hgemv is stored (0 = full matrix)
+    int shard_nranks = 0, shard_rank = -1;
 
     mutable std::mutex plan_mu;
     mutable std::shared_ptr<HgemvPlan> plan[3];   // [transpose], [2]: symmetric few-vector plan
@@ -140,5 +146,6 @@ void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, doub
 void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha, double beta,
                     cudaStream_t s);
 int64_t dist_owned_rows(const DistPlan& p, int64_t* begin);
+int dist_launch_count(const DistPlan& p);
 
 }  // namespace h2b

@@ -1330,6 +1330,8 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
     if (b < 1) throw std::invalid_argument("matvec: need at least one column");
     if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
+    if (h.shard_nranks > 0)
+        throw std::invalid_argument("hgemv: this matrix holds one row-subtree shard; use the sharded hgemv");
     auto plan = select_plan(h, transpose, b);
     HgemvGraph& g = ws.graph;
     HgemvGraph::Key k;
@@ -1625,6 +1627,8 @@ __global__ void exchange_kernel(const XItem* __restrict__ items, int64_t b, doub
 }  // namespace
 
 std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nranks, int rank) {
+    if (h.shard_nranks > 0 && (h.shard_nranks != nranks || h.shard_rank != rank))
+        throw std::invalid_argument("dist plan: the matrix holds a different shard");
     auto p = std::make_shared<DistPlan>();
     p->h = &h;
     p->transpose = transpose;
@@ -1662,6 +1666,13 @@ std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nra
 void dist_counts(const DistPlan& p, std::vector<int64_t>& send_rows, std::vector<int64_t>& recv_rows) {
     send_rows = p.send_rows;
     recv_rows = p.recv_rows;
+}
+
+int dist_launch_count(const DistPlan& p) {
+    int c = p.plan->num_leaves > 0 ? 1 : 0;
+    for (const LaunchDesc& ld : p.plan->launches)
+        if (ld.task_end > ld.task_begin || ld.item_end > ld.item_begin) ++c;
+    return c + (p.nsend ? 1 : 0) + (p.nrecv ? 1 : 0);
 }
 
 int64_t dist_owned_rows(const DistPlan& p, int64_t* begin) {

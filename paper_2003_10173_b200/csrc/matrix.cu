@@ -9,17 +9,21 @@
 
 namespace h2b {
 
-void BasisDev::layout(const ClusterTree& t) {
+void BasisDev::layout(const ClusterTree& t) { layout(t, nullptr, nullptr); }
+
+void BasisDev::layout(const ClusterTree& t, const std::vector<char>* need_leaf, const std::vector<char>* need_xfer) {
     const int nn = t.num_nodes();
     leaf_off.assign(size_t(nn), -1);
     xfer_off.assign(size_t(nn), -1);
     int64_t lo = 0, xo = 0;
     for (int v : t.leaves) {
+        if (need_leaf && !(*need_leaf)[size_t(v)]) continue;
         leaf_off[size_t(v)] = lo;
         lo += t.size(v) * rank[size_t(v)];
     }
     for (int v = 0; v < nn; ++v) {
         if (t.parent[size_t(v)] < 0) continue;
+        if (need_xfer && !(*need_xfer)[size_t(v)]) continue;
         xfer_off[size_t(v)] = xo;
         xo += int64_t(rank[size_t(v)]) * rank[size_t(t.parent[size_t(v)])];
     }
@@ -27,7 +31,9 @@ void BasisDev::layout(const ClusterTree& t) {
     xfer.resize(size_t(xo));
 }
 
-void H2Dev::layout_blocks() {
+void H2Dev::layout_blocks() { layout_blocks(nullptr, nullptr); }
+
+void H2Dev::layout_blocks(const std::vector<char>* need_s, const std::vector<char>* need_d) {
     const ClusterTree& t = tree();
     const BasisDev& vb = vbasis();
     s_off.assign(bt->adm.size(), -1);
@@ -35,13 +41,13 @@ void H2Dev::layout_blocks() {
     int64_t so = 0, dof = 0;
     for (size_t i = 0; i < bt->adm.size(); ++i) {
         const int b = bt->adm[i];
-        if (!stores(b)) continue;
+        if (!stores(b) || (need_s && !(*need_s)[i])) continue;
         s_off[i] = so;
         so += int64_t(row.rank[size_t(bt->row[size_t(b)])]) * vb.rank[size_t(bt->col[size_t(b)])];
     }
     for (size_t i = 0; i < bt->dense.size(); ++i) {
         const int b = bt->dense[i];
-        if (!stores(b)) continue;
+        if (!stores(b) || (need_d && !(*need_d)[i])) continue;
         d_off[i] = dof;
         dof += t.size(bt->row[size_t(b)]) * t.size(bt->col[size_t(b)]);
     }
@@ -172,7 +178,7 @@ __global__ void gen_leaf_kernel(const int* leaves, int nleaves, const int64_t* b
 __global__ void gen_transfer_kernel(int nn, const int* parent, const int* rank, const int64_t* off,
                                     const NodeGrid* grids, int dim, double* E) {
     const int v = blockIdx.x;
-    if (v >= nn || parent[v] < 0) return;
+    if (v >= nn || parent[v] < 0 || off[v] < 0) return;
     const int kc = rank[v], kp = rank[parent[v]];
     for (int idx = threadIdx.x; idx < kc * kp; idx += blockDim.x) {
         const int ac = idx % kc, ap = idx / kc;
@@ -243,12 +249,43 @@ void axis_counts(int dim, int k, const double* ext, int* p) {
 }  // namespace
 
 std::unique_ptr<H2Dev> make_kernel_h2(std::shared_ptr<const BlockTree> bt, const double* coords, int kind,
-                                      double ell, int rank) {
+                                      double ell, int rank, int shard_nranks, int shard_rank) {
     const ClusterTree& t = *bt->tree;
     const int nn = t.num_nodes(), dim = t.dim;
     std::vector<int> ranks(static_cast<size_t>(nn));
     for (int v = 0; v < nn; ++v) ranks[size_t(v)] = int(std::min<int64_t>(rank, t.size(v)));
-    auto h = make_h2(bt, true, ranks.data(), nullptr);
+    std::unique_ptr<H2Dev> h;
+    if (shard_nranks > 0) {
+        // only the payload this rank's sharded hgemv reads (see make_dist_plan):
+        // owned leaves' bases, transfers of local nodes and of every partition
+        // root, couplings touching a local node, dense blocks touching an owned leaf
+        const DistSpec d = make_dist_spec(t, shard_nranks, shard_rank);
+        auto own = [&](int v) { return d.owner[size_t(v)] == shard_rank; };
+        auto local = [&](int v) { return d.owner[size_t(v)] == shard_rank || d.owner[size_t(v)] < 0; };
+        std::vector<char> nl(size_t(nn), 0), nx(size_t(nn), 0), ns(bt->adm.size(), 0), nd(bt->dense.size(), 0);
+        for (int v = 0; v < nn; ++v) {
+            nl[size_t(v)] = own(v);
+            nx[size_t(v)] = local(v) || t.level[size_t(v)] == d.lp;
+        }
+        for (size_t i = 0; i < bt->adm.size(); ++i) {
+            const int b = bt->adm[i];
+            ns[i] = local(bt->row[size_t(b)]) || local(bt->col[size_t(b)]);
+        }
+        for (size_t i = 0; i < bt->dense.size(); ++i) {
+            const int b = bt->dense[i];
+            nd[i] = own(bt->row[size_t(b)]) || own(bt->col[size_t(b)]);
+        }
+        h = std::make_unique<H2Dev>();
+        h->bt = bt;
+        h->symmetric = true;
+        h->row.rank = ranks;
+        h->row.layout(t, &nl, &nx);
+        h->layout_blocks(&ns, &nd);
+        h->shard_nranks = shard_nranks;
+        h->shard_rank = shard_rank;
+    } else {
+        h = make_h2(bt, true, ranks.data(), nullptr);
+    }
     std::vector<NodeGrid> grids(static_cast<size_t>(nn));
     for (int v = 0; v < nn; ++v) {
         NodeGrid& g = grids[size_t(v)];
@@ -278,15 +315,20 @@ std::unique_ptr<H2Dev> make_kernel_h2(std::shared_ptr<const BlockTree> bt, const
     dperm.upload(t.perm);
     dbeg.upload(t.begin);
     dend.upload(t.end);
-    dleaves.upload(t.leaves);
+    std::vector<int> gl;
+    for (int v : t.leaves)
+        if (h->row.leaf_off[size_t(v)] >= 0) gl.push_back(v);
+    dleaves.upload(gl);
     drank.upload(h->row.rank);
     dpar.upload(t.parent);
     dloff.upload(h->row.leaf_off);
     dxoff.upload(h->row.xfer_off);
-    gen_leaf_kernel<<<int(t.leaves.size()), 256>>>(dleaves.data(), int(t.leaves.size()), dbeg.data(), dend.data(),
-                                                   drank.data(), dloff.data(), dgrids.data(), dpts.data(), dim, t.n,
-                                                   dperm.data(), h->row.leaf.data());
-    H2B_LAUNCH();
+    if (!gl.empty()) {
+        gen_leaf_kernel<<<int(gl.size()), 256>>>(dleaves.data(), int(gl.size()), dbeg.data(), dend.data(),
+                                                 drank.data(), dloff.data(), dgrids.data(), dpts.data(), dim, t.n,
+                                                 dperm.data(), h->row.leaf.data());
+        H2B_LAUNCH();
+    }
     gen_transfer_kernel<<<nn, 256>>>(nn, dpar.data(), drank.data(), dxoff.data(), dgrids.data(), dim, h->row.xfer.data());
     H2B_LAUNCH();
     std::vector<int> sr, sc, dr, dc;

@@ -18,7 +18,8 @@ void download_packed(const H2Dev& h, double* const parts[6]);
 // symmetric kernel matrix K(x,y) (kind 0 exponential, 1 Gaussian, 2 Matern-3/2,
 // length scale ell) with uniform rank, generated on the device by Chebyshev
 // tensor interpolation; coords n x dim column-major in user ordering
+// shard_nranks > 0: only the payload of rank `shard_rank`'s row-subtree shard
 std::unique_ptr<H2Dev> make_kernel_h2(std::shared_ptr<const BlockTree> bt, const double* coords, int kind,
-                                      double ell, int rank);
+                                      double ell, int rank, int shard_nranks = 0, int shard_rank = -1);
 
 }  // namespace h2b

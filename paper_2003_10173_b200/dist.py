@@ -59,6 +59,11 @@ class DistPlan:
             lib.h2c_dist_plan_destroy(self._h)
             self._h = None
 
+    def launches(self):
+        v = C.c_int()
+        check(lib.h2c_dist_plan_launches(self._h, C.byref(v)))
+        return v.value
+
     def begin(self, x, sendbuf, b, stream=None):
         check(lib.h2c_dist_hgemv_begin(self._h, int(b), x.data_ptr(), x.stride(1) if x.dim() == 2 else x.shape[0],
                                        sendbuf.data_ptr(), stream))

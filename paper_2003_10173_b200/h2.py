@@ -193,13 +193,18 @@ class H2Matrix:
         return m
 
     @staticmethod
-    def kernel(bt, points, kind="gaussian", ell=0.1, rank=32):
-        """Symmetric kernel matrix generated on the device (benchmark inputs)."""
+    def kernel(bt, points, kind="gaussian", ell=0.1, rank=32, shard=None):
+        """Symmetric kernel matrix generated on the device (benchmark inputs).
+        shard=(nranks, rank): only that row-subtree shard's payload (sharded hgemv only)."""
         kinds = {"exponential": 0, "gaussian": 1, "matern32": 2}
         pts = np.asfortranarray(np.asarray(points, np.float64).reshape(bt.tree.n, -1))
         h = H()
-        check(lib.h2c_matrix_kernel(bt._h, pts.ctypes.data_as(C.c_void_p), kinds[kind], float(ell), int(rank),
-                                    C.byref(h)))
+        if shard is None:
+            check(lib.h2c_matrix_kernel(bt._h, pts.ctypes.data_as(C.c_void_p), kinds[kind], float(ell), int(rank),
+                                        C.byref(h)))
+        else:
+            check(lib.h2c_matrix_kernel_sharded(bt._h, pts.ctypes.data_as(C.c_void_p), kinds[kind], float(ell),
+                                                int(rank), int(shard[0]), int(shard[1]), C.byref(h)))
         return H2Matrix(h, bt)
 
     # ---- properties ------------------------------------------------------

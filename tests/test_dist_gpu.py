@@ -77,3 +77,37 @@ def test_sharded_exchange_volume_2d(cuda):
     owned = pts.shape[0] // 8
     # measured 17,920 rows per vector column at this size (x-hat + x halo)
     assert recv <= 2.5 * owned, (recv, owned)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_payload_equals_unsharded(cuda, P):
+    # each rank generates only its shard's payload; the assembled y is bitwise the full hgemv
+    import torch
+    pts = O.grid2d(96, 96)
+    ct = build_cluster_tree(pts, 32)
+    bt = build_block_tree(ct, ct, 1.0)
+    full = H2Matrix.kernel(bt, pts, "gaussian", 0.1, 16)
+    n, b = pts.shape[0], 32
+    x = torch.randn(b, n, dtype=torch.float64, device=cuda).t()
+    y_ref = torch.zeros(b, n, dtype=torch.float64, device=cuda).t()
+    full.hgemv(x, y_ref)
+    shards = [H2Matrix.kernel(bt, pts, "gaussian", 0.1, 16, shard=(P, r)) for r in range(P)]
+    plans = [DistPlan(shards[r], P, r) for r in range(P)]
+    sends = [torch.zeros(max(1, int(p.send_rows.sum()) * b), dtype=torch.float64, device=cuda) for p in plans]
+    for p, s in zip(plans, sends):
+        p.begin(x, s, b)
+    y = torch.full((b, n), 3.0, dtype=torch.float64, device=cuda).t()
+    for r, p in enumerate(plans):
+        segs = [sends[q][int(pq.send_rows[:r].sum()) * b:int(pq.send_rows[:r + 1].sum()) * b]
+                for q, pq in enumerate(plans)]
+        recv = torch.cat(segs)
+        if recv.numel() == 0:
+            recv = torch.zeros(1, dtype=torch.float64, device=cuda)
+        p.end(recv, y, b)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    fsz = sum(full.packed_sizes())
+    ssz = [sum(s.packed_sizes()) for s in shards]
+    assert max(ssz) < 0.8 * fsz and sum(ssz) < 1.6 * fsz   # payload is actually sharded
+    with pytest.raises(ValueError):
+        shards[0].hgemv(x, y)
