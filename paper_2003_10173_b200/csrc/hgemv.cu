@@ -218,10 +218,19 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
     }
     int ce = tk.e_begin, ck = 0;   // consumer cursor
     for (int s = 0; s < nsteps; ++s) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        if (s + STAGES - 1 < nsteps) issue((s + STAGES - 1) % STAGES);
-        cp_async_commit();
+        if constexpr (STAGES == 1) {
+            // single buffer: the other CTAs resident on the SM hide this CTA's load latency
+            __syncthreads();
+            issue(0);
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncthreads();
+        } else {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            if (s + STAGES - 1 < nsteps) issue((s + STAGES - 1) % STAGES);
+            cp_async_commit();
+        }
         const SegEntry& ec = args.entries[ce];
         const bool trans = ec.trans;
         const int ksteps = (min(KC, ec.k - ck) + 3) >> 2;
@@ -1284,6 +1293,7 @@ void dispatch(const SegArgs& a, int ntasks, int64_t b, int mt, bool vec, int mod
         if (nb == 32) {
             if (vec) switch (g_tune[0]) {
                 case 1: return launch_vec_mode<64, 32, 4, 1, 2, 32>(a, ntasks, b, mode, s);
+                case 2: return launch_vec_mode<64, 32, 2, 2, 1, 32>(a, ntasks, b, mode, s);
                 default: break;
             }
             launch_mode<64, 32, 2, 2>(a, ntasks, b, vec, mode, s);
@@ -1293,10 +1303,11 @@ void dispatch(const SegArgs& a, int ntasks, int64_t b, int mt, bool vec, int mod
     } else {
         if (nb == 32) {
             if (vec) switch (g_tune[1]) {
-                case 1: return launch_vec_mode<32, 32, 2, 2, 3, 32>(a, ntasks, b, mode, s);
+                case 1: return launch_vec_mode<32, 32, 2, 2, 2, 32>(a, ntasks, b, mode, s);
                 default: break;
             }
-            launch_mode<32, 32, 2, 2>(a, ntasks, b, vec, mode, s);
+            // single-buffered 18 KB CTAs: up to 12 per SM, whose interleaving hides the loads
+            launch_mode<32, 32, 2, 2, 1>(a, ntasks, b, vec, mode, s);
         }
         else if (nb == 16) launch_mode<32, 16, 2, 2>(a, ntasks, b, vec, mode, s);
         else launch_mode<32, 8, 4, 1>(a, ntasks, b, vec, mode, s);
