@@ -31,6 +31,26 @@ using la::SvdDesc;
 
 namespace {
 
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+// host wall time per construction phase (stream synchronised at the phase end):
+// 0 panel RNG, 1 operator applies, 2 residual hgemv of the partial matrix,
+// 3 absorb_panel, 4 transposed-pass bookkeeping, 5 local updates, 6 recompress,
+// 7 dense-leaf extraction
+double g_phase_ms[16];   // 8 orthogonalize, 9 truncation bases, 10 projection (inside recompress)
+struct Phase {
+    int id;
+    cudaStream_t s;
+    Clock::time_point t0;
+    Phase(int i, cudaStream_t st) : id(i), s(st), t0(Clock::now()) {}
+    ~Phase() {
+        cudaStreamSynchronize(s);
+        g_phase_ms[id] += ms_since(t0);
+    }
+};
+
 int ld1(int64_t x) { return int(std::max<int64_t>(x, 1)); }
 
 double* Up(const BasisDev& b, int v) { return const_cast<double*>(b.leaf.data()) + b.leaf_off[size_t(v)]; }
@@ -244,6 +264,7 @@ std::vector<int> ortho_ranks(const ClusterTree& ct, const BasisDev& b) {
 }  // namespace
 
 std::unique_ptr<H2Dev> orthogonalize(const H2Dev& h, cudaStream_t s) {
+    Phase ph(8, s);
     const ClusterTree& ct = h.tree();
     const BlockTree& bt = *h.bt;
     const std::vector<int> kr = ortho_ranks(ct, h.row);
@@ -461,9 +482,12 @@ std::unique_ptr<H2Dev> recompress(const H2Dev& hin, double eps, cudaStream_t s) 
         by_row[size_t(bt.row[size_t(b)])].push_back(i);
         by_col[size_t(bt.col[size_t(b)])].push_back(i);
     }
+    Phase* ph9 = new Phase(9, s);
     Truncation wr = truncation_bases(g, true, eps, level_corr, by_row, by_col, s);
     Truncation wc_store;
     if (!g.symmetric) wc_store = truncation_bases(g, false, eps, level_corr, by_row, by_col, s);
+    delete ph9;
+    Phase* ph10 = new Phase(10, s);
     const Truncation& wc = g.symmetric ? wr : wc_store;
     auto out = make_h2(g.bt, g.symmetric, wr.rank.data(), g.symmetric ? nullptr : wc.rank.data());
     // couplings: S <- w_row^T S w_col
@@ -496,6 +520,7 @@ std::unique_ptr<H2Dev> recompress(const H2Dev& hin, double eps, cudaStream_t s) 
     if (!g.symmetric) project_basis(ct, g.col, out->col, wc, s);
     copy_array(out->D, g.D, s);
     out->orthonormal = false;
+    delete ph10;
     return orthogonalize(*out, s);
 }
 
@@ -629,26 +654,7 @@ std::unique_ptr<H2Dev> apply_local_updates(const H2Dev& h, const std::vector<Loc
 // peel_construct (construction.hpp:226-382)
 // ---------------------------------------------------------------------------
 namespace {
-using Clock = std::chrono::steady_clock;
-double ms_since(Clock::time_point t0) {
-    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
-}
 
-// host wall time per construction phase (stream synchronised at the phase end):
-// 0 panel RNG, 1 operator applies, 2 residual hgemv of the partial matrix,
-// 3 absorb_panel, 4 transposed-pass bookkeeping, 5 local updates, 6 recompress,
-// 7 dense-leaf extraction
-double g_phase_ms[8];
-struct Phase {
-    int id;
-    cudaStream_t s;
-    Clock::time_point t0;
-    Phase(int i, cudaStream_t st) : id(i), s(st), t0(Clock::now()) {}
-    ~Phase() {
-        cudaStreamSynchronize(s);
-        g_phase_ms[id] += ms_since(t0);
-    }
-};
 
 struct PeelContext {
     DevOperator& op;
@@ -858,7 +864,7 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
 PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, const PeelConfig& cfg,
                           cudaStream_t s) {
     const auto t_start = Clock::now();
-    std::fill(g_phase_ms, g_phase_ms + 8, 0.0);
+    std::fill(g_phase_ms, g_phase_ms + 16, 0.0);
     const ClusterTree& ct = *bt->tree;
     if (ct.n != op.dim()) throw std::invalid_argument("peel_construct: dimension mismatch");
     std::mt19937_64 rng(cfg.seed);
@@ -967,6 +973,6 @@ double estimate_relative_error(DevOperator& op, const H2Dev& h, double op_norm, 
 
 // diagnostic hook (not part of the public ABI): per-phase host wall time of the last peel_construct
 extern "C" int h2b_hara_phase_ms(double* out, int n) {
-    for (int i = 0; i < n && i < 8; ++i) out[i] = h2b::g_phase_ms[i];
+    for (int i = 0; i < n && i < 16; ++i) out[i] = h2b::g_phase_ms[i];
     return 0;
 }
