@@ -32,6 +32,7 @@ extern "C" {
 #define H2C_CUDA_ERROR (-5)       /* CUDA failure (no reference counterpart) */
 #define H2C_CALLBACK_ERROR (-6)   /* user operator callback returned non-zero */
 #define H2C_DIVERGENCE_ERROR (-7) /* h2::divergence_error    (inversion.hpp:41-46) */
+#define H2C_IO_ERROR (-8)         /* h2::io_error            (types.hpp:29-38); kind via h2c_last_io_error_kind */
 
 typedef struct h2c_cluster_tree_s* h2c_cluster_tree;
 typedef struct h2c_block_tree_s* h2c_block_tree;
@@ -62,6 +63,9 @@ void h2c_block_tree_destroy(h2c_block_tree b);
 int h2c_block_tree_info(h2c_block_tree b, int* num_nodes, int* num_admissible, int* num_dense, int* max_level);
 /* node(b) fields; tag 0 interior, 1 admissible, 2 dense (block_tree.hpp:29-39) */
 int h2c_block_tree_nodes(h2c_block_tree b, int* row, int* col, int* level, int* parent, int* tag);
+/* eta(), mode() (block_tree.hpp:120-124) and the row/column cluster tree (new handle, shared tree) */
+int h2c_block_tree_params(h2c_block_tree b, double* eta, int* weak);
+int h2c_block_tree_cluster_tree(h2c_block_tree b, h2c_cluster_tree* out);
 /* admissible_leaves(), dense_leaves() (block_tree.hpp:64-65) */
 int h2c_block_tree_leaves(h2c_block_tree b, int* admissible, int* dense);
 
@@ -258,6 +262,18 @@ void h2c_lowrank_destroy(h2c_lowrank f);
 int h2c_hybrid_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config* cfg, h2c_matrix* out,
                          int64_t* global_rank, int64_t* total_samples, h2c_level_stats* levels, int max_levels,
                          int* num_levels);
+
+/* ---- H2M1 container (serialize.hpp; SURVEY §8(f) "next"): byte-compatible
+ *      with the reference's serialize / deserialize / write_h2_file / read_h2_file */
+/* serialized size in bytes, then the bytes into a caller buffer of that size */
+int h2c_serialize_size(h2c_matrix h, int64_t* bytes);
+int h2c_serialize(h2c_matrix h, void* buf, int64_t bytes);
+/* new block tree (rebuilt from the stored cluster tree and (eta, mode)) and matrix */
+int h2c_deserialize(const void* buf, int64_t bytes, h2c_block_tree* bt_out, h2c_matrix* out);
+int h2c_write_h2_file(h2c_matrix h, const char* path);
+int h2c_read_h2_file(const char* path, h2c_block_tree* bt_out, h2c_matrix* out);
+/* kind of the last H2C_IO_ERROR on this thread: 0 bad_magic, 1 version_mismatch, 2 truncated, 3 malformed */
+int h2c_last_io_error_kind(void);
 
 #ifdef __cplusplus
 }

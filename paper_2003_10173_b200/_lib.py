@@ -66,6 +66,8 @@ _sig("h2c_block_tree_destroy", None, H)
 _sig("h2c_block_tree_info", i32, H, P(i32), P(i32), P(i32), P(i32))
 _sig("h2c_block_tree_nodes", i32, H, vp, vp, vp, vp, vp)
 _sig("h2c_block_tree_leaves", i32, H, vp, vp)
+_sig("h2c_block_tree_params", i32, H, P(f64), P(i32))
+_sig("h2c_block_tree_cluster_tree", i32, H, P(H))
 _sig("h2c_matrix_create", i32, H, i32, vp, vp, P(H))
 _sig("h2c_matrix_destroy", None, H)
 _sig("h2c_matrix_info", i32, H, P(i64), P(i32), P(i32))
@@ -162,3 +164,34 @@ _sig("h2c_lowrank_info", i32, H, P(i64), P(i64), P(i32), P(f64), P(i32), P(i64))
 _sig("h2c_lowrank_download", i32, H, vp, vp)
 _sig("h2c_lowrank_destroy", None, H)
 _sig("h2c_hybrid_construct", i32, H, H, P(PeelConfigC), P(H), P(i64), P(i64), P(LevelStatsC), i32, P(i32))
+
+H2C_IO_ERROR = -8
+
+
+class io_error(RuntimeError):
+    """Mirror of h2::io_error (types.hpp:29-38); .kind in {bad_magic, version_mismatch, truncated, malformed}."""
+
+    KINDS = ("bad_magic", "version_mismatch", "truncated", "malformed")
+
+    def __init__(self, msg, kind):
+        super().__init__(msg)
+        self.kind = kind
+
+
+_check_base = check
+
+
+def check(rc):   # noqa: F811  (extends the mapping with io_error)
+    if rc == H2C_IO_ERROR:
+        k = lib.h2c_last_io_error_kind()
+        raise io_error(lib.h2c_last_error().decode(errors="replace"),
+                       io_error.KINDS[k] if 0 <= k < 4 else "malformed")
+    _check_base(rc)
+
+
+_sig("h2c_serialize_size", i32, H, P(i64))
+_sig("h2c_serialize", i32, H, vp, i64)
+_sig("h2c_deserialize", i32, vp, i64, P(H), P(H))
+_sig("h2c_write_h2_file", i32, H, C.c_char_p)
+_sig("h2c_read_h2_file", i32, C.c_char_p, P(H), P(H))
+_sig("h2c_last_io_error_kind", i32)

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -11,6 +12,7 @@
 #include "h2dev.hpp"
 #include "hara.hpp"
 #include "inversion.hpp"
+#include "serialize.hpp"
 #include "matrix.hpp"
 
 struct h2c_cluster_tree_s {
@@ -47,6 +49,7 @@ struct h2c_operator_s {
 
 namespace {
 thread_local std::string g_err;
+thread_local int g_io_kind = -1;
 
 template <class F>
 int guard(F&& f) {
@@ -56,6 +59,10 @@ int guard(F&& f) {
     } catch (const h2b::cuda_error& e) {
         g_err = e.what();
         return H2C_CUDA_ERROR;
+    } catch (const h2b::io_error& e) {
+        g_err = e.what();
+        g_io_kind = int(e.kind);
+        return H2C_IO_ERROR;
     } catch (const h2b::divergence_error& e) {
         g_err = e.what();
         return H2C_DIVERGENCE_ERROR;
@@ -156,6 +163,21 @@ int h2c_block_tree_nodes(h2c_block_tree b, int* row, int* col, int* level, int* 
         if (level) std::memcpy(level, t.level.data(), nn * sizeof(int));
         if (parent) std::memcpy(parent, t.parent.data(), nn * sizeof(int));
         if (tag) std::memcpy(tag, t.tag.data(), nn * sizeof(int));
+    });
+}
+
+int h2c_block_tree_params(h2c_block_tree b, double* eta, int* weak) {
+    return guard([&] {
+        need(b != nullptr, "null block tree");
+        if (eta) *eta = b->b->eta;
+        if (weak) *weak = b->b->weak ? 1 : 0;
+    });
+}
+
+int h2c_block_tree_cluster_tree(h2c_block_tree b, h2c_cluster_tree* out) {
+    return guard([&] {
+        need(b != nullptr && out != nullptr, "null argument");
+        *out = new h2c_cluster_tree_s{std::const_pointer_cast<h2b::ClusterTree>(b->b->tree)};
     });
 }
 
@@ -684,7 +706,11 @@ int h2c_h_inverse(h2c_matrix a, h2c_matrix x0, int method, int arg, int dynamic_
                                                                           max_iter, nullptr);
             export_trace(r.trace, rows, max_rows, num_rows, final_residual, converged);
             *out = wrap_matrix(std::move(r.X));
-        } catch (const h2b::divergence_error& e) {
+        } catch (const h2b::io_error& e) {
+        g_err = e.what();
+        g_io_kind = int(e.kind);
+        return H2C_IO_ERROR;
+    } catch (const h2b::divergence_error& e) {
             export_trace(e.trace, rows, max_rows, num_rows, final_residual, converged);
             throw;
         }
@@ -785,5 +811,65 @@ int h2c_hybrid_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_conf
         *out = wrap_matrix(std::move(r.matrix));
     });
 }
+
+// ---- H2M1 --------------------------------------------------------------------------
+int h2c_serialize_size(h2c_matrix h, int64_t* bytes) {
+    return guard([&] {
+        need(h != nullptr && bytes != nullptr, "null argument");
+        *bytes = int64_t(h2b::serialize(*h->h).size());
+    });
+}
+
+int h2c_serialize(h2c_matrix h, void* buf, int64_t bytes) {
+    return guard([&] {
+        need(h != nullptr && buf != nullptr, "null argument");
+        const std::string s = h2b::serialize(*h->h);
+        need(int64_t(s.size()) <= bytes, "serialize: buffer too small");
+        std::memcpy(buf, s.data(), s.size());
+    });
+}
+
+namespace {
+void wrap_deserialized(h2b::Deserialized d, h2c_block_tree* bt_out, h2c_matrix* out) {
+    auto bt = new h2c_block_tree_s{std::const_pointer_cast<h2b::BlockTree>(d.bt)};
+    *out = wrap_matrix(std::move(d.h));
+    *bt_out = bt;
+}
+}  // namespace
+
+int h2c_deserialize(const void* buf, int64_t bytes, h2c_block_tree* bt_out, h2c_matrix* out) {
+    return guard([&] {
+        need(buf != nullptr && bt_out != nullptr && out != nullptr && bytes >= 0, "null argument");
+        wrap_deserialized(h2b::deserialize(static_cast<const char*>(buf), size_t(bytes)), bt_out, out);
+    });
+}
+
+int h2c_write_h2_file(h2c_matrix h, const char* path) {
+    return guard([&] {
+        need(h != nullptr && path != nullptr, "null argument");
+        const std::string s = h2b::serialize(*h->h);
+        FILE* f = std::fopen(path, "wb");
+        if (!f) throw h2b::io_error(h2b::io_error::malformed, std::string("cannot open ") + path + " for writing");
+        const size_t w = std::fwrite(s.data(), 1, s.size(), f);
+        std::fclose(f);
+        if (w != s.size()) throw h2b::io_error(h2b::io_error::malformed, std::string("short write to ") + path);
+    });
+}
+
+int h2c_read_h2_file(const char* path, h2c_block_tree* bt_out, h2c_matrix* out) {
+    return guard([&] {
+        need(path != nullptr && bt_out != nullptr && out != nullptr, "null argument");
+        FILE* f = std::fopen(path, "rb");
+        if (!f) throw h2b::io_error(h2b::io_error::malformed, std::string("cannot open ") + path);
+        std::string s;
+        char tmp[1 << 16];
+        size_t r;
+        while ((r = std::fread(tmp, 1, sizeof tmp, f)) > 0) s.append(tmp, r);
+        std::fclose(f);
+        wrap_deserialized(h2b::deserialize(s.data(), s.size()), bt_out, out);
+    });
+}
+
+int h2c_last_io_error_kind(void) { return g_io_kind; }
 
 }  // extern "C"

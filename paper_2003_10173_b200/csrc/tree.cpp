@@ -154,6 +154,49 @@ std::shared_ptr<ClusterTree> build_cluster_tree(const double* coords, int64_t n,
     return t;
 }
 
+std::shared_ptr<ClusterTree> restore_cluster_tree(int64_t n, int dim, int64_t leaf_size, std::vector<int64_t> begin,
+                                                  std::vector<int64_t> end, std::vector<int> level,
+                                                  std::vector<int> parent, std::vector<int> child0,
+                                                  std::vector<int> child1, std::vector<double> lo,
+                                                  std::vector<double> hi, std::vector<int64_t> perm) {
+    const size_t nn = begin.size();
+    if (end.size() != nn || level.size() != nn || parent.size() != nn || child0.size() != nn ||
+        child1.size() != nn || lo.size() != 3 * nn || hi.size() != 3 * nn || perm.size() != size_t(n) || nn == 0)
+        throw std::invalid_argument("cluster tree restore: inconsistent arrays");
+    auto t = std::make_shared<ClusterTree>();
+    t->n = n;
+    t->dim = dim;
+    t->leaf_size = leaf_size;
+    t->begin = std::move(begin);
+    t->end = std::move(end);
+    t->level = std::move(level);
+    t->parent = std::move(parent);
+    t->child0 = std::move(child0);
+    t->child1 = std::move(child1);
+    t->lo = std::move(lo);
+    t->hi = std::move(hi);
+    t->perm = std::move(perm);
+    t->inv_perm.assign(size_t(n), -1);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t p = t->perm[size_t(i)];
+        if (p < 0 || p >= n || t->inv_perm[size_t(p)] >= 0)
+            throw std::invalid_argument("cluster tree restore: permutation is not a bijection");
+        t->inv_perm[size_t(p)] = i;
+    }
+    for (int v = 0; v < int(nn); ++v) {
+        const int c0 = t->child0[size_t(v)], c1 = t->child1[size_t(v)];
+        if ((c0 < 0) != (c1 < 0) || c0 >= int(nn) || c1 >= int(nn) || t->begin[size_t(v)] > t->end[size_t(v)])
+            throw std::invalid_argument("cluster tree restore: bad node");
+        t->depth = std::max(t->depth, t->level[size_t(v)]);
+    }
+    t->levels.assign(size_t(t->depth + 1), {});
+    for (int v = 0; v < int(nn); ++v) {
+        t->levels[size_t(t->level[size_t(v)])].push_back(v);
+        if (t->is_leaf(v)) t->leaves.push_back(v);
+    }
+    return t;
+}
+
 std::shared_ptr<BlockTree> build_block_tree(std::shared_ptr<const ClusterTree> ct, double eta, bool weak) {
     auto bt = std::make_shared<BlockTree>();
     bt->tree = ct;

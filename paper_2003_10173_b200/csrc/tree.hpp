@@ -58,4 +58,11 @@ struct BlockTree {
 
 std::shared_ptr<BlockTree> build_block_tree(std::shared_ptr<const ClusterTree> ct, double eta, bool weak);
 
+// ClusterTree::restore (cluster_tree.hpp:95-117): a tree from stored nodes and permutation
+std::shared_ptr<ClusterTree> restore_cluster_tree(int64_t n, int dim, int64_t leaf_size, std::vector<int64_t> begin,
+                                                  std::vector<int64_t> end, std::vector<int> level,
+                                                  std::vector<int> parent, std::vector<int> child0,
+                                                  std::vector<int> child1, std::vector<double> lo,
+                                                  std::vector<double> hi, std::vector<int64_t> perm);
+
 }  // namespace h2b

@@ -47,6 +47,15 @@ class ClusterTree:
         coords = np.asfortranarray(pts)
         h = H()
         check(lib.h2c_cluster_tree_create(coords.ctypes.data_as(C.c_void_p), n, d, int(leaf_size), C.byref(h)))
+        self._load(h, leaf_size)
+
+    @classmethod
+    def from_handle(cls, h, leaf_size=0):
+        obj = cls.__new__(cls)
+        obj._load(h, leaf_size)
+        return obj
+
+    def _load(self, h, leaf_size):
         self._h = h
         nn_, dim_, depth_, nodes_, leaves_ = C.c_int64(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
         check(lib.h2c_cluster_tree_info(h, C.byref(nn_), C.byref(dim_), C.byref(depth_), C.byref(nodes_),
@@ -69,7 +78,7 @@ class ClusterTree:
         self.inv_perm = np.empty_like(self.perm)
         self.inv_perm[self.perm] = np.arange(self.n)
         self.leaves = np.nonzero(self.child0 < 0)[0].astype(np.int32)
-        self.leaf_size = int(leaf_size)
+        self.leaf_size = int(leaf_size) if leaf_size else int((self.end[self.leaves] - self.begin[self.leaves]).max())
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -108,6 +117,20 @@ class BlockTree:
     def __init__(self, ct, eta=1.0, mode=Admissibility.strong):
         h = H()
         check(lib.h2c_block_tree_create(ct._h, float(eta), int(mode == Admissibility.weak), C.byref(h)))
+        self._load(h, ct, eta, mode)
+
+    @classmethod
+    def from_handle(cls, h):
+        """Wrap a block tree handle returned by the library (e.g. by read_h2_file)."""
+        ch = H()
+        check(lib.h2c_block_tree_cluster_tree(h, C.byref(ch)))
+        eta, weak = C.c_double(), C.c_int()
+        check(lib.h2c_block_tree_params(h, C.byref(eta), C.byref(weak)))
+        obj = cls.__new__(cls)
+        obj._load(h, ClusterTree.from_handle(ch), eta.value, Admissibility.weak if weak.value else Admissibility.strong)
+        return obj
+
+    def _load(self, h, ct, eta, mode):
         self._h = h
         self.tree = ct
         self.eta = float(eta)
@@ -304,3 +327,32 @@ class H2Matrix:
         n = C.c_int()
         check(lib.h2c_hgemv_launches(self._h, int(transpose), int(b), C.byref(n)))
         return n.value
+
+
+# ---- H2M1 container (serialize.hpp:110-322), byte-compatible with the reference ----
+
+def serialize(m):
+    """Bytes of the H2M1 container (serialize.hpp:110-182)."""
+    n = C.c_int64()
+    check(lib.h2c_serialize_size(m._h, C.byref(n)))
+    buf = (C.c_char * n.value)()
+    check(lib.h2c_serialize(m._h, buf, n.value))
+    return bytes(buf)
+
+
+def deserialize(data):
+    """H2Matrix from H2M1 bytes (serialize.hpp:184-308); the block tree is rebuilt."""
+    data = bytes(data)
+    bt, h = H(), H()
+    check(lib.h2c_deserialize(data, len(data), C.byref(bt), C.byref(h)))
+    return H2Matrix(h, BlockTree.from_handle(bt))
+
+
+def write_h2_file(m, path):
+    check(lib.h2c_write_h2_file(m._h, str(path).encode()))
+
+
+def read_h2_file(path):
+    bt, h = H(), H()
+    check(lib.h2c_read_h2_file(str(path).encode(), C.byref(bt), C.byref(h)))
+    return H2Matrix(h, BlockTree.from_handle(bt))
