@@ -275,6 +275,29 @@ int h2c_read_h2_file(const char* path, h2c_block_tree* bt_out, h2c_matrix* out);
 /* kind of the last H2C_IO_ERROR on this thread: 0 bad_magic, 1 version_mismatch, 2 truncated, 3 malformed */
 int h2c_last_io_error_kind(void);
 
+/* ---- Device black-box operator of cfg3: the 1D diffusion
+ *      density-inversion Hessian at the target density, diffusion1d.hpp:62-354 */
+typedef struct h2c_diff1d_s* h2c_diff1d;
+typedef struct {
+    int64_t n;                       /* parameter nodes on [-1, 1] */
+    int64_t steps;
+    double final_time, t_p, t_0, source_amplitude, alpha, beta, pad;
+    int num_sources;                 /* source_positions NULL: the reference's {-0.5, 0, 0.5} */
+    const double* source_positions;
+    int64_t num_receivers;
+} h2c_diff1d_config;                 /* Diffusion1DConfig (diffusion1d.hpp:62-73) */
+void h2c_diff1d_config_default(h2c_diff1d_config* cfg);
+/* Diffusion1D(cfg): stepper + cached state marches on `stream` (diffusion1d.hpp:77-112) */
+int h2c_diff1d_create(const h2c_diff1d_config* cfg, void* stream, h2c_diff1d* out);
+void h2c_diff1d_destroy(h2c_diff1d d);
+int h2c_diff1d_info(h2c_diff1d d, int64_t* nstate, int64_t* npad, double* spacing, double* dt, int64_t* pde_solves);
+/* hessvec_at_target (:173-175): y = H x, x and y n x b column-major DEVICE buffers (ld n) */
+int h2c_diff1d_hessvec(h2c_diff1d d, int include_tv, int64_t b, const double* x, double* y, void* stream);
+/* cached state field of one source at the physical nodes, n x (steps+1) column-major, to host */
+int h2c_diff1d_state_field(h2c_diff1d d, int source, double* out);
+/* hessian_operator(include_tv) (:177-181); the operator keeps the problem alive */
+int h2c_diff1d_operator(h2c_diff1d d, int include_tv, h2c_operator* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,7 @@
 #include <string>
 #include <thread>
 
+#include "diffusion1d.hpp"
 #include "test_support.hpp"
 
 using namespace h2;
@@ -377,4 +378,48 @@ int ora_gaussian(uint64_t seed, int64_t r, int64_t c, double* outp) {
     });
 }
 
+// ---- diffusion1d Hessian at the target (oracle/diffusion1d.hpp) ----
+struct ora_diff1d {
+    h2ora::Diff1DOracle d;
+};
+int ora_diff1d_create(int64_t n, int64_t steps, double final_time, double t_p, double t_0, double amp,
+                      double alpha, double beta, double pad, int nsrc, const double* src_pos, int64_t nrcv,
+                      ora_diff1d** o) {
+    return guard([&] {
+        h2ora::Diff1DConfig c;
+        c.n = n;
+        c.steps = steps;
+        c.final_time = final_time;
+        c.t_p = t_p;
+        c.t_0 = t_0;
+        c.source_amplitude = amp;
+        c.alpha = alpha;
+        c.beta = beta;
+        c.pad = pad;
+        if (nsrc >= 0) c.source_positions.assign(src_pos, src_pos + nsrc);
+        c.num_receivers = nrcv;
+        *o = new ora_diff1d{h2ora::Diff1DOracle(c)};
+    });
+}
+void ora_diff1d_destroy(ora_diff1d* d) { delete d; }
+int ora_diff1d_info(ora_diff1d* d, int64_t* nstate, int64_t* npad, double* h, double* dt, int64_t* marches) {
+    return guard([&] {
+        *nstate = d->d.nstate();
+        *npad = d->d.npad();
+        *h = d->d.spacing();
+        *dt = d->d.dt();
+        *marches = d->d.pde_solves();
+    });
+}
+int ora_diff1d_hessvec(ora_diff1d* d, int64_t b, const double* x, double* y, int include_tv, int nthreads) {
+    return guard([&] { d->d.hessvec(b, x, y, include_tv != 0, nthreads); });
+}
+int ora_diff1d_state(ora_diff1d* d, int source, double* u) {
+    return guard([&] {
+        const auto& v = d->d.state(size_t(source));
+        std::memcpy(u, v.data(), sizeof(double) * v.size());
+    });
+}
+
 }  // extern "C"
+

@@ -58,6 +58,12 @@ _sig("ora_peel_dense", vp, vp, i32, f64, i64, i64, i64, u64, f64, P(vp), P(i64),
 _sig("ora_peel_h2", vp, vp, f64, u64, f64, P(vp), P(i64))
 _sig("ora_pnorm2_dense", vp, i64, i32, P(f64), P(i32))
 _sig("ora_gaussian", u64, i64, i64, vp)
+_sig("ora_diff1d_create", i64, i64, f64, f64, f64, f64, f64, f64, f64, i32, vp, i64, P(vp))
+_lib.ora_diff1d_destroy.argtypes = [vp]
+_lib.ora_diff1d_destroy.restype = None
+_sig("ora_diff1d_info", vp, P(i64), P(i64), P(f64), P(f64), P(i64))
+_sig("ora_diff1d_hessvec", vp, i64, vp, vp, i32, i32)
+_sig("ora_diff1d_state", vp, i32, vp)
 
 
 class OracleError(RuntimeError):
@@ -278,3 +284,57 @@ def grid3d(nx, ny, nz, a=0.0, b=1.0):
     k = np.repeat(np.arange(nz), nx * ny)
     s = lambda q, m: a + (b - a) * q / max(m - 1, 1)
     return np.stack([s(i, nx), s(j, ny), s(k, nz)], axis=1)
+
+
+DIFF1D_DEFAULTS = dict(n=512, steps=512, T=30.0, tp=1.0, t0=0.0, amp=1000.0, alpha=3e-5, beta=1e-3, pad=0.5,
+                       sources=(-0.5, 0.0, 0.5), receivers=8)
+
+
+class Diff1D:
+    """1D diffusion Hessian at the target density (oracle/diffusion1d.hpp,
+    restating proj/include/h2/oracles/diffusion1d.hpp). Keys follow the
+    reference registry overrides (registry.hpp:104-116)."""
+
+    def __init__(self, **cfg):
+        c = dict(DIFF1D_DEFAULTS)
+        unknown = set(cfg) - set(c)
+        if unknown:
+            raise ValueError(f"unknown diffusion keys {sorted(unknown)}")
+        c.update(cfg)
+        self.cfg = c
+        src = np.ascontiguousarray(c["sources"], np.float64)
+        h = vp()
+        _check(_lib.ora_diff1d_create(int(c["n"]), int(c["steps"]), float(c["T"]), float(c["tp"]), float(c["t0"]),
+                                      float(c["amp"]), float(c["alpha"]), float(c["beta"]), float(c["pad"]),
+                                      len(src), _p(src), int(c["receivers"]), C.byref(h)))
+        self._h = h
+        self.n = int(c["n"])
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.ora_diff1d_destroy(self._h)
+            self._h = None
+
+    def info(self):
+        ns, npad, h, dt, m = i64(), i64(), f64(), f64(), i64()
+        _check(_lib.ora_diff1d_info(self._h, C.byref(ns), C.byref(npad), C.byref(h), C.byref(dt), C.byref(m)))
+        return dict(nstate=ns.value, npad=npad.value, h=h.value, dt=dt.value, marches=m.value)
+
+    def hessvec(self, x, include_tv=True, threads=1):
+        x = np.asarray(x, np.float64)
+        vec = x.ndim == 1
+        xf = np.asfortranarray(x[:, None] if vec else x)
+        y = np.empty_like(xf, order="F")
+        _check(_lib.ora_diff1d_hessvec(self._h, xf.shape[1], _p(xf), _p(y), int(include_tv), int(threads)))
+        return y[:, 0] if vec else y
+
+    def state(self, source):
+        inf = self.info()
+        u = np.empty((inf["nstate"], int(self.cfg["steps"]) + 1), order="F")
+        _check(_lib.ora_diff1d_state(self._h, int(source), _p(u)))
+        return u
+
+    def points(self):
+        """Grid1D(-1, 1, n).points() (grid.hpp:10-24)."""
+        h = 2.0 / (self.n - 1)
+        return (-1.0 + h * np.arange(self.n))[:, None]

@@ -195,3 +195,20 @@ _sig("h2c_deserialize", i32, vp, i64, P(H), P(H))
 _sig("h2c_write_h2_file", i32, H, C.c_char_p)
 _sig("h2c_read_h2_file", i32, C.c_char_p, P(H), P(H))
 _sig("h2c_last_io_error_kind", i32)
+
+
+class Diff1DConfigC(C.Structure):
+    """h2c_diff1d_config (Diffusion1DConfig, diffusion1d.hpp:62-73)."""
+    _fields_ = [("n", C.c_int64), ("steps", C.c_int64), ("final_time", C.c_double), ("t_p", C.c_double),
+                ("t_0", C.c_double), ("source_amplitude", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
+                ("pad", C.c_double), ("num_sources", C.c_int), ("source_positions", C.POINTER(C.c_double)),
+                ("num_receivers", C.c_int64)]
+
+
+_sig("h2c_diff1d_config_default", None, P(Diff1DConfigC))
+_sig("h2c_diff1d_create", i32, P(Diff1DConfigC), vp, P(H))
+_sig("h2c_diff1d_destroy", None, H)
+_sig("h2c_diff1d_info", i32, H, P(i64), P(i64), P(f64), P(f64), P(i64))
+_sig("h2c_diff1d_hessvec", i32, H, i32, i64, vp, vp, vp)
+_sig("h2c_diff1d_state_field", i32, H, i32, vp)
+_sig("h2c_diff1d_operator", i32, H, i32, P(H))

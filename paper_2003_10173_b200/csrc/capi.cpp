@@ -12,6 +12,7 @@
 #include "h2dev.hpp"
 #include "hara.hpp"
 #include "inversion.hpp"
+#include "diffusion1d.hpp"
 #include "serialize.hpp"
 #include "matrix.hpp"
 
@@ -871,5 +872,87 @@ int h2c_read_h2_file(const char* path, h2c_block_tree* bt_out, h2c_matrix* out) 
 }
 
 int h2c_last_io_error_kind(void) { return g_io_kind; }
+
+// ---- diffusion1d device operator ----
+struct h2c_diff1d_s {
+    std::shared_ptr<h2b::Diffusion1DDev> d;
+};
+
+void h2c_diff1d_config_default(h2c_diff1d_config* cfg) {
+    if (!cfg) return;
+    const h2b::Diff1DConfig d;
+    cfg->n = d.n;
+    cfg->steps = d.steps;
+    cfg->final_time = d.final_time;
+    cfg->t_p = d.t_p;
+    cfg->t_0 = d.t_0;
+    cfg->source_amplitude = d.source_amplitude;
+    cfg->alpha = d.alpha;
+    cfg->beta = d.beta;
+    cfg->pad = d.pad;
+    cfg->num_sources = int(d.source_positions.size());
+    cfg->source_positions = nullptr;
+    cfg->num_receivers = d.num_receivers;
+}
+
+int h2c_diff1d_create(const h2c_diff1d_config* cfg, void* stream, h2c_diff1d* out) {
+    return guard([&] {
+        need(cfg != nullptr && out != nullptr, "null argument");
+        h2b::Diff1DConfig c;
+        c.n = cfg->n;
+        c.steps = cfg->steps;
+        c.final_time = cfg->final_time;
+        c.t_p = cfg->t_p;
+        c.t_0 = cfg->t_0;
+        c.source_amplitude = cfg->source_amplitude;
+        c.alpha = cfg->alpha;
+        c.beta = cfg->beta;
+        c.pad = cfg->pad;
+        if (cfg->source_positions) {
+            need(cfg->num_sources > 0, "diffusion1d: num_sources < 1");
+            c.source_positions.assign(cfg->source_positions, cfg->source_positions + cfg->num_sources);
+        }
+        c.num_receivers = cfg->num_receivers;
+        auto s = static_cast<cudaStream_t>(stream);
+        auto d = std::make_shared<h2b::Diffusion1DDev>(c, s);
+        H2B_CUDA(cudaStreamSynchronize(s));
+        *out = new h2c_diff1d_s{std::move(d)};
+    });
+}
+
+void h2c_diff1d_destroy(h2c_diff1d d) { delete d; }
+
+int h2c_diff1d_info(h2c_diff1d d, int64_t* nstate, int64_t* npad, double* spacing, double* dt, int64_t* pde_solves) {
+    return guard([&] {
+        need(d != nullptr, "null argument");
+        if (nstate) *nstate = d->d->nstate();
+        if (npad) *npad = d->d->npad();
+        if (spacing) *spacing = d->d->spacing();
+        if (dt) *dt = d->d->dt();
+        if (pde_solves) *pde_solves = d->d->pde_solves();
+    });
+}
+
+int h2c_diff1d_hessvec(h2c_diff1d d, int include_tv, int64_t b, const double* x, double* y, void* stream) {
+    return guard([&] {
+        need(d != nullptr && x != nullptr && y != nullptr, "null argument");
+        d->d->hessvec(include_tv != 0, b, x, y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_diff1d_state_field(h2c_diff1d d, int source, double* out) {
+    return guard([&] {
+        need(d != nullptr && out != nullptr, "null argument");
+        auto v = d->d->state_field(source, nullptr);
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+int h2c_diff1d_operator(h2c_diff1d d, int include_tv, h2c_operator* out) {
+    return guard([&] {
+        need(d != nullptr && out != nullptr, "null argument");
+        *out = new h2c_operator_s{h2b::diffusion_hessian_operator(d->d, include_tv != 0)};
+    });
+}
 
 }  // extern "C"

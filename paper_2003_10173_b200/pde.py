@@ -1,0 +1,133 @@
+"""Device PDE black-box operators (the reference's h2::oracles, SURVEY §8(f)
+row 2): the 1D diffusion density-inversion Hessian of BASELINE cfg3, computed
+on the B200 so HARA's operator applies never leave HBM.
+
+Mirrors proj/include/h2/oracles/diffusion1d.hpp (Diffusion1D, :62-354) and
+the "diff1d-<n>" entry of make_oracle (registry.hpp:104-124). Only the
+evaluation-point Hessian (hessvec_at_target / hessian_operator) is built; the
+misfit, gradient and general-density Hessian are not on the HARA path.
+"""
+import ctypes as C
+
+import numpy as np
+
+from ._lib import Diff1DConfigC, H, check, lib
+from .construction import LinearOperator
+
+
+class Diffusion1D:
+    """Diffusion1D(cfg) (diffusion1d.hpp:75-112). Keyword names follow
+    Diffusion1DConfig (:62-73)."""
+
+    def __init__(self, n=512, steps=512, final_time=30.0, t_p=1.0, t_0=0.0, source_amplitude=1000.0, alpha=3e-5,
+                 beta=1e-3, pad=0.5, source_positions=None, num_receivers=8):
+        c = Diff1DConfigC()
+        lib.h2c_diff1d_config_default(C.byref(c))
+        c.n, c.steps, c.final_time, c.t_p, c.t_0 = int(n), int(steps), float(final_time), float(t_p), float(t_0)
+        c.source_amplitude, c.alpha, c.beta, c.pad = float(source_amplitude), float(alpha), float(beta), float(pad)
+        c.num_receivers = int(num_receivers)
+        self._src = None
+        if source_positions is not None:
+            self._src = np.ascontiguousarray(source_positions, np.float64)
+            c.num_sources = len(self._src)
+            c.source_positions = self._src.ctypes.data_as(C.POINTER(C.c_double))
+        h = H()
+        check(lib.h2c_diff1d_create(C.byref(c), None, C.byref(h)))
+        self._h = h
+        self._n = int(n)
+        self.steps = int(steps)
+        self.config = dict(n=n, steps=steps, final_time=final_time, t_p=t_p, t_0=t_0,
+                           source_amplitude=source_amplitude, alpha=alpha, beta=beta, pad=pad,
+                           source_positions=source_positions, num_receivers=num_receivers)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.h2c_diff1d_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        ns, npad, h, dt, m = C.c_int64(), C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
+        check(lib.h2c_diff1d_info(self._h, C.byref(ns), C.byref(npad), C.byref(h), C.byref(dt), C.byref(m)))
+        return ns.value, npad.value, h.value, dt.value, m.value
+
+    def n(self):
+        return self._n
+
+    def nstate(self):
+        return self._info()[0]
+
+    def spacing(self):
+        return self._info()[2]
+
+    def dt(self):
+        return self._info()[3]
+
+    def pde_solves(self):   # :121
+        return self._info()[4]
+
+    def points(self):
+        """Grid1D(-1, 1, n).points() (grid.hpp:10-24, diffusion1d.hpp:123)."""
+        return (-1.0 + (2.0 / (self._n - 1)) * np.arange(self._n))[:, None]
+
+    def hessvec_device(self, x, y, b, include_tv=True, stream=None):
+        """y = H x on device pointers (n x b column-major, ld n)."""
+        check(lib.h2c_diff1d_hessvec(self._h, int(include_tv), int(b), x, y, stream))
+
+    def hessvec_at_target(self, nu, include_tv=True):
+        """hessvec_at_target (:173-175) on host arrays (n x b)."""
+        import torch
+        nu = np.asarray(nu, np.float64)
+        vec = nu.ndim == 1
+        xm = nu[:, None] if vec else nu
+        if xm.shape[0] != self._n:
+            raise ValueError("hessvec: dimension mismatch")
+        xd = torch.from_numpy(np.ascontiguousarray(xm.T)).cuda()
+        yd = torch.empty_like(xd)
+        self.hessvec_device(xd.data_ptr(), yd.data_ptr(), xm.shape[1], include_tv)
+        torch.cuda.synchronize()
+        y = yd.cpu().numpy().T
+        return y[:, 0] if vec else np.asfortranarray(y)
+
+    def hessian_operator(self, include_tv=True):
+        """hessian_operator(include_tv) (:177-181): symmetric black box on the device."""
+        h = H()
+        check(lib.h2c_diff1d_operator(self._h, int(include_tv), C.byref(h)))
+        return LinearOperator(h, self._n, True, keep=self)
+
+    def state_field(self, source):
+        """Cached target state of one source at the physical nodes, n x (steps+1)."""
+        out = np.empty((self._n, self.steps + 1), order="F")
+        check(lib.h2c_diff1d_state_field(self._h, int(source), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+class Oracle:
+    """Oracle record of make_oracle (registry.hpp:58-81): op, points, leaf, mode, eta."""
+
+    def __init__(self, name, op, points, leaf, mode, eta, diffusion):
+        self.name, self.op, self.points, self.leaf, self.mode, self.eta = name, op, points, leaf, mode, eta
+        self.diffusion = diffusion
+
+    def default_block_tree(self, leaf=None, eta=None):
+        from .h2 import build_block_tree, build_cluster_tree
+        ct = build_cluster_tree(self.points, self.leaf if leaf is None else leaf)
+        return build_block_tree(ct, ct, self.eta if eta is None else eta, self.mode)
+
+
+def make_oracle(name, config=None):
+    """make_oracle for "diff1d-<n>" (registry.hpp:104-124), with the same
+    override keys (steps, T, tp, t0, alpha, amp, beta, pad, tv, leaf, eta).
+    The surface / advdiff operators are not ported to the device."""
+    from .h2 import Admissibility
+    cfg = dict(config or {})
+    if not name.startswith("diff1d-"):
+        if name.startswith(("surface", "advdiff-")):
+            raise NotImplementedError(f"make_oracle: {name} has no device port")
+        raise ValueError(f"unknown oracle {name}")
+    num = lambda k, d: float(cfg.get(k, d))
+    d = Diffusion1D(n=int(name[7:]), steps=int(cfg.get("steps", 512)), final_time=num("T", 30.0),
+                    t_p=num("tp", 1.0), t_0=num("t0", 0.0), alpha=num("alpha", 3e-5),
+                    source_amplitude=num("amp", 1000.0), beta=num("beta", 1e-3), pad=num("pad", 0.5))
+    tv = int(cfg.get("tv", 1)) != 0
+    return Oracle(name, d.hessian_operator(tv), d.points(), int(cfg.get("leaf", 32)), Admissibility.weak,
+                  num("eta", 1.0), d)
