@@ -35,15 +35,22 @@ CONFIGS = {
     # BASELINE.json configs[0] structure (hgemv part)
     "cfg1": dict(workload="2D exponential-kernel H2 hgemv N=16384 (128^2), leaf 64, rank 32, 1 vector",
                  grid=(128, 128), kind="exponential", ell=0.2, rank=32, b=1, leaf=64),
-    # BASELINE.json configs[2]: HARA from a black-box matvec of a diffusion-Hessian proxy. The heat
-    # propagator F = exp(T*Laplacian) is a Gaussian convolution, so the misfit Hessian F^T F of a
-    # fully observed 1D diffusion inverse problem is a Gaussian kernel; the black box applies it as
-    # a rank-32 H^2 (hgemv) on the weak 1D tree of the reference's diff1d case (leaf 32).
-    "cfg3": dict(workload="HARA peel_construct from a black-box matvec, 1D diffusion-Hessian proxy "
-                          "(Gaussian heat-kernel F^T F, ell=0.05, applied as a rank-32 H^2), N=2^18, "
+    # BASELINE.json configs[2]: HARA from a black-box matvec of a diffusion Hessian: the reference's own
+    # "diff1d-262144" oracle (registry.hpp:104-124; misfit + TV Hessian at the target density, two
+    # Crank-Nicolson marches per source per application) with steps=64 as SURVEY §9.3 recommends,
+    # applied on the device (paper_2003_10173_b200/csrc/diffusion1d.cu)
+    "cfg3": dict(workload="HARA peel_construct from the black-box diffusion Hessian diff1d-262144 (registry.hpp:104-124, "
+                          "steps=64, misfit+TV, 3 sources, 8 receivers; operator marched on the B200), N=2^18, "
                           "weak admissibility, leaf 32, eps 1e-6, PeelConfig defaults (b=16, p=10)",
-                 grid=(262144,), kind="gaussian", ell=0.05, rank=32, leaf=32, eps=1e-6, hara=True,
-                 sample_n=16384),
+                 grid=(262144,), pde=True, steps=64, leaf=32, eps=1e-6, hara=True, sample_n=16384),
+    # the earlier analytic proxy: the heat propagator F = exp(T*Laplacian) is a Gaussian convolution, so
+    # the misfit Hessian F^T F of a fully observed 1D diffusion inverse problem is a Gaussian kernel,
+    # applied as a rank-32 H^2 (hgemv) on the same weak 1D tree
+    "cfg3k": dict(workload="HARA peel_construct from a black-box matvec, 1D diffusion-Hessian proxy "
+                           "(Gaussian heat-kernel F^T F, ell=0.05, applied as a rank-32 H^2), N=2^18, "
+                           "weak admissibility, leaf 32, eps 1e-6, PeelConfig defaults (b=16, p=10)",
+                  grid=(262144,), kind="gaussian", ell=0.05, rank=32, leaf=32, eps=1e-6, hara=True,
+                  sample_n=16384),
     # BASELINE.json configs[4]: recompression + low-rank update, then hierarchical Newton-Schulz on a
     # regularised Hessian proxy: the cfg3 diffusion proxy (Gaussian heat kernel F^T F) at N=2^16 plus a
     # Tikhonov shift alpha I, updated by a rank-8 symmetric term (a quasi-Newton-style correction)
@@ -488,14 +495,23 @@ def hara_problem(cfg, n):
     return pts, ct, bt, src
 
 
+def hara_operator(cfg, n):
+    """(black-box operator, block tree, keep-alive) of a HARA config."""
+    from paper_2003_10173_b200 import H2Operator, make_oracle
+    if cfg.get("pde"):
+        o = make_oracle(f"diff1d-{n}", {"steps": str(cfg["steps"]), "leaf": str(cfg["leaf"])})
+        return o.op, o.default_block_tree(), o
+    pts, ct, bt, src = hara_problem(cfg, n)
+    return H2Operator(src), bt, src
+
+
 def run_hara(args, cfg, world, rank, local, dist):
     """cfg3: HARA build time on the B200 (one step = one peel_construct)."""
     import torch
-    from paper_2003_10173_b200 import H2Operator, PeelConfig, estimate_relative_error, peel_construct
+    from paper_2003_10173_b200 import PeelConfig, estimate_relative_error, peel_construct
     torch.cuda.set_device(local)
     n = cfg["grid"][0]
-    pts, ct, bt, src = hara_problem(cfg, n)
-    op = H2Operator(src)
+    op, bt, keep = hara_operator(cfg, n)
     rngs = {"device": 1, "reference": 0}
     pc = PeelConfig(eps=cfg["eps"], rng=rngs[args.hara_rng])
     for _ in range(max(1, min(args.warmup, 1))):
@@ -534,15 +550,19 @@ def run_hara(args, cfg, world, rank, local, dist):
     phases["all_steps_s"] = [round(v, 4) for v in times]
     err = estimate_relative_error(op, res.matrix)
     prof = [int(v) for v in res.matrix.rank_profile()]
+    data = ("synthetic: the reference's diff1d oracle (target density, Ricker sources) marched on the device"
+            if cfg.get("pde") else "synthetic (device-generated kernel H^2 black box)")
     out = {"metric": "HARA build time (N=2^18, tol 1e-6)", "value": t, "unit": "s", "n_gpus": world,
            "steps": steps, "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated kernel H^2 black box)",
+           "vs_baseline": None, "dtype": "f64", "data": data,
            "config": {"workload": cfg["workload"], "n": n, "eps": cfg["eps"], "rng": args.hara_rng,
                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
            "hara": {"op_s": statistics.median(opms) / 1e3, "construction_s": t - statistics.median(opms) / 1e3,
                     "samples": res.stats.total, "relative_error_2norm": err, "rank_profile": prof,
                     "level_samples": [lv.samples for lv in res.stats.levels], "phases_s": phases},
            "clocks": clk.summary()}
+    if cfg.get("pde"):
+        out["hara"]["pde_solves"] = keep.diffusion.pde_solves()
     return out
 
 
@@ -604,31 +624,65 @@ def run_inversion(args, cfg, world, rank, local, dist):
             "clocks": clk.summary()}
 
 
-def cpu_baseline_hara(args, cfg):
-    """The oracle (restated reference, 1 thread) on a bounded sample: the same
-    problem at N = sample_n, next to the B200 on the same sample."""
-    import torch
+def cpu_hara_build(cfg, n, threads):
+    """One peel_construct on the CPU restatement (oracle) of the same problem:
+    (seconds, samples, operator seconds)."""
     from oracle import pyoracle as O
-    from paper_2003_10173_b200 import H2Operator, PeelConfig, peel_construct
-    n = cfg["sample_n"]
+    if cfg.get("pde"):
+        d = O.Diff1D(n=n, steps=cfg["steps"])
+        ref = O.Tree(d.points(), cfg["leaf"], 1.0, True)
+        t0 = time.perf_counter()
+        _, tot, ops = d.peel(ref, eps=cfg["eps"], threads=threads)
+        return time.perf_counter() - t0, tot, ops
     pts, ct, bt, src = hara_problem(cfg, n)
     ref = O.Tree(pts, cfg["leaf"], 1.0, True)
     rr, _ = src.ranks()
     osrc = O.H2.from_packed(ref, True, rr, None, src.download())
     t0 = time.perf_counter()
-    ora, tot = O.peel_h2(ref, osrc, eps=cfg["eps"])
-    tc = time.perf_counter() - t0
-    op = H2Operator(src)
+    _, tot = O.peel_h2(ref, osrc, eps=cfg["eps"])
+    return time.perf_counter() - t0, tot, None
+
+
+def cpu_baseline_hara(args, cfg):
+    """The oracle (restated reference) on a bounded sample: the same problem
+    at N = sample_n, next to the B200 on the same sample."""
+    import torch
+    from paper_2003_10173_b200 import PeelConfig, peel_construct
+    n = cfg["sample_n"]
+    threads = os.cpu_count() if cfg.get("pde") else 1
+    tc, tot, ops = cpu_hara_build(cfg, n, threads)
+    op, bt, keep = hara_operator(cfg, n)
     peel_construct(op, bt, PeelConfig(eps=cfg["eps"], rng=0))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = peel_construct(op, bt, PeelConfig(eps=cfg["eps"], rng=0))
     torch.cuda.synchronize()
     tg = time.perf_counter() - t0
-    return {"value": tc, "unit": "s", "cores": 1, "kind": "port",
-            "sample": f"same problem at N={n} (oracle restatement, 1 thread): {tc:.2f} s, {tot} samples; "
+    opnote = f" (operator applies {ops:.2f} s on {threads} threads)" if ops is not None else ""
+    return {"value": tc, "unit": "s", "cores": threads, "kind": "port",
+            "sample": f"same problem at N={n} (oracle restatement): {tc:.2f} s{opnote}, {tot} samples; "
                       f"B200 on the same sample with the reference RNG stream: {tg:.3f} s, {res.stats.total} samples",
             "b200_same_sample_s": tg, "speedup_same_sample": tc / tg}
+
+
+def reference_hara(args, cfg, world):
+    """--impl reference for HARA configs. cfg3 (diffusion Hessian): the full
+    N=2^18 build on the CPU restatement with every host thread applying the
+    operator (the reference's construction is single-threaded); one step.
+    cfg3k: the bounded N=sample_n sample."""
+    if cfg.get("pde"):
+        n = cfg["grid"][0]
+        threads = os.cpu_count()
+        t, tot, ops = cpu_hara_build(cfg, n, threads)
+        cb = {"value": t, "unit": "s", "cores": threads, "kind": "port",
+              "sample": f"the full N={n} build, 1 step: {tot} samples, operator applies {ops:.1f} s on {threads} "
+                        f"threads, construction {t - ops:.1f} s on 1 thread (oracle restatement; Eigen absent)"}
+    else:
+        cb = cpu_baseline_hara(args, cfg)
+    return {"impl": "reference", "metric": "HARA build time (N=2^18, tol 1e-6)", "value": cb["value"], "unit": "s",
+            "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": False,
+            "config": {"workload": cfg["workload"]}, "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main():
@@ -668,14 +722,7 @@ def main():
     if cfg.get("hara"):
         if args.impl == "reference":
             if rank == 0:
-                from oracle import pyoracle as O  # noqa: F401
-                import torch  # noqa: F401
-                cb = cpu_baseline_hara(args, cfg)
-                print(json.dumps({"impl": "reference", "metric": "HARA build time (N=2^18, tol 1e-6)",
-                                  "value": cb["value"], "unit": "s", "n_gpus": world, "steps": 1, "warmup": 0,
-                                  "higher_is_better": False, "config": {"workload": cfg["workload"]},
-                                  "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "s",
-                                                              "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+                print(json.dumps(reference_hara(args, cfg, world)), flush=True)
             return
         out = run_hara(args, cfg, world, rank, local, dist)
         if rank == 0 and not args.no_cpu_baseline:

@@ -421,5 +421,30 @@ int ora_diff1d_state(ora_diff1d* d, int source, double* u) {
     });
 }
 
+// peel_construct over the diffusion Hessian at the target (registry "diff1d-<n>"
+// with hessian_operator(include_tv), diffusion1d.hpp:177-181); the operator
+// applies run on `nthreads` host threads (columns are independent)
+int ora_peel_diff1d(ora_tree* t, ora_diff1d* d, int include_tv, double eps, uint64_t seed, int nthreads, ora_h2** o,
+                    int64_t* total_samples, double* op_seconds) {
+    return guard([&] {
+        const Index n = d->d.n();
+        double op_s = 0;
+        auto op = make_operator(n, true, [&](const Matrix& x) {
+            Matrix y(n, x.cols());
+            const auto t0 = std::chrono::steady_clock::now();
+            d->d.hessvec(x.cols(), x.data(), y.data(), include_tv != 0, nthreads);
+            op_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return y;
+        });
+        PeelConfig cfg;
+        cfg.eps = eps;
+        cfg.seed = seed;
+        PeelResult r = peel_construct(*op, t->bt, cfg);
+        *total_samples = r.stats.total;
+        *op_seconds = op_s;
+        *o = new ora_h2{std::move(r.matrix)};
+    });
+}
+
 }  // extern "C"
 

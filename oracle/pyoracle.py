@@ -64,6 +64,7 @@ _lib.ora_diff1d_destroy.restype = None
 _sig("ora_diff1d_info", vp, P(i64), P(i64), P(f64), P(f64), P(i64))
 _sig("ora_diff1d_hessvec", vp, i64, vp, vp, i32, i32)
 _sig("ora_diff1d_state", vp, i32, vp)
+_sig("ora_peel_diff1d", vp, vp, i32, f64, u64, i32, P(vp), P(i64), P(f64))
 
 
 class OracleError(RuntimeError):
@@ -333,6 +334,14 @@ class Diff1D:
         u = np.empty((inf["nstate"], int(self.cfg["steps"]) + 1), order="F")
         _check(_lib.ora_diff1d_state(self._h, int(source), _p(u)))
         return u
+
+    def peel(self, tree, eps=1e-6, seed=42, include_tv=True, threads=1):
+        """peel_construct(hessian_operator(include_tv), bt, {eps, seed}) on the CPU:
+        returns (H2, total samples, seconds spent in operator applies)."""
+        h, tot, ops = vp(), i64(), f64()
+        _check(_lib.ora_peel_diff1d(tree._h, self._h, int(include_tv), float(eps), int(seed), int(threads),
+                                    C.byref(h), C.byref(tot), C.byref(ops)))
+        return H2(h, tree), tot.value, ops.value
 
     def points(self):
         """Grid1D(-1, 1, n).points() (grid.hpp:10-24)."""
