@@ -1,7 +1,7 @@
 // Device 1D diffusion Hessian at the target density (diffusion1d.hpp here;
 // reference proj/include/h2/oracles/diffusion1d.hpp). See the header for the
 // chunked-recurrence solve; layout in HBM:
-//   coef_   [padded state row][8]   mdiag, cu, cl (A- stencil), mult, rdfac, beta (LU), wg, hb (carry weights)
+//   coef_   [padded state row][6]   mdiag (A- diagonal), mult (L), wg, hb (carry weights), rdfac, beta (U)
 //   chunk_  [chunk][3]              G (forward carry gain), WG, HB (backward carry weights at the chunk start)
 //   u_      [step][k][source]       cached state at the physical nodes
 //   W       [padded state row][col] chunk-local solutions, columns = source-major (s * bb + j)
@@ -17,9 +17,10 @@ namespace h2b {
 namespace {
 
 constexpr int kL = 32;            // state rows per chunk (per thread)
-constexpr int kCoef = 8;
-constexpr int kMaxBatch = 64;     // operator columns per internal batch
-enum { kMdiag = 0, kCu, kCl, kMult, kRdfac, kBeta, kWg, kHb };
+constexpr int kCoef = 6;          // per row, as three double2: (mdiag, mult) (wg, hb) (rdfac, beta)
+int g_max_batch = 64;             // operator columns per internal batch (h2b_diff1d_tune)
+int g_cpb_max = 16;               // chunks per step CTA cap (h2b_diff1d_tune)
+enum { kMdiag = 0, kMult, kWg, kHb, kRdfac, kBeta };
 
 struct StepArgs {
     const double* __restrict__ coef;
@@ -38,11 +39,12 @@ struct StepArgs {
     double fval;          // mode 0: source value of the step; mode 2: quadrature weight
     const double* vr;     // mode 2: receiver traces of this step, [R][B]
     const double* nu;     // mode 1: perturbation, [n][bb]
-    const double* U0;     // u_j   at physical nodes, [n][S]
-    const double* U1;     // u_j+1 at physical nodes, [n][S]
+    const double* du;     // u_{j+1} - u_j at physical nodes, [n][S]
     double c;             // h / dt
     double* Uout;         // mode 0: x_j at physical nodes, [n][S]
-    double* acc;          // mode 2: [n][B] += x_j (U1 - U0)
+    double* acc;          // mode 2: [n][B] += x_j (u_{j+1} - u_j)
+    int64_t ns;           // state rows (the A- off-diagonals stop at the far Dirichlet ends)
+    double moff;          // A- off-diagonal
 };
 
 __device__ __forceinline__ double carry_x(const double* __restrict__ coef, const double* W, const double* Yin,
@@ -52,101 +54,162 @@ __device__ __forceinline__ double carry_x(const double* __restrict__ coef, const
     return fma(cf[kHb], Xin[col * P + c], fma(cf[kWg], Yin[col * P + c], W[row * B + col]));
 }
 
-// one Crank-Nicolson step for every (chunk, column): finish x_j from its carry
-// form, consume it (state store / adjoint accumulation), form the right-hand
-// side A- x_j + f_j (Stepper::apply_minus, diffusion1d.hpp:203-209, and the
-// forcing of :245-246, :302-303, :325-326), and solve the chunk locally with
-// zero boundary carries (TridiagSolver::solve_in_place, grid.hpp:67-73)
-__global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a) {
-    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (t >= a.P * a.B) return;
-    const int64_t ch = t / a.B;
-    const int col = int(t - ch * a.B);
-    const int src = col / a.bb;
-    const int64_t s0 = ch * kL;
-    const double* __restrict__ coef = a.coef;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+// TMA 1D bulk copies (contiguous, 16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
 
-    double x[kL + 2];
-    if (a.Wp) {
-        const double yc = a.Yin[col * a.P + ch], xc = a.Xin[col * a.P + ch];
-#pragma unroll
-        for (int i = 0; i < kL; ++i) {
-            const double* cf = coef + (s0 + i) * kCoef;
-            x[i + 1] = fma(cf[kHb], xc, fma(cf[kWg], yc, a.Wp[(s0 + i) * a.B + col]));
-        }
-        x[0] = ch > 0 ? carry_x(coef, a.Wp, a.Yin, a.Xin, a.P, a.B, col, s0 - 1) : 0.0;
-        x[kL + 1] = ch + 1 < a.P ? carry_x(coef, a.Wp, a.Yin, a.Xin, a.P, a.B, col, s0 + kL) : 0.0;
-    } else {
-#pragma unroll
-        for (int i = 0; i < kL + 2; ++i) x[i] = 0.0;
+// One Crank-Nicolson step for every (chunk, column): finish x_j from its
+// carry form, consume it (state store / adjoint accumulation), form the
+// right-hand side A- x_j + f_j (Stepper::apply_minus, diffusion1d.hpp:203-209,
+// and the forcing of :245-246, :302-303, :325-326), and solve the chunk locally
+// with zero boundary carries (TridiagSolver::solve_in_place, grid.hpp:67-73).
+// A CTA owns `cpb` consecutive chunks for all B columns: their W rows and row
+// coefficients are one contiguous range each, staged into shared memory by a
+// single TMA bulk copy; the eliminated values overwrite the tile in place and
+// the finished tile leaves with one bulk store. Thread = (chunk, column).
+template <int MODE>
+__global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
+    extern __shared__ __align__(128) double smem[];
+    __shared__ uint64_t bar;
+    const int B = a.B;
+    const int64_t ch0 = int64_t(blockIdx.x) * cpb;
+    const int nch = int(a.P - ch0 < cpb ? a.P - ch0 : cpb);
+    const int64_t r0 = ch0 * kL;
+    const int nrows = nch * kL;
+    double* tile = smem;                              // [cpb * kL][B]
+    double* cft = tile + size_t(cpb) * kL * B;        // [cpb * kL][kCoef]
+    const bool prev = a.Wp != nullptr;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar);
+        const uint32_t cbytes = uint32_t(nrows) * kCoef * sizeof(double);
+        const uint32_t wbytes = prev ? uint32_t(nrows) * B * sizeof(double) : 0u;
+        mbar_expect_tx(&bar, cbytes + wbytes);
+        bulk_g2s(cft, a.coef + r0 * kCoef, cbytes, &bar);
+        if (prev) bulk_g2s(tile, a.Wp + r0 * B, wbytes, &bar);
     }
-
-    // consumers of x_j on the physical nodes of this chunk
-    const int64_t k0 = s0 - a.row0;
-    if (a.mode == 0 && a.Uout) {
-#pragma unroll
-        for (int i = 0; i < kL; ++i) {
-            const int64_t k = k0 + i;
-            if (k >= 0 && k < a.n) a.Uout[k * a.S + col] = x[i + 1];
-        }
-    } else if (a.mode == 2 && a.Wp) {   // acc_q += q (u(j+1) - u(j)), diffusion1d.hpp:329-332
-#pragma unroll
-        for (int i = 0; i < kL; ++i) {
-            const int64_t k = k0 + i;
-            if (k >= 0 && k < a.n) {
-                double& ac = a.acc[k * a.B + col];
-                ac += x[i + 1] * (a.U1[k * a.S + src] - a.U0[k * a.S + src]);
-            }
-        }
-    }
-
-    double r[kL];
-#pragma unroll
-    for (int i = 0; i < kL; ++i) {
-        const double* cf = coef + (s0 + i) * kCoef;
-        r[i] = fma(cf[kCl], x[i], fma(cf[kCu], x[i + 2], cf[kMdiag] * x[i + 1]));
-    }
-    if (a.mode == 1) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    const int lc = threadIdx.x / B;
+    const int col = threadIdx.x - lc * B;
+    if (lc < nch) {
+        const int64_t ch = ch0 + lc;
+        const int64_t s0 = ch * kL;
+        const int src = col / a.bb;
         const int jc = col - src * a.bb;
-#pragma unroll
-        for (int i = 0; i < kL; ++i) {
-            const int64_t k = k0 + i;
-            if (k >= 0 && k < a.n)
-                r[i] -= a.c * (a.nu[k * a.bb + jc] * (a.U1[k * a.S + src] - a.U0[k * a.S + src]));
-        }
-    } else if (a.mode == 0) {   // point source of this column (:245-246)
-        const int64_t d = a.frow[col] - s0;
-        if (d >= 0 && d < kL) {
-#pragma unroll
+        double* tcol = tile + size_t(lc) * kL * B + col;   // tcol[i * B] = row s0 + i
+        const double* cf = cft + size_t(lc) * kL * kCoef;  // cf[i * kCoef + field]
+        const int64_t k0 = s0 - a.row0;                    // physical node of the chunk's first row
+        double xm = 0.0, xe = 0.0;
+        if (prev) {   // x_j from its carry form, in place; the neighbours' edge values
+            const double yc = a.Yin[col * a.P + ch], xc = a.Xin[col * a.P + ch];
+            if (ch > 0) xm = carry_x(a.coef, a.Wp, a.Yin, a.Xin, a.P, B, col, s0 - 1);
+            if (ch + 1 < a.P) xe = carry_x(a.coef, a.Wp, a.Yin, a.Xin, a.P, B, col, s0 + kL);
+#pragma unroll 8
             for (int i = 0; i < kL; ++i)
-                if (i == d) r[i] += a.fval;
-        }
-    } else {   // receiver residual sources (:325-326)
-        for (int q = 0; q < a.nfrow; ++q) {
-            const int64_t d = a.frow[q] - s0;
-            if (d >= 0 && d < kL) {
-                const double v = a.fval * a.vr[q * a.B + col];
-#pragma unroll
+                tcol[i * B] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, tcol[i * B]));
+            // consumers of x_j (loads first, then the read-modify-writes)
+            if (MODE == 0 && a.Uout) {
+#pragma unroll 8
                 for (int i = 0; i < kL; ++i)
-                    if (i == d) r[i] -= v;
+                    if (k0 + i >= 0 && k0 + i < a.n) a.Uout[(k0 + i) * a.S + col] = tcol[i * B];
+            } else if (MODE == 2) {   // acc_q += q (u(j+1) - u(j)), diffusion1d.hpp:329-332
+#pragma unroll 1
+                for (int i0 = 0; i0 < kL; i0 += 8) {   // eight loads in flight, then the stores
+                    double d[8], ac[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int64_t k = k0 + i0 + i;
+                        const bool ph = k >= 0 && k < a.n;
+                        d[i] = ph ? __ldg(a.du + k * a.S + src) : 0.0;
+                        ac[i] = ph ? a.acc[k * B + col] : 0.0;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int64_t k = k0 + i0 + i;
+                        if (k >= 0 && k < a.n) a.acc[k * B + col] = ac[i] + tcol[(i0 + i) * B] * d[i];
+                    }
+                }
             }
+        } else {
+#pragma unroll 8
+            for (int i = 0; i < kL; ++i) tcol[i * B] = 0.0;
         }
+        bool force = false;   // a point source / receiver row inside this chunk
+        if (MODE == 0) {
+            force = (a.frow[col] - s0) >= 0 && (a.frow[col] - s0) < kL;
+        } else if (MODE == 2) {
+            for (int q = 0; q < a.nfrow; ++q) force |= (a.frow[q] - s0) >= 0 && (a.frow[q] - s0) < kL;
+        }
+        double zp = 0.0, xi = tcol[0];
+#pragma unroll 8
+        for (int i = 0; i < kL; ++i) {
+            const int64_t row = s0 + i;
+            const double xn = i + 1 < kL ? tcol[(i + 1) * B] : xe;
+            const double cu = row + 1 < a.ns ? a.moff : 0.0;
+            const double cl = row >= 1 && row < a.ns ? a.moff : 0.0;
+            double r = fma(cl, xm, fma(cu, xn, cf[i * kCoef + kMdiag] * xi));
+            const int64_t k = row - a.row0;
+            if (MODE == 1 && k >= 0 && k < a.n)   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
+                r -= a.c * (__ldg(a.nu + k * a.bb + jc) * __ldg(a.du + k * a.S + src));
+            if (force) {
+                if (MODE == 0) {   // point source of the column (:245-246)
+                    if (a.frow[col] == row) r += a.fval;
+                } else {   // receiver residual sources (:325-326)
+                    for (int q = 0; q < a.nfrow; ++q)
+                        if (a.frow[q] == row) r -= a.fval * __ldg(a.vr + q * B + col);
+                }
+            }
+            // local forward elimination y_i = r_i - m_i y_{i-1} (zero carry-in)
+            zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
+            tcol[i * B] = zp;   // row i's x_j already lives in the window
+            xm = xi;
+            xi = xn;
+        }
+        a.zend[col * a.P + ch] = zp;
+        // local back substitution x_i = y_i / d_i - beta_i x_{i+1} (zero carry-in)
+        double w = zp * cf[(kL - 1) * kCoef + kRdfac];
+        tcol[(kL - 1) * B] = w;
+#pragma unroll 8
+        for (int i = kL - 2; i >= 0; --i) {
+            w = fma(-cf[i * kCoef + kBeta], w, cf[i * kCoef + kRdfac] * tcol[i * B]);
+            tcol[i * B] = w;
+        }
+        a.wstart[col * a.P + ch] = w;
     }
-
-    // local forward elimination y_i = r_i - m_i y_{i-1} (zero carry-in)
-#pragma unroll
-    for (int i = 1; i < kL; ++i) r[i] = fma(-coef[(s0 + i) * kCoef + kMult], r[i - 1], r[i]);
-    a.zend[col * a.P + ch] = r[kL - 1];
-    // local back substitution x_i = y_i / d_i - beta_i x_{i+1} (zero carry-in)
-    r[kL - 1] *= coef[(s0 + kL - 1) * kCoef + kRdfac];
-#pragma unroll
-    for (int i = kL - 2; i >= 0; --i) {
-        const double* cf = coef + (s0 + i) * kCoef;
-        r[i] = fma(-cf[kBeta], r[i + 1], cf[kRdfac] * r[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < kL; ++i) a.Wn[(s0 + i) * a.B + col] = r[i];
-    a.wstart[col * a.P + ch] = r[0];
+    __syncthreads();
+    if (threadIdx.x == 0) bulk_s2g(a.Wn + r0 * B, tile, uint32_t(nrows) * B * sizeof(double));
 }
 
 struct Aff {   // v -> a v + b
@@ -221,6 +284,32 @@ __device__ __forceinline__ Aff bwd_map(const CarryArgs& a, int col, int64_t c, d
     return c < a.P ? Aff{a.chunk[c * 3 + 2], fma(a.chunk[c * 3 + 1], yin, a.wstart[col * a.P + c])} : Aff{1.0, 0.0};
 }
 
+// composition of the segment maps q in [q0, q1) (ascending, or descending when
+// `desc`), evaluated by one warp as an order-preserving tree reduction
+__device__ Aff warp_compose(const double* agg, int q0, int q1, bool desc) {
+    const int lane = threadIdx.x & 31;
+    Aff run = {1.0, 0.0};
+    for (int base = 0; base < q1 - q0; base += 32) {
+        const int idx = base + lane;
+        Aff v = {1.0, 0.0};
+        if (idx < q1 - q0) {
+            const int q = desc ? q1 - 1 - idx : q0 + idx;
+            v = Aff{agg[2 * q], agg[2 * q + 1]};
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            Aff o;
+            o.a = __shfl_down_sync(0xffffffffu, v.a, off);
+            o.b = __shfl_down_sync(0xffffffffu, v.b, off);
+            if (lane + off < 32) v = then(v, o);
+        }
+        v.a = __shfl_sync(0xffffffffu, v.a, 0);
+        v.b = __shfl_sync(0xffffffffu, v.b, 0);
+        run = then(run, v);
+    }
+    return run;
+}
+
 __global__ void __launch_bounds__(kSeg) carry_fwd_reduce_kernel(CarryArgs a) {
     __shared__ Aff sm[32];
     const int seg = blockIdx.x, col = blockIdx.y;
@@ -238,11 +327,9 @@ __global__ void __launch_bounds__(kSeg) carry_fwd_scan_kernel(CarryArgs a) {
     __shared__ Aff run_s;
     const int seg = blockIdx.x, col = blockIdx.y;
     const int64_t c = int64_t(seg) * kSeg + threadIdx.x;
-    if (threadIdx.x == 0) {   // composition of every earlier segment
-        Aff run = {1.0, 0.0};
-        for (int q = 0; q < seg; ++q)
-            run = then(run, Aff{a.aggF[(col * a.nseg + q) * 2], a.aggF[(col * a.nseg + q) * 2 + 1]});
-        run_s = run;
+    if (threadIdx.x < 32) {   // composition of every earlier segment
+        const Aff run = warp_compose(a.aggF + size_t(col) * a.nseg * 2, 0, seg, false);
+        if (threadIdx.x == 0) run_s = run;
     }
     const Aff f = fwd_map(a, col, c);
     const Aff pre = block_exscan(f, false, sm);   // its barriers publish run_s
@@ -262,11 +349,9 @@ __global__ void __launch_bounds__(kSeg) carry_bwd_scan_kernel(CarryArgs a) {
     __shared__ Aff run_s;
     const int seg = blockIdx.x, col = blockIdx.y;
     const int64_t c = int64_t(seg) * kSeg + threadIdx.x;
-    if (threadIdx.x == 0) {   // composition of every later segment, last first
-        Aff run = {1.0, 0.0};
-        for (int q = a.nseg - 1; q > seg; --q)
-            run = then(run, Aff{a.aggB[(col * a.nseg + q) * 2], a.aggB[(col * a.nseg + q) * 2 + 1]});
-        run_s = run;
+    if (threadIdx.x < 32) {   // composition of every later segment, last first
+        const Aff run = warp_compose(a.aggB + size_t(col) * a.nseg * 2, seg + 1, a.nseg, true);
+        if (threadIdx.x == 0) run_s = run;
     }
     const double yin = c < a.P ? a.Yin[col * a.P + c] : 0.0;
     const Aff g = bwd_map(a, col, c, yin);
@@ -322,8 +407,8 @@ struct FinishArgs {
 __global__ void hess_finish_kernel(FinishArgs a) {
     const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (t >= a.n * a.bb) return;
-    const int jc = int(t / a.n);
-    const int64_t k = t - int64_t(jc) * a.n;
+    const int64_t k = t / a.bb;   // adjacent threads read adjacent columns of a row
+    const int jc = int(t - k * a.bb);
     double o = 0.0;
     for (int s = 0; s < a.S; ++s) {
         const int col = s * a.bb + jc;
@@ -341,6 +426,13 @@ __global__ void hess_finish_kernel(FinishArgs a) {
     a.y[(a.j0 + jc) * a.n + k] = o;
 }
 
+// u_{j+1} - u_j for every step (the du of both Hessian marches)
+__global__ void state_diff_kernel(const double* U, int64_t per_step, int64_t steps, double* du) {
+    const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (t >= per_step * steps) return;
+    du[t] = U[t + per_step] - U[t];
+}
+
 double ricker_wavelet(double t, double t_p) {   // ricker.hpp:12-19
     if (t_p <= 0) throw std::invalid_argument("ricker: t_p must be positive");
     const double u = M_PI * (t - 1.4 * t_p) / t_p;
@@ -355,15 +447,21 @@ struct Marcher {
     DeviceArray<double> W[2], zend, wstart, Yin, Xin, aggF, aggB;
     StepArgs a{};
     CarryArgs ca{};
-    int cur = 0, blocks = 0;
+    int cur = 0, cpb = 1;
+    size_t smem = 0;
     cudaStream_t s;
     Marcher(const double* coef, const double* chunk, int64_t P, int B, int bb, int S, int64_t row0, int64_t n,
-            double c, const int64_t* rrow, int R, cudaStream_t st)
+            int64_t ns, double moff, double c, const int64_t* rrow, int R, cudaStream_t st)
         : zend(size_t(P) * B, st), wstart(size_t(P) * B, st), Yin(size_t(P) * B, st), Xin(size_t(P) * B, st), s(st) {
         const int nseg = int((P + kSeg - 1) / kSeg);
         aggF.resize(size_t(nseg) * B * 2, st);
         aggB.resize(size_t(nseg) * B * 2, st);
         ca.nseg = nseg;
+        cpb = std::max(1, std::min(g_cpb_max, 256 / B));
+        smem = size_t(cpb) * kL * (B + kCoef) * sizeof(double);
+        H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         ca.aggF = aggF.data();
         ca.aggB = aggB.data();
         W[0].resize(size_t(P) * kL * B, st);
@@ -376,6 +474,8 @@ struct Marcher {
         a.row0 = row0;
         a.n = n;
         a.c = c;
+        a.ns = ns;
+        a.moff = moff;
         a.zend = zend.data();
         a.wstart = wstart.data();
         a.Yin = Yin.data();
@@ -390,13 +490,17 @@ struct Marcher {
         ca.Xin = Xin.data();
         ca.rrow = rrow;
         ca.R = R;
-        blocks = grid_for(P * B, 256);
     }
     // x_{j+1} from x_j (x_j = 0 when !has_prev); optionally record x_{j+1} at the receivers
     void step(bool has_prev, double* vr_out) {
         a.Wp = has_prev ? W[cur].data() : nullptr;
         a.Wn = W[cur ^ 1].data();
-        cn_step_kernel<<<blocks, 256, 0, s>>>(a);
+        if (a.mode == 0)
+            cn_step_kernel<0><<<grid_for(a.P, cpb), cpb * a.B, smem, s>>>(a, cpb);
+        else if (a.mode == 1)
+            cn_step_kernel<1><<<grid_for(a.P, cpb), cpb * a.B, smem, s>>>(a, cpb);
+        else
+            cn_step_kernel<2><<<grid_for(a.P, cpb), cpb * a.B, smem, s>>>(a, cpb);
         H2B_LAUNCH();
         ca.W = a.Wn;
         ca.vr_out = vr_out;
@@ -447,7 +551,8 @@ Diffusion1DDev::Diffusion1DDev(const Diff1DConfig& cfg, cudaStream_t s) : c_(cfg
     for (int64_t k = 0; k < c_.n; ++k) re[size_t(npad_ + k - 1)] = rho_[size_t(k)];
     for (double v : re)
         if (v <= 0) throw std::invalid_argument("diffusion1d: density must be positive");
-    const double koff = -1.0 / h_, kdiag = 2.0 / h_, off = koff / 2, moff = -koff / 2;
+    const double koff = -1.0 / h_, kdiag = 2.0 / h_, off = koff / 2;
+    moff_ = -koff / 2;
     std::vector<double> dfac(static_cast<size_t>(ns_)), mult(static_cast<size_t>(ns_), 0.0);
     for (int64_t i = 0; i < ns_; ++i) dfac[size_t(i)] = h_ * re[size_t(i)] / dt_ + kdiag / 2;
     for (int64_t i = 1; i < ns_; ++i) {
@@ -459,11 +564,11 @@ Diffusion1DDev::Diffusion1DDev(const Diff1DConfig& cfg, cudaStream_t s) : c_(cfg
     auto C = [&](int64_t i, int f) -> double& { return cf[size_t(i * kCoef + f)]; };
     for (int64_t i = 0; i < ns_; ++i) {
         C(i, kMdiag) = h_ * re[size_t(i)] / dt_ - kdiag / 2;
-        C(i, kCu) = i + 1 < ns_ ? moff : 0.0;
-        C(i, kCl) = i >= 1 ? moff : 0.0;
-        C(i, kMult) = mult[size_t(i)];
+        // the multipliers as the device evaluates them: off * (1 / d); the
+        // factor d itself follows the reference recurrence (grid.hpp:59-63)
         C(i, kRdfac) = 1.0 / dfac[size_t(i)];
-        C(i, kBeta) = i + 1 < ns_ ? off / dfac[size_t(i)] : 0.0;
+        C(i, kMult) = i >= 1 ? off * (1.0 / dfac[size_t(i - 1)]) : 0.0;
+        C(i, kBeta) = i + 1 < ns_ ? off * C(i, kRdfac) : 0.0;
     }
     // carry weights per chunk: g_i = prod_{s..i} (-m), hb_i = prod_{i..e-1} (-beta),
     // wg = local back substitution of g / d
@@ -512,7 +617,8 @@ Diffusion1DDev::Diffusion1DDev(const Diff1DConfig& cfg, cudaStream_t s) : c_(cfg
 void Diffusion1DDev::march_states(cudaStream_t s) {   // march_states (:237-255)
     const int S = num_sources();
     const int64_t T = c_.steps, nS = c_.n * S;
-    Marcher m(coef_.data(), chunk_.data(), P_, S, 1, S, npad_ - 1, c_.n, h_ / dt_, nullptr, 0, s);
+    H2B_CUDA(cudaMemsetAsync(u_.data(), 0, sizeof(double) * size_t(nS), s));
+    Marcher m(coef_.data(), chunk_.data(), P_, S, 1, S, npad_ - 1, c_.n, ns_, moff_, h_ / dt_, nullptr, 0, s);
     m.a.mode = 0;
     m.a.frow = rows_.data();
     for (int64_t j = 0; j < T; ++j) {   // store u_j while stepping to u_{j+1}
@@ -520,9 +626,11 @@ void Diffusion1DDev::march_states(cudaStream_t s) {   // march_states (:237-255)
         m.a.Uout = j > 0 ? u_.data() + j * nS : nullptr;
         m.step(j > 0, nullptr);
     }
-    H2B_CUDA(cudaMemsetAsync(u_.data(), 0, sizeof(double) * size_t(nS), s));
     store_state_kernel<<<grid_for(nS, 256), 256, 0, s>>>(coef_.data(), P_, S, m.Wcur(), m.Yin.data(), m.Xin.data(),
                                                          npad_ - 1, c_.n, u_.data() + T * nS);
+    H2B_LAUNCH();
+    du_.resize(size_t(T) * size_t(nS), s);
+    state_diff_kernel<<<grid_for(T * nS, 256), 256, 0, s>>>(u_.data(), nS, T, du_.data());
     H2B_LAUNCH();
     marches_ += S;
 }
@@ -531,20 +639,22 @@ void Diffusion1DDev::hessvec(bool include_tv, int64_t b, const double* x, double
     if (b < 1) throw std::invalid_argument("hessvec: dimension mismatch");
     const int S = num_sources(), R = num_receivers();
     const int64_t T = c_.steps, nS = c_.n * S;
-    for (int64_t j0 = 0; j0 < b; j0 += kMaxBatch) {
-        const int bb = int(std::min<int64_t>(kMaxBatch, b - j0));
+    // B = S * bb columns per batch, one thread each, at most 1024 per CTA
+    const int bmax = std::min(g_max_batch, std::max(1, 1024 / S));
+    for (int64_t j0 = 0; j0 < b; j0 += bmax) {
+        const int bb = int(std::min<int64_t>(bmax, b - j0));
         const int B = S * bb;
         DeviceArray<double> nu(size_t(c_.n) * bb, s), acc(size_t(c_.n) * B, s), vr(size_t(T + 1) * R * B, s);
         nu_rowmajor_kernel<<<grid_for(c_.n * bb, 256), 256, 0, s>>>(x, c_.n, j0, bb, nu.data());
         H2B_LAUNCH();
         acc.zero(s);
-        Marcher m(coef_.data(), chunk_.data(), P_, B, bb, S, npad_ - 1, c_.n, h_ / dt_, rows_.data() + S, R, s);
+        Marcher m(coef_.data(), chunk_.data(), P_, B, bb, S, npad_ - 1, c_.n, ns_, moff_, h_ / dt_, rows_.data() + S,
+                  R, s);
         // incremental state, forward (:297-313); v_{j+1} recorded at the receivers
         m.a.mode = 1;
         m.a.nu = nu.data();
         for (int64_t j = 0; j < T; ++j) {
-            m.a.U0 = u_.data() + j * nS;
-            m.a.U1 = u_.data() + (j + 1) * nS;
+            m.a.du = du_.data() + j * nS;
             m.step(j > 0, vr.data() + (j + 1) * R * B);
         }
         // incremental adjoint, backward (:317-333); each step first accumulates q_{j+1}
@@ -555,8 +665,7 @@ void Diffusion1DDev::hessvec(bool include_tv, int64_t b, const double* x, double
         for (int64_t j = T; j >= 1; --j) {
             m.a.fval = (j == T) ? dt_ / 2 : dt_;   // quad_weight (:188-190)
             m.a.vr = vr.data() + j * R * B;
-            m.a.U0 = u_.data() + j * nS;
-            m.a.U1 = j < T ? u_.data() + (j + 1) * nS : nullptr;
+            m.a.du = j < T ? du_.data() + j * nS : nullptr;
             m.step(j < T, nullptr);
         }
         FinishArgs f{};
@@ -603,3 +712,10 @@ std::unique_ptr<DevOperator> diffusion_hessian_operator(std::shared_ptr<Diffusio
 }
 
 }  // namespace h2b
+
+// diagnostics: kernel shape knobs for tools/diff1d_probe.py (not part of h2c.h)
+extern "C" int h2b_diff1d_tune(int cpb_max, int max_batch) {
+    if (cpb_max > 0) h2b::g_cpb_max = cpb_max;
+    if (max_batch > 0) h2b::g_max_batch = max_batch;
+    return 0;
+}

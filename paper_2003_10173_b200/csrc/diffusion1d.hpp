@@ -60,7 +60,7 @@ private:
 
     Diff1DConfig c_;
     int64_t npad_ = 0, ns_ = 0, P_ = 0;
-    double h_ = 0, dt_ = 0;
+    double h_ = 0, dt_ = 0, moff_ = 0;
     std::vector<int64_t> src_, rcv_;
     std::vector<double> rho_, srcval_;
     DeviceArray<double> coef_;      // per padded row: mdiag, cu, cl, mult, rdfac, beta, wg, hb
@@ -68,6 +68,7 @@ private:
     DeviceArray<double> tvw_;       // TV second-variation weight per edge (:31-32)
     DeviceArray<int64_t> rows_;     // source rows then receiver rows
     DeviceArray<double> u_;         // state at physical nodes: [step][k][source]
+    DeviceArray<double> du_;        // u_{j+1} - u_j: [step][k][source]
     long marches_ = 0;
 };
 

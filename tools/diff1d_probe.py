@@ -19,7 +19,7 @@ def main():
     ap.add_argument("--b", type=int, nargs="+", default=[1, 16, 32, 64])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--check", type=int, default=2)
-    ap.add_argument("--tune", nargs="*", default=[], help="cpb:batch pairs to sweep (chunks per step CTA cap, columns per batch), e.g. 16:64 4:16")
+    ap.add_argument("--tune", nargs="*", default=[], help="cpb:batch pairs to sweep (chunks per step CTA cap, columns per batch)")
     a = ap.parse_args()
     torch.cuda.init()
     t = time.perf_counter()
@@ -28,10 +28,10 @@ def main():
     print(f"setup {time.perf_counter() - t:.3f} s  nstate {d.nstate()}")
     from paper_2003_10173_b200._lib import lib
     combos = [tuple(int(v) for v in t.split(":")) for t in a.tune] or [(0, 0)]
-    for cpt, batch in combos:
-      if cpt:
-        lib.h2b_diff1d_tune(cpt, batch)
-        print(f"-- cpb<= {cpt}, batch {batch}")
+    for cpb, batch in combos:
+      if cpb:
+        lib.h2b_diff1d_tune(cpb, batch)
+        print(f"-- cpb<= {cpb}, batch {batch}")
       for b in a.b:
         x = torch.randn(b, a.n, dtype=torch.float64, device="cuda")
         y = torch.empty_like(x)
