@@ -707,11 +707,7 @@ int h2c_h_inverse(h2c_matrix a, h2c_matrix x0, int method, int arg, int dynamic_
                                                                           max_iter, nullptr);
             export_trace(r.trace, rows, max_rows, num_rows, final_residual, converged);
             *out = wrap_matrix(std::move(r.X));
-        } catch (const h2b::io_error& e) {
-        g_err = e.what();
-        g_io_kind = int(e.kind);
-        return H2C_IO_ERROR;
-    } catch (const h2b::divergence_error& e) {
+        } catch (const h2b::divergence_error& e) {
             export_trace(e.trace, rows, max_rows, num_rows, final_residual, converged);
             throw;
         }

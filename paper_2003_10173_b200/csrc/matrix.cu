@@ -228,7 +228,8 @@ __global__ void gen_dense_kernel(int nb, const int* rows, const int* cols, const
 // first, e.g. 2D k=32 -> 8 x 4, 3D k=32 -> 4 x 4 x 2, k=64 -> 4 x 4 x 4
 void axis_counts(int dim, int k, const double* ext, int* p) {
     int order[3] = {0, 1, 2};
-    std::sort(order, order + dim, [&](int a, int b) { return ext[a] > ext[b]; });
+    for (int i = 1; i < dim && i < 3; ++i)   // stable insertion sort of <= 3 axes, longest first
+        for (int j = i; j > 0 && ext[order[j]] > ext[order[j - 1]]; --j) std::swap(order[j], order[j - 1]);
     for (int d = 0; d < 3; ++d) p[d] = 1;
     // factor k into dim factors as evenly as possible, biggest to longest axis
     int rem = k;

@@ -300,14 +300,14 @@ Deserialized deserialize(const char* data, size_t size) {   // serialize.hpp:184
             if (t.is_leaf(v)) {
                 const Mat& m = in.leaf[size_t(v)];
                 if (m.r != t.size(v) || m.c != k) throw io_error(io_error::malformed, "H2M1: leaf basis shape");
-                if (m.r * m.c) std::memcpy(leaf.data() + lay.leaf_off[size_t(v)], m.d, size_t(m.r * m.c) * 8);
+                if (m.r > 0 && m.c > 0) std::memcpy(leaf.data() + lay.leaf_off[size_t(v)], m.d, size_t(m.r * m.c) * 8);
             }
             const int par = t.parent[size_t(v)];
             if (par >= 0) {
                 const Mat& m = in.xfer[size_t(v)];
                 if (m.r != k || m.c != lay.rank[size_t(par)])
                     throw io_error(io_error::malformed, "H2M1: transfer shape");
-                if (m.r * m.c) std::memcpy(xf.data() + lay.xfer_off[size_t(v)], m.d, size_t(m.r * m.c) * 8);
+                if (m.r > 0 && m.c > 0) std::memcpy(xf.data() + lay.xfer_off[size_t(v)], m.d, size_t(m.r * m.c) * 8);
             }
         }
     };
@@ -322,7 +322,7 @@ Deserialized deserialize(const char* data, size_t size) {   // serialize.hpp:184
         if (h->s_off[size_t(i)] < 0) continue;   // non-canonical slot of a symmetric matrix stays empty
         if (m.r != h->row.rank[size_t(bt->row[size_t(b)])] || m.c != cb.rank[size_t(bt->col[size_t(b)])])
             throw io_error(io_error::malformed, "H2M1: coupling shape");
-        if (m.r * m.c) std::memcpy(S.data() + h->s_off[size_t(i)], m.d, size_t(m.r * m.c) * 8);
+        if (m.r > 0 && m.c > 0) std::memcpy(S.data() + h->s_off[size_t(i)], m.d, size_t(m.r * m.c) * 8);
     }
     for (auto& [b, m] : dens) {
         if (b < 0 || b >= bt->num_nodes() || bt->dense_ord[size_t(b)] < 0)
@@ -331,7 +331,7 @@ Deserialized deserialize(const char* data, size_t size) {   // serialize.hpp:184
         if (h->d_off[size_t(i)] < 0) continue;
         if (m.r != t.size(bt->row[size_t(b)]) || m.c != t.size(bt->col[size_t(b)]))
             throw io_error(io_error::malformed, "H2M1: dense shape");
-        if (m.r * m.c) std::memcpy(Dd.data() + h->d_off[size_t(i)], m.d, size_t(m.r * m.c) * 8);
+        if (m.r > 0 && m.c > 0) std::memcpy(Dd.data() + h->d_off[size_t(i)], m.d, size_t(m.r * m.c) * 8);
     }
     const double* parts[6] = {U.data(), E.data(), sym ? nullptr : V.data(), sym ? nullptr : F.data(), S.data(),
                               Dd.data()};
