@@ -524,12 +524,16 @@ def run_hara(args, cfg, world, rank, local, dist):
     from paper_2003_10173_b200._lib import lib as _l
     _l.h2b_plan_build_ms.restype = C.c_double
     _l.h2b_plan_build_ms.argtypes = [C.c_int]
+    _l.h2b_plan_sync_ms.restype = C.c_double
+    _l.h2b_plan_sync_ms.argtypes = [C.c_int]
     times, opms = [], []
     with ClockSampler(local) as clk:
         for _ in range(steps):
             op.reset_counter()
             torch.cuda.synchronize()
             _l.h2b_plan_build_ms(1)
+            _l.h2b_plan_sync_ms(1)
+            _l.h2b_plan_parts_ms((C.c_double * 4)(), 1)
             t0 = time.perf_counter()
             res = peel_construct(op, bt, pc)
             torch.cuda.synchronize()
@@ -541,12 +545,18 @@ def run_hara(args, cfg, world, rank, local, dist):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     plan_ms = _l.h2b_plan_build_ms(0)
+    plan_sync_ms = _l.h2b_plan_sync_ms(0)
+    parts = (C.c_double * 4)()
+    _l.h2b_plan_parts_ms(parts, 0)
     ph = (C.c_double * 16)()
     _l.h2b_hara_phase_ms(ph, 16)
     phases = dict(zip(["rng", "op_apply", "residual_hgemv", "absorb", "transposed_pass", "local_updates",
                        "recompress", "dense_leaves", "orthogonalize_all", "truncation_bases", "projection"],
                       [round(v / 1e3, 4) for v in ph]))
     phases["hgemv_plan_builds"] = round(plan_ms / 1e3, 4)
+    phases["hgemv_plan_builds_device_sync"] = round(plan_sync_ms / 1e3, 4)
+    phases["hgemv_plan_builds_split"] = {"task_lists": round(parts[0] / 1e3, 4), "ue_products": round(parts[1] / 1e3, 4),
+                                         "uploads": round(parts[2] / 1e3, 4), "count": int(parts[3])}
     phases["all_steps_s"] = [round(v, 4) for v in times]
     err = estimate_relative_error(op, res.matrix)
     prof = [int(v) for v in res.matrix.rank_profile()]

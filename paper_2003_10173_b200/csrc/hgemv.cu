@@ -794,15 +794,17 @@ struct PlanBuilder {
     std::vector<SegEntry> entries;
     std::vector<LaunchDesc> launches;
 
+    // one output of a launch: its entries are pool[e_begin, e_end) of the caller's flat pool
     struct Pending {
         int rows;
         int out_ld;
         int64_t out_unit;
-        std::vector<SegEntry> es;
+        int e_begin, e_end;
     };
 
     int phase = 0;
-    void emit(std::vector<Pending>& outs, int mode, int out, int stage, bool zero_yhat = false) {
+    void emit(const std::vector<Pending>& outs, const std::vector<SegEntry>& pool, int mode, int out, int stage,
+              bool zero_yhat = false) {
         LaunchDesc ld;
         ld.phase = phase;
         ld.stage = stage;
@@ -813,12 +815,15 @@ struct PlanBuilder {
         for (auto& p : outs) maxrows = std::max(maxrows, p.rows);
         ld.mt = maxrows > 32 ? 64 : 32;
         ld.task_begin = int(tasks.size());
+        entries.reserve(entries.size() + pool.size());
+        tasks.reserve(tasks.size() + outs.size());
         bool vec = true, ue = true;
         for (auto& p : outs) {
             if (p.rows <= 0) continue;
             const int e0 = int(entries.size());
             int nsteps = 0, nsteps16 = 0;
-            for (auto& e : p.es) {
+            for (int q = p.e_begin; q < p.e_end; ++q) {
+                const SegEntry& e = pool[size_t(q)];
                 if (e.k <= 0) continue;
                 entries.push_back(e);
                 nsteps += (e.k + 31) / 32;
@@ -826,7 +831,9 @@ struct PlanBuilder {
                 const int64_t aoff = reinterpret_cast<uintptr_t>(e.A) / sizeof(double);
                 vec = vec && (aoff % 2 == 0) && (e.lda % 2 == 0) && (e.ldb % 2 == 0);
                 ue = ue && (e.b_unit % 2 == 0);
+                ld.flops_per_col += 2.0 * p.rows * e.k;
             }
+            ld.out_per_col += p.rows;
             const int e1 = int(entries.size());
             for (int r0 = 0; r0 < p.rows; r0 += ld.mt) {
                 SegTask tk{};
@@ -858,14 +865,23 @@ struct PlanBuilder {
         ld.vec = vec;
         ld.units_even = ue;
         ld.task_end = int(tasks.size());
-        for (auto& p : outs) {
-            if (p.rows <= 0) continue;
-            ld.out_per_col += p.rows;
-            for (auto& e : p.es)
-                if (e.k > 0) ld.flops_per_col += 2.0 * p.rows * e.k;
-        }
         if (ld.task_end > ld.task_begin || zero_yhat) launches.push_back(ld);
     }
+};
+
+// entries grouped by output node in a flat pool: count, then fill in call order
+struct EntryCsr {
+    std::vector<int> start;   // per node: first slot; start[nn] = total
+    std::vector<int> fill;
+    std::vector<SegEntry> pool;
+    explicit EntryCsr(int nn) : start(size_t(nn) + 1, 0) {}
+    void count(int v, int c = 1) { start[size_t(v) + 1] += c; }
+    void finish_count() {
+        for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
+        fill.assign(start.begin(), start.end() - 1);
+        pool.resize(size_t(start.back()));
+    }
+    void add(int v, const SegEntry& e) { pool[size_t(fill[size_t(v)]++)] = e; }
 };
 
 SegEntry make_entry(const double* A, int lda, int k, bool trans, int src, int64_t b_unit, int ldb) {
@@ -900,6 +916,9 @@ std::shared_ptr<const DeviceArray<int>> tree_perm(const std::shared_ptr<const Cl
     return d;
 }
 
+double g_plan_sync_ms = 0;   // of which: the closing device synchronisation (diagnostics)
+double g_plan_part_ms[4];    // diagnostics: task lists / U E products / uploads / count of builds
+
 std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const DistSpec* ds = nullptr,
                                       bool small = false) {
     const ClusterTree& ct = h.tree();
@@ -924,33 +943,44 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     }
     PlanBuilder pb;
     using P = PlanBuilder::Pending;
+    auto tpart = std::chrono::steady_clock::now();
+    auto lap = [&](int q) {
+        const auto t = std::chrono::steady_clock::now();
+        g_plan_part_ms[q] += std::chrono::duration<double, std::milli>(t - tpart).count();
+        tpart = t;
+    };
+    g_plan_part_ms[3] += 1;
+    std::vector<P> outs;
+    std::vector<SegEntry> pool;
     // stage 1a: leaves  xhat_t = U_t^T X_t
     {
-        std::vector<P> outs;
+        outs.clear();
+        pool.clear();
         for (int t : ct.leaves) {
             if (!own(t)) continue;
             const int k = up.rank[size_t(t)], m = int(ct.size(t));
-            P p{k, k, cu[size_t(t)], {}};
-            p.es.push_back(make_entry(up.leaf.data() + up.leaf_off[size_t(t)], m, m, true, 0, ct.begin[size_t(t)], m));
-            outs.push_back(std::move(p));
+            const int e0 = int(pool.size());
+            pool.push_back(make_entry(up.leaf.data() + up.leaf_off[size_t(t)], m, m, true, 0, ct.begin[size_t(t)], m));
+            outs.push_back(P{k, k, cu[size_t(t)], e0, e0 + 1});
         }
-        pb.emit(outs, kModeSet, 1, 1);
+        pb.emit(outs, pool, kModeSet, 1, 1);
     }
     // stage 1b: transfers bottom-up
     for (int l = ct.depth - 1; l >= 0; --l) {
-        std::vector<P> outs;
+        outs.clear();
+        pool.clear();
         pb.phase = (ds && l < ds->lp) ? 1 : 0;
         for (int v : ct.levels[size_t(l)]) {
             if (ct.is_leaf(v) || !local(v)) continue;
             const int kv = up.rank[size_t(v)];
-            P p{kv, kv, cu[size_t(v)], {}};
+            const int e0 = int(pool.size());
             for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]}) {
                 const int kc = up.rank[size_t(c)];
-                p.es.push_back(make_entry(up.xfer.data() + up.xfer_off[size_t(c)], kc, kc, true, 1, cu[size_t(c)], kc));
+                pool.push_back(make_entry(up.xfer.data() + up.xfer_off[size_t(c)], kc, kc, true, 1, cu[size_t(c)], kc));
             }
-            outs.push_back(std::move(p));
+            outs.push_back(P{kv, kv, cu[size_t(v)], e0, int(pool.size())});
         }
-        pb.emit(outs, kModeSet, 1, 2);
+        pb.emit(outs, pool, kModeSet, 1, 2);
     }
     // symmetric few-vector path: block passes (kinds 1, 3) + slot sums (kinds 2, 4)
     std::vector<SymBlock> sblocks;
@@ -1030,7 +1060,19 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     }
     // stage 2: couplings, row-CSR over target nodes (yhat zeroed first)
     if (!small) {
-        std::vector<std::vector<SegEntry>> by_target(static_cast<size_t>(nn));
+        EntryCsr by_target(nn);
+        for (size_t i = 0; i < bt.adm.size(); ++i) {
+            const int b = bt.adm[i];
+            if (!h.stores(b)) continue;
+            const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
+            if (!swap) {
+                by_target.count(r);
+                if (h.symmetric && r != c) by_target.count(c);
+            } else {
+                by_target.count(c);
+            }
+        }
+        by_target.finish_count();
         for (size_t i = 0; i < bt.adm.size(); ++i) {
             const int b = bt.adm[i];
             if (!h.stores(b)) continue;
@@ -1038,39 +1080,41 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
             const double* S = h.S.data() + h.s_off[i];
             const int kr = h.row.rank[size_t(r)], kc = h.vbasis().rank[size_t(c)];
             if (!swap) {
-                by_target[size_t(r)].push_back(make_entry(S, kr, kc, false, 1, cu[size_t(c)], kc));
-                if (h.symmetric && r != c) by_target[size_t(c)].push_back(make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
+                by_target.add(r, make_entry(S, kr, kc, false, 1, cu[size_t(c)], kc));
+                if (h.symmetric && r != c) by_target.add(c, make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
             } else {
-                by_target[size_t(c)].push_back(make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
+                by_target.add(c, make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
             }
         }
-        std::vector<P> outs;
+        outs.clear();
         pb.phase = 1;
         for (int v = 0; v < nn; ++v) {
             // every local node with a rank gets a task (nodes without couplings write
             // zeros), so y-hat needs no memset before the downsweep accumulates
             if (!local(v) || down.rank[size_t(v)] == 0) continue;
             const int k = down.rank[size_t(v)];
-            outs.push_back(P{k, k, cd[size_t(v)], std::move(by_target[size_t(v)])});
+            outs.push_back(P{k, k, cd[size_t(v)], by_target.start[size_t(v)], by_target.start[size_t(v) + 1]});
         }
-        pb.emit(outs, kModeSet, 2, 3);
+        pb.emit(outs, by_target.pool, kModeSet, 2, 3);
     }
     // stage 3: downsweep top-down  yhat_c += E_c yhat_v
     for (int l = 0; l < ct.depth; ++l) {
-        std::vector<P> outs;
+        outs.clear();
+        pool.clear();
         for (int v : ct.levels[size_t(l)]) {
             if (ct.is_leaf(v)) continue;
             const int kv = down.rank[size_t(v)];
             for (int c : {ct.child0[size_t(v)], ct.child1[size_t(v)]}) {
                 if (!local(c) || ct.is_leaf(c)) continue;   // leaves: folded into stage 5 via U_t E_t
                 const int kc = down.rank[size_t(c)];
-                P p{kc, kc, cd[size_t(c)], {}};
-                p.es.push_back(make_entry(down.xfer.data() + down.xfer_off[size_t(c)], kc, kv, false, 2, cd[size_t(v)], kv));
-                outs.push_back(std::move(p));
+                const int e0 = int(pool.size());
+                pool.push_back(make_entry(down.xfer.data() + down.xfer_off[size_t(c)], kc, kv, false, 2, cd[size_t(v)], kv));
+                outs.push_back(P{kc, kc, cd[size_t(c)], e0, e0 + 1});
             }
         }
-        pb.emit(outs, kModeAdd, 2, 4);
+        pb.emit(outs, pool, kModeAdd, 2, 4);
     }
+    lap(0);
     // U_t E_t for every owned non-root leaf (one batched GEMM at plan time)
     std::vector<int64_t> ue_off(static_cast<size_t>(nn), -1);
     {
@@ -1092,15 +1136,29 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         }
         la::bgemm(g, nullptr);
     }
+    lap(1);
     // stage 3b + 4: leaves  y_t = alpha (U_t yhat_t + (U_t E_t) yhat_parent + sum op(D) X_s) + beta y_t
     {
-        std::vector<std::vector<SegEntry>> by_leaf(static_cast<size_t>(nn));
+        EntryCsr by_leaf(nn);
+        for (int t : ct.leaves) by_leaf.count(t, ue_off[size_t(t)] >= 0 ? 2 : 1);
+        for (size_t i = 0; i < bt.dense.size() && !small; ++i) {
+            const int b = bt.dense[i];
+            if (!h.stores(b)) continue;
+            const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
+            if (!swap) {
+                by_leaf.count(r);
+                if (h.symmetric && r != c) by_leaf.count(c);
+            } else {
+                by_leaf.count(c);
+            }
+        }
+        by_leaf.finish_count();
         for (int t : ct.leaves) {
             const int k = down.rank[size_t(t)], m = int(ct.size(t));
-            by_leaf[size_t(t)].push_back(make_entry(down.leaf.data() + down.leaf_off[size_t(t)], m, k, false, 2, cd[size_t(t)], k));
+            by_leaf.add(t, make_entry(down.leaf.data() + down.leaf_off[size_t(t)], m, k, false, 2, cd[size_t(t)], k));
             if (ue_off[size_t(t)] >= 0) {
                 const int p = ct.parent[size_t(t)], kp = down.rank[size_t(p)];
-                by_leaf[size_t(t)].push_back(make_entry(plan->ue.data() + ue_off[size_t(t)], m, kp, false, 2, cd[size_t(p)], kp));
+                by_leaf.add(t, make_entry(plan->ue.data() + ue_off[size_t(t)], m, kp, false, 2, cd[size_t(p)], kp));
             }
         }
         for (size_t i = 0; i < bt.dense.size() && !small; ++i) {
@@ -1110,19 +1168,19 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
             const double* D = h.D.data() + h.d_off[i];
             const int mr = int(ct.size(r)), mc = int(ct.size(c));
             if (!swap) {
-                by_leaf[size_t(r)].push_back(make_entry(D, mr, mc, false, 0, ct.begin[size_t(c)], mc));
-                if (h.symmetric && r != c) by_leaf[size_t(c)].push_back(make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
+                by_leaf.add(r, make_entry(D, mr, mc, false, 0, ct.begin[size_t(c)], mc));
+                if (h.symmetric && r != c) by_leaf.add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
             } else {
-                by_leaf[size_t(c)].push_back(make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
+                by_leaf.add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
             }
         }
-        std::vector<P> outs;
+        outs.clear();
         for (int t : ct.leaves) {
             if (!own(t)) continue;
             const int m = int(ct.size(t));
-            outs.push_back(P{m, m, ct.begin[size_t(t)], std::move(by_leaf[size_t(t)])});
+            outs.push_back(P{m, m, ct.begin[size_t(t)], by_leaf.start[size_t(t)], by_leaf.start[size_t(t) + 1]});
         }
-        pb.emit(outs, kModeY, 3, 5);
+        pb.emit(outs, by_leaf.pool, kModeY, 3, 5);
     }
     if (small) {
         std::vector<int> lv, lr;
@@ -1146,6 +1204,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         plan->csr_slots.upload(sslots);
         plan->scratch_rows = srows;
     }
+    lap(0);
     plan->launches = std::move(pb.launches);
     plan->tasks.upload(pb.tasks);
     plan->entries.upload(pb.entries);
@@ -1163,7 +1222,10 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     plan->cu = std::move(cu);
     plan->leaf_begin.upload(lb);
     plan->leaf_m.upload(lm);
+    lap(2);
+    const auto ts = std::chrono::steady_clock::now();
     H2B_CUDA(cudaDeviceSynchronize());
+    g_plan_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count();
     return plan;
 }
 
@@ -1739,5 +1801,17 @@ extern "C" int h2b_tune(int which, int value) {
 extern "C" double h2b_plan_build_ms(int reset) {
     const double v = h2b::g_plan_build_ms;
     if (reset) h2b::g_plan_build_ms = 0;
+    return v;
+}
+extern "C" int h2b_plan_parts_ms(double* out, int reset) {
+    for (int q = 0; q < 4; ++q) {
+        out[q] = h2b::g_plan_part_ms[q];
+        if (reset) h2b::g_plan_part_ms[q] = 0;
+    }
+    return 0;
+}
+extern "C" double h2b_plan_sync_ms(int reset) {
+    const double v = h2b::g_plan_sync_ms;
+    if (reset) h2b::g_plan_sync_ms = 0;
     return v;
 }
