@@ -31,6 +31,9 @@ void ensure_mem_pool();
 // pinned host staging for small host->device uploads (descriptor lists, plans):
 // a pageable cudaMemcpyAsync would synchronise the stream first
 void* stage_to_device(const void* host, size_t bytes, void* dev_dst, cudaStream_t s);
+// read-only descriptor list for kernels launched on `s`: copied into a device
+// ring (no allocation); nullptr when too large for the ring (caller allocates)
+const void* stage_descriptors(const void* host, size_t bytes, cudaStream_t s);
 
 // owning device allocation (never host memory); `s` = the stream the buffer is
 // allocated on and freed on (nullptr = legacy default stream)

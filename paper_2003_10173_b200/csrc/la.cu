@@ -14,18 +14,24 @@ namespace h2b {
 namespace la {
 namespace {
 
+// descriptor list in device memory for one launch: a slot of the staging
+// ring when it fits (no allocation), else a pool allocation
 template <class T>
 struct DevVec {
-    T* p = nullptr;
+    const T* p = nullptr;
+    T* own = nullptr;
     cudaStream_t s;
     DevVec(const std::vector<T>& h, cudaStream_t st) : s(st) {
         if (h.empty()) return;
+        p = static_cast<const T*>(stage_descriptors(h.data(), h.size() * sizeof(T), s));
+        if (p) return;
         ensure_mem_pool();
-        H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), h.size() * sizeof(T), s));
-        stage_to_device(h.data(), h.size() * sizeof(T), p, s);
+        H2B_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&own), h.size() * sizeof(T), s));
+        H2B_CUDA(cudaMemcpyAsync(own, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        p = own;
     }
     ~DevVec() {
-        if (p) cudaFreeAsync(p, s);
+        if (own) cudaFreeAsync(own, s);
     }
 };
 
