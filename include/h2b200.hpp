@@ -20,6 +20,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -214,8 +215,20 @@ public:
     }
     void reset_counter() const { detail::check(h2c_operator_reset_counter(h_.get())); }
     h2c_operator handle() const { return h_.get(); }
+    // apply / apply_transpose (linear_operator.hpp:28-39): n x b host matrix in user ordering
+    template <class M>
+    Matrix apply(const M& x) const { return run(x, 0); }
+    template <class M>
+    Matrix apply_transpose(const M& x) const { return run(x, 1); }
 
 private:
+    template <class M>
+    Matrix run(const M& x, int t) const {
+        if (Index(x.rows()) != n_) throw std::invalid_argument("operator apply: dimension mismatch");
+        Matrix y(n_, x.cols());
+        if (x.cols() > 0) detail::check(h2c_operator_apply_host(h_.get(), t, x.cols(), x.data(), y.data()));
+        return y;
+    }
     std::shared_ptr<h2c_operator_s> h_;
     Index n_;
     bool sym_;
@@ -331,6 +344,123 @@ inline double estimate_relative_error(const LinearOperator& op, const H2Matrix& 
     detail::check(h2c_estimate_relative_error(op.handle(), h.handle(), op_norm, &v));
     return v;
 }
+
+// ---- h2::oracles (oracles/diffusion1d.hpp, registry.hpp): the cfg3 black box on the device ----
+namespace oracles {
+
+struct Diffusion1DConfig {   // diffusion1d.hpp:62-73
+    Index n = 512;
+    double pad = 0.5;
+    double final_time = 30.0;
+    Index steps = 512;
+    double t_p = 1.0;
+    double t_0 = 0.0;
+    double source_amplitude = 1000.0;
+    double alpha = 3e-5, beta = 1e-3;
+    std::vector<double> source_positions{-0.5, 0.0, 0.5};
+    Index num_receivers = 8;
+};
+
+class Diffusion1D {   // diffusion1d.hpp:75-123, Hessian at the target only (:173-181)
+public:
+    explicit Diffusion1D(Diffusion1DConfig cfg = {}) : cfg_(std::move(cfg)) {
+        h2c_diff1d_config c;
+        h2c_diff1d_config_default(&c);
+        c.n = cfg_.n;
+        c.steps = cfg_.steps;
+        c.final_time = cfg_.final_time;
+        c.t_p = cfg_.t_p;
+        c.t_0 = cfg_.t_0;
+        c.source_amplitude = cfg_.source_amplitude;
+        c.alpha = cfg_.alpha;
+        c.beta = cfg_.beta;
+        c.pad = cfg_.pad;
+        c.num_sources = int(cfg_.source_positions.size());
+        c.source_positions = cfg_.source_positions.data();
+        c.num_receivers = cfg_.num_receivers;
+        h2c_diff1d d = nullptr;
+        detail::check(h2c_diff1d_create(&c, nullptr, &d));
+        h_ = std::shared_ptr<h2c_diff1d_s>(d, [](h2c_diff1d p) { h2c_diff1d_destroy(p); });
+    }
+    Index n() const { return cfg_.n; }
+    const Diffusion1DConfig& config() const { return cfg_; }
+    double spacing() const { return info().h; }
+    double dt() const { return info().dt; }
+    long pde_solves() const { return long(info().solves); }
+    PointSet points() const {   // Grid1D(-1, 1, n).points() (grid.hpp:10-24)
+        std::vector<double> c(static_cast<size_t>(cfg_.n));
+        const double h = 2.0 / double(cfg_.n - 1);
+        for (Index i = 0; i < cfg_.n; ++i) c[size_t(i)] = -1.0 + h * double(i);
+        return PointSet(cfg_.n, 1, c);
+    }
+    // hessian_operator(include_tv) (:177-181): the operator keeps the problem alive
+    LinearOperator hessian_operator(bool include_tv = true) const {
+        h2c_operator o = nullptr;
+        detail::check(h2c_diff1d_operator(h_.get(), include_tv ? 1 : 0, &o));
+        return LinearOperator(o, cfg_.n, true, h_);
+    }
+
+private:
+    struct Info {
+        int64_t ns, npad, solves;
+        double h, dt;
+    };
+    Info info() const {
+        Info i{};
+        detail::check(h2c_diff1d_info(h_.get(), &i.ns, &i.npad, &i.h, &i.dt, &i.solves));
+        return i;
+    }
+    Diffusion1DConfig cfg_;
+    std::shared_ptr<h2c_diff1d_s> h_;
+};
+
+struct Oracle {   // registry.hpp:58-81 (diffusion entries)
+    std::string name;
+    std::shared_ptr<LinearOperator> op;
+    PointSet points{0, 1, {}};
+    Index leaf = 32;
+    Admissibility mode = Admissibility::weak;
+    double eta = 1.0;
+    std::shared_ptr<Diffusion1D> diffusion;
+    std::shared_ptr<const BlockTree> default_block_tree() const {
+        auto ct = build_cluster_tree(points, leaf);
+        return build_block_tree(ct, ct, eta, mode);
+    }
+};
+
+using Config = std::map<std::string, std::string>;
+// make_oracle("diff1d-<n>", config) (registry.hpp:104-124); other oracles have no device port
+inline Oracle make_oracle(const std::string& name, const Config& config = {}) {
+    auto num = [&](const char* k, double d) {
+        auto it = config.find(k);
+        return it == config.end() ? d : std::stod(it->second);
+    };
+    if (name.rfind("diff1d-", 0) != 0) {
+        if (name.rfind("surface", 0) == 0 || name.rfind("advdiff-", 0) == 0)
+            throw std::logic_error("make_oracle: " + name + " has no device port");
+        throw std::invalid_argument("unknown oracle " + name);
+    }
+    Diffusion1DConfig dc;
+    dc.n = Index(std::stoll(name.substr(7)));
+    dc.steps = Index(num("steps", double(dc.steps)));
+    dc.final_time = num("T", dc.final_time);
+    dc.t_p = num("tp", dc.t_p);
+    dc.t_0 = num("t0", dc.t_0);
+    dc.alpha = num("alpha", dc.alpha);
+    dc.source_amplitude = num("amp", dc.source_amplitude);
+    dc.beta = num("beta", dc.beta);
+    dc.pad = num("pad", dc.pad);
+    Oracle o;
+    o.name = name;
+    o.diffusion = std::make_shared<Diffusion1D>(dc);
+    o.op = std::make_shared<LinearOperator>(o.diffusion->hessian_operator(num("tv", 1) != 0));
+    o.points = o.diffusion->points();
+    o.leaf = Index(num("leaf", 32));
+    o.eta = num("eta", 1.0);
+    return o;
+}
+
+}  // namespace oracles
 
 }  // namespace b200
 }  // namespace h2

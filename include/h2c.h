@@ -148,6 +148,9 @@ int h2c_operator_host_callback(int64_t n, int symmetric, int has_transpose, h2c_
 void h2c_operator_destroy(h2c_operator op);
 /* LinearOperator::apply / apply_transpose on device buffers */
 int h2c_operator_apply(h2c_operator op, int transpose, int64_t b, const double* x, double* y, void* stream);
+/* the same on HOST buffers (n x b column-major; staged through HBM; returns when y is written):
+ * the by-value LinearOperator::apply(const Matrix&) (linear_operator.hpp:28-39) */
+int h2c_operator_apply_host(h2c_operator op, int transpose, int64_t b, const double* x, double* y);
 /* columns_applied() / reset_counter() */
 int h2c_operator_columns_applied(h2c_operator op, int64_t* cols);
 int h2c_operator_reset_counter(h2c_operator op);

@@ -433,6 +433,19 @@ int h2c_operator_apply(h2c_operator op, int transpose, int64_t b, const double* 
     });
 }
 
+int h2c_operator_apply_host(h2c_operator op, int transpose, int64_t b, const double* x, double* y) {
+    return guard([&] {
+        need(op != nullptr && x != nullptr && y != nullptr, "null argument");
+        need(b >= 1, "operator apply: need at least one column");
+        const size_t nb = size_t(op->op->dim()) * size_t(b);
+        h2b::DeviceArray<double> dx(nb, nullptr), dy(nb, nullptr);
+        H2B_CUDA(cudaMemcpy(dx.data(), x, nb * sizeof(double), cudaMemcpyHostToDevice));
+        if (transpose) op->op->apply_transpose(b, dx.data(), dy.data(), nullptr);
+        else op->op->apply(b, dx.data(), dy.data(), nullptr);
+        H2B_CUDA(cudaMemcpy(y, dy.data(), nb * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
 int h2c_operator_columns_applied(h2c_operator op, int64_t* cols) {
     return guard([&] {
         need(op != nullptr && cols != nullptr, "null argument");

@@ -116,3 +116,35 @@ TEST_CASE("max_rank_error is raised with the reference's exception type") {   //
 }
 
 MINI_MAIN
+
+TEST_CASE("diffusion oracle: registry, symmetric PSD Hessian, two marches per source") {   // test_oracles.cpp:205-238, 321-331
+    auto o = oracles::make_oracle("diff1d-64", {{"steps", "32"}, {"leaf", "16"}});
+    CHECK(o.op->dim() == 64);
+    CHECK(o.leaf == 16);
+    CHECK(o.mode == Admissibility::weak);
+    CHECK(o.diffusion->config().steps == 32);
+    std::mt19937_64 rng(85);
+    Matrix x = random_matrix(64, 1, rng), y = random_matrix(64, 1, rng);
+    const Matrix hx = o.op->apply(x), hy = o.op->apply(y);
+    double a = 0, b = 0, q = 0;
+    for (Index i = 0; i < 64; ++i) {
+        a += x(i, 0) * hy(i, 0);
+        b += y(i, 0) * hx(i, 0);
+        q += x(i, 0) * hx(i, 0);
+    }
+    CHECK(std::abs(a - b) <= 1e-10 * std::abs(b));
+    CHECK(q >= 0.0);
+    const long before = o.diffusion->pde_solves();
+    o.op->apply(x);
+    CHECK(o.diffusion->pde_solves() - before == 6);
+    bool threw = false;
+    try {
+        oracles::make_oracle("surface16");
+    } catch (const std::logic_error&) {
+        threw = true;
+    }
+    CHECK(threw);
+    // HARA on the device operator (the cfg3 pipeline at desk scale)
+    auto res = peel_construct(*o.op, o.default_block_tree(), PeelConfig{1e-6});
+    CHECK(estimate_relative_error(*o.op, res.matrix) <= 3e-6);
+}
