@@ -40,13 +40,16 @@ double ms_since(Clock::time_point t0) {
 // 3 absorb_panel, 4 transposed-pass bookkeeping, 5 local updates, 6 recompress,
 // 7 dense-leaf extraction
 double g_phase_ms[16];   // 8 orthogonalize, 9 truncation bases, 10 projection (inside recompress)
+// phase timers drain the stream only when enabled (h2b_hara_phase_sync): a
+// synchronisation per phase would otherwise stall the device at every phase end
+int g_phase_sync = 0;
 struct Phase {
     int id;
     cudaStream_t s;
     Clock::time_point t0;
     Phase(int i, cudaStream_t st) : id(i), s(st), t0(Clock::now()) {}
     ~Phase() {
-        cudaStreamSynchronize(s);
+        if (g_phase_sync) cudaStreamSynchronize(s);
         g_phase_ms[id] += ms_since(t0);
     }
 };
@@ -303,7 +306,6 @@ std::unique_ptr<H2Dev> orthogonalize(const H2Dev& h, cudaStream_t s) {
     bgemm(g2, s);
     copy_array(out->D, h.D, s);
     out->orthonormal = true;
-    H2B_CUDA(cudaStreamSynchronize(s));
     return out;
 }
 
@@ -661,7 +663,6 @@ struct PeelContext {
     const H2Dev* partial = nullptr;   // residual = op - partial (ResidualOperator, :203-222)
     DeviceArray<int> perm;
     Workspace ws;
-    double op_ms = 0;
     cudaStream_t s;
     int64_t n;
     unsigned long long panel_counter = 0;
@@ -670,12 +671,36 @@ struct PeelContext {
         perm.upload(int32_perm(ct));
     }
     // y = residual(x) or residual^T(x), user ordering
+    // operator time: bracketing events on the stream (summed once at the end of
+    // the build), so timing the black box costs no synchronisation
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> op_events;
+    ~PeelContext() {
+        for (auto& e : op_events) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    }
+    double op_device_ms() {
+        double t = 0;
+        for (auto& e : op_events) {
+            float ms = 0;
+            H2B_CUDA(cudaEventSynchronize(e.second));
+            H2B_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+            t += ms;
+        }
+        return t;
+    }
     void residual(bool transpose, int64_t b, const double* x, double* y) {
         const auto t0 = Clock::now();
+        cudaEvent_t e0, e1;
+        H2B_CUDA(cudaEventCreate(&e0));
+        H2B_CUDA(cudaEventCreate(&e1));
+        op_events.emplace_back(e0, e1);
+        H2B_CUDA(cudaEventRecord(e0, s));
         if (transpose) op.apply_transpose(b, x, y, s);
         else op.apply(b, x, y, s);
-        H2B_CUDA(cudaStreamSynchronize(s));
-        op_ms += ms_since(t0);
+        H2B_CUDA(cudaEventRecord(e1, s));
+        if (g_phase_sync) H2B_CUDA(cudaStreamSynchronize(s));
         g_phase_ms[1] += ms_since(t0);
         if (partial) {
             Phase ph(2, s);
@@ -741,7 +766,6 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
             philox_fill_kernel<<<dim3(unsigned(std::max<int64_t>(bx, 1)), unsigned(segs.size())), 256, 0, s>>>(
                 dsegs.data(), int(segs.size()), panel, n, om.data(), cfg.seed, ctx.panel_counter++);
             H2B_LAUNCH();
-            H2B_CUDA(cudaStreamSynchronize(s));
         }
         la::permute_rows(om.data(), n, omu.data(), n, ctx.perm.data(), n, panel, true, s);
         delete ph_rng;
@@ -899,7 +923,6 @@ PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, 
             if (!ups.empty()) {
                 Phase ph(5, s);
                 partial = apply_local_updates(*partial, ups, s);
-                H2B_CUDA(cudaStreamSynchronize(s));
             }
         };
         group(pairs);
@@ -941,14 +964,13 @@ PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, 
             add.push_back(CopyDesc{yi.data() + ct.begin[size_t(r)], Dp(*partial, i), sz, sz, int(n), sz, sym ? 4 : 3});
         }
         bcopy(add, s);
-        H2B_CUDA(cudaStreamSynchronize(s));
     }
     stats.add_level({ct.depth + 1, int64_t(ct.leaves.size()), 0, op.columns_applied() - before});
     PeelResult res;
     res.matrix = recompress(*partial, cfg.eps, s);
     res.stats = std::move(stats);
     H2B_CUDA(cudaStreamSynchronize(s));
-    res.times.op_ms = ctx.op_ms;
+    res.times.op_ms = ctx.op_device_ms();
     res.times.total_ms = ms_since(t_start);
     return res;
 }
@@ -972,6 +994,12 @@ double estimate_relative_error(DevOperator& op, const H2Dev& h, double op_norm, 
 }  // namespace h2b
 
 // diagnostic hook (not part of the public ABI): per-phase host wall time of the last peel_construct
+// diagnostics: 1 = drain the stream at every phase end so the phase timers are
+// device-accurate (slower builds); 0 (default) = no timing synchronisation
+extern "C" int h2b_hara_phase_sync(int on) {
+    h2b::g_phase_sync = on;
+    return 0;
+}
 extern "C" int h2b_hara_phase_ms(double* out, int n) {
     for (int i = 0; i < n && i < 16; ++i) out[i] = h2b::g_phase_ms[i];
     return 0;
