@@ -149,7 +149,6 @@ void diag_apply(H2Dev& h, double value, int add, cudaStream_t s) {
     dm.upload(m, s);
     diag_set_kernel<<<unsigned(off.size()), 128, 0, s>>>(doff.data(), dm.data(), value, h.D.data(), add);
     H2B_LAUNCH();
-    H2B_CUDA(cudaStreamSynchronize(s));
 }
 
 // hgemv of one matrix with its own workspace (samplers own one per matrix)
@@ -419,7 +418,6 @@ std::unique_ptr<H2Dev> desymmetrized(const H2Dev& h, cudaStream_t s) {   // h2_m
     }
     la::bcopy(cps, s);
     out->orthonormal = h.orthonormal;
-    H2B_CUDA(cudaStreamSynchronize(s));
     return out;
 }
 
@@ -455,7 +453,6 @@ std::unique_ptr<H2Dev> low_rank_update(const H2Dev& h, const double* X, const do
     }
     const int root = ct.levels[0][0];
     auto upd = apply_local_updates(*g, {LocalUpdate{root, root, k, xi.data(), n, yp, n}}, s);
-    H2B_CUDA(cudaStreamSynchronize(s));
     return recompress(*upd, eps, s);
 }
 
