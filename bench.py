@@ -247,7 +247,7 @@ def run_b200(args, cfg, world, rank, local, dist):
     pts = grid_points(cfg["grid"])
     n = pts.shape[0]
     t0 = time.perf_counter()
-    ct = build_cluster_tree(pts, cfg["leaf"])
+    ct = build_cluster_tree(pts, cfg["leaf"], device=True)   # the same tree as the host builder, on the B200
     bt = build_block_tree(ct, ct, 1.0)
     t_tree = time.perf_counter() - t0
     t0 = time.perf_counter()

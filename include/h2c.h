@@ -47,6 +47,10 @@ const char* h2c_version(void);
  *      (cluster_tree.hpp:31-47, build_cluster_tree :186-188) ------------- */
 int h2c_cluster_tree_create(const double* coords /* n x dim, col-major */, int64_t n, int dim, int64_t leaf_size,
                             h2c_cluster_tree* out);
+/* the same tree built on the device: bitwise-identical nodes, boxes and
+ * permutation; coords on the host */
+int h2c_cluster_tree_create_device(const double* coords, int64_t n, int dim, int64_t leaf_size, void* stream,
+                                   h2c_cluster_tree* out);
 void h2c_cluster_tree_destroy(h2c_cluster_tree t);
 /* n(), dim(), depth(), num_nodes(), leaves().size()  (cluster_tree.hpp:49-58) */
 int h2c_cluster_tree_info(h2c_cluster_tree t, int64_t* n, int* dim, int* depth, int* num_nodes, int* num_leaves);

@@ -57,6 +57,7 @@ def _sig(name, res, *args):
 _sig("h2c_last_error", C.c_char_p)
 _sig("h2c_version", C.c_char_p)
 _sig("h2c_cluster_tree_create", i32, vp, i64, i32, i64, P(H))
+_sig("h2c_cluster_tree_create_device", i32, vp, i64, i32, i64, vp, P(H))
 _sig("h2c_cluster_tree_destroy", None, H)
 _sig("h2c_cluster_tree_info", i32, H, P(i64), P(i32), P(i32), P(i32), P(i32))
 _sig("h2c_cluster_tree_nodes", i32, H, vp, vp, vp, vp, vp, vp, vp, vp)

@@ -99,6 +99,15 @@ int h2c_cluster_tree_create(const double* coords, int64_t n, int dim, int64_t le
         *out = new h2c_cluster_tree_s{std::move(t)};
     });
 }
+int h2c_cluster_tree_create_device(const double* coords, int64_t n, int dim, int64_t leaf_size, void* stream,
+                                   h2c_cluster_tree* out) {
+    return guard([&] {
+        need(out != nullptr, "null output handle");
+        need(coords != nullptr || n == 0, "null coordinates");
+        auto t = h2b::build_cluster_tree_device(coords, n, dim, leaf_size, static_cast<cudaStream_t>(stream));
+        *out = new h2c_cluster_tree_s{std::move(t)};
+    });
+}
 void h2c_cluster_tree_destroy(h2c_cluster_tree t) { delete t; }
 
 int h2c_cluster_tree_info(h2c_cluster_tree t, int64_t* n, int* dim, int* depth, int* num_nodes, int* num_leaves) {

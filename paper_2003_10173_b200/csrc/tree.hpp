@@ -10,6 +10,8 @@
 // threads, and an explicit-stack block-tree traversal.
 #include <array>
 #include <cstdint>
+#include <cuda_runtime.h>
+
 #include <memory>
 #include <vector>
 
@@ -39,6 +41,9 @@ struct ClusterTree {
 
 // coords: n x dim column-major (user ordering)
 std::shared_ptr<ClusterTree> build_cluster_tree(const double* coords, int64_t n, int dim, int64_t leaf_size);
+// the same tree built on the device (tree_dev.cu); coords on the host
+std::shared_ptr<ClusterTree> build_cluster_tree_device(const double* coords, int64_t n, int dim, int64_t leaf_size,
+                                                       cudaStream_t s);
 
 enum BlockTag : int { kInterior = 0, kAdmissible = 1, kDense = 2 };
 

@@ -35,9 +35,10 @@ def _f64(a):
 
 
 class ClusterTree:
-    """KD cluster tree (cluster_tree.hpp:18-188); built on the host in C++."""
+    """KD cluster tree (cluster_tree.hpp:18-188); built in C++ on the host, or level by level on
+    the device (device=True; the same tree bit for bit)."""
 
-    def __init__(self, points, leaf_size):
+    def __init__(self, points, leaf_size, device=False):
         pts = np.asarray(points, dtype=np.float64)
         if pts.ndim == 1:
             pts = pts[:, None]
@@ -46,7 +47,11 @@ class ClusterTree:
         n, d = pts.shape
         coords = np.asfortranarray(pts)
         h = H()
-        check(lib.h2c_cluster_tree_create(coords.ctypes.data_as(C.c_void_p), n, d, int(leaf_size), C.byref(h)))
+        if device:
+            check(lib.h2c_cluster_tree_create_device(coords.ctypes.data_as(C.c_void_p), n, d, int(leaf_size), None,
+                                                     C.byref(h)))
+        else:
+            check(lib.h2c_cluster_tree_create(coords.ctypes.data_as(C.c_void_p), n, d, int(leaf_size), C.byref(h)))
         self._load(h, leaf_size)
 
     @classmethod
@@ -107,8 +112,9 @@ class ClusterTree:
         return out
 
 
-def build_cluster_tree(points, leaf_size):
-    return ClusterTree(points, leaf_size)
+def build_cluster_tree(points, leaf_size, device=False):
+    """build_cluster_tree (cluster_tree.hpp:186-188); device=True builds it on the B200."""
+    return ClusterTree(points, leaf_size, device)
 
 
 class BlockTree:
