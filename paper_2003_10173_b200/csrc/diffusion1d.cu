@@ -120,9 +120,55 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
         if (prev) bulk_g2s(tile, a.Wp + r0 * B, wbytes, &bar);
     }
     __syncthreads();
+    // carries of the CTA's chunks and of its two neighbour chunks, [chunk + 1][col]
+    double* ys = cft + size_t(cpb) * kL * kCoef;
+    double* xs = ys + size_t(cpb + 2) * B;
+    double* edge = xs + size_t(cpb + 2) * B;   // [2][B]: x at rows r0 - 1 and r0 + nrows
+    if (prev) {
+        for (int e = threadIdx.x; e < (nch + 2) * B; e += blockDim.x) {
+            const int col = e / (nch + 2), q = e - col * (nch + 2);   // chunk fastest: contiguous per column
+            const int64_t ch = ch0 - 1 + q;
+            const bool ok = ch >= 0 && ch < a.P;
+            ys[q * B + col] = ok ? a.Yin[col * a.P + ch] : 0.0;
+            xs[q * B + col] = ok ? a.Xin[col * a.P + ch] : 0.0;
+        }
+    }
     mbar_wait(&bar, 0);
+    __syncthreads();
     const int lc = threadIdx.x / B;
     const int col = threadIdx.x - lc * B;
+    // the neighbours' edge rows (outside the tile), finished from their carry form
+    for (int e = threadIdx.x; prev && e < 2 * B; e += blockDim.x) {
+        const int side = e / B, c = e - side * B;
+        const int64_t row = side == 0 ? r0 - 1 : r0 + nrows;
+        double v = 0.0;
+        if (row >= 0 && row < a.P * kL) {
+            const double* cf = a.coef + row * kCoef;
+            const int q = side == 0 ? 0 : nch + 1;
+            v = fma(cf[kHb], xs[q * B + c], fma(cf[kWg], ys[q * B + c], a.Wp[row * B + c]));
+        }
+        edge[side * B + c] = v;
+    }
+    double xm = 0.0, xe = 0.0;
+    if (lc < nch) {   // x_j from its carry form, in place
+        double* tcol = tile + size_t(lc) * kL * B + col;
+        const double* cf = cft + size_t(lc) * kL * kCoef;
+        if (prev) {
+            const double yc = ys[(lc + 1) * B + col], xc = xs[(lc + 1) * B + col];
+#pragma unroll 8
+            for (int i = 0; i < kL; ++i)
+                tcol[i * B] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, tcol[i * B]));
+        } else {
+#pragma unroll 8
+            for (int i = 0; i < kL; ++i) tcol[i * B] = 0.0;
+        }
+    }
+    __syncthreads();
+    if (lc < nch) {   // the neighbouring rows' x_j, before anyone overwrites its rows
+        xm = lc > 0 ? tile[(size_t(lc) * kL - 1) * B + col] : (prev ? edge[col] : 0.0);
+        xe = lc + 1 < nch ? tile[(size_t(lc) + 1) * kL * B + col] : (prev ? edge[B + col] : 0.0);
+    }
+    __syncthreads();
     if (lc < nch) {
         const int64_t ch = ch0 + lc;
         const int64_t s0 = ch * kL;
@@ -131,15 +177,7 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
         double* tcol = tile + size_t(lc) * kL * B + col;   // tcol[i * B] = row s0 + i
         const double* cf = cft + size_t(lc) * kL * kCoef;  // cf[i * kCoef + field]
         const int64_t k0 = s0 - a.row0;                    // physical node of the chunk's first row
-        double xm = 0.0, xe = 0.0;
-        if (prev) {   // x_j from its carry form, in place; the neighbours' edge values
-            const double yc = a.Yin[col * a.P + ch], xc = a.Xin[col * a.P + ch];
-            if (ch > 0) xm = carry_x(a.coef, a.Wp, a.Yin, a.Xin, a.P, B, col, s0 - 1);
-            if (ch + 1 < a.P) xe = carry_x(a.coef, a.Wp, a.Yin, a.Xin, a.P, B, col, s0 + kL);
-#pragma unroll 8
-            for (int i = 0; i < kL; ++i)
-                tcol[i * B] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, tcol[i * B]));
-            // consumers of x_j (loads first, then the read-modify-writes)
+        if (prev) {   // consumers of x_j (loads first, then the read-modify-writes)
             if (MODE == 0 && a.Uout) {
 #pragma unroll 8
                 for (int i = 0; i < kL; ++i)
@@ -162,9 +200,6 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
                     }
                 }
             }
-        } else {
-#pragma unroll 8
-            for (int i = 0; i < kL; ++i) tcol[i * B] = 0.0;
         }
         bool force = false;   // a point source / receiver row inside this chunk
         if (MODE == 0) {
@@ -458,7 +493,7 @@ struct Marcher {
         aggB.resize(size_t(nseg) * B * 2, st);
         ca.nseg = nseg;
         cpb = std::max(1, std::min(g_cpb_max, 256 / B));
-        smem = size_t(cpb) * kL * (B + kCoef) * sizeof(double);
+        smem = (size_t(cpb) * kL * (B + kCoef) + 2 * size_t(cpb + 2) * B + 2 * size_t(B)) * sizeof(double);
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
