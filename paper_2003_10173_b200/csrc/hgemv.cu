@@ -760,6 +760,12 @@ struct LaunchDesc {
     int item_begin = 0, item_end = 0;   // blocks / units of kinds 1-4
 };
 
+// entry order inside a task (L2 reuse of the symmetric partner read): 0 = block-tree
+// order, 1 = by partner distance |b_unit - own unit| (then b_unit). Task order:
+// g_task_order 0 = longest first (stable), 1 = tree order
+int g_entry_order = 1;
+int g_task_order = 0;
+
 struct HgemvPlan {
     uint64_t id = 0;   // unique per plan (graph cache key)
     std::vector<LaunchDesc> launches;
@@ -850,7 +856,7 @@ struct PlanBuilder {
         }
         // longest tasks first (stable: equal-cost tasks keep tree order for L2 locality)
         // so the last wave is made of short tasks; counting sort on the chunk count
-        {
+        if (g_task_order == 0) {
             const int t0 = ld.task_begin, t1 = int(tasks.size());
             int maxs = 0;
             for (int i = t0; i < t1; ++i) maxs = std::max(maxs, tasks[size_t(i)].nsteps);
@@ -914,6 +920,18 @@ std::shared_ptr<const DeviceArray<int>> tree_perm(const std::shared_ptr<const Cl
     d->upload(p32);
     cache[t.get()] = {t, d};
     return d;
+}
+
+
+// sort the entries of pool[e0, e1) whose B source is `src` by their distance to `own`
+void order_entries(std::vector<SegEntry>& pool, int e0, int e1, int src, int64_t own) {
+    if (g_entry_order == 0) return;
+    int a = e0;
+    while (a < e1 && pool[size_t(a)].src != src) ++a;
+    std::stable_sort(pool.begin() + a, pool.begin() + e1, [own](const SegEntry& x, const SegEntry& y) {
+        const int64_t dx = std::llabs(x.b_unit - own), dy = std::llabs(y.b_unit - own);
+        return dx != dy ? dx < dy : x.b_unit < y.b_unit;
+    });
 }
 
 double g_plan_sync_ms = 0;   // of which: the closing device synchronisation (diagnostics)
@@ -1086,6 +1104,8 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
                 by_target.add(c, make_entry(S, kr, kr, true, 1, cu[size_t(r)], kr));
             }
         }
+        for (int v = 0; v < nn; ++v)
+            order_entries(by_target.pool, by_target.start[size_t(v)], by_target.start[size_t(v) + 1], 1, cu[size_t(v)]);
         outs.clear();
         pb.phase = 1;
         for (int v = 0; v < nn; ++v) {
@@ -1174,6 +1194,8 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
                 by_leaf.add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
             }
         }
+        for (int t : ct.leaves)
+            order_entries(by_leaf.pool, by_leaf.start[size_t(t)], by_leaf.start[size_t(t) + 1], 0, ct.begin[size_t(t)]);
         outs.clear();
         for (int t : ct.leaves) {
             if (!own(t)) continue;
@@ -1327,6 +1349,9 @@ void launch_vec_mode(const SegArgs& a, int ntasks, int64_t b, int mode, cudaStre
     else launch_one<MT, NB, WM, WN, STAGES, KC, true, kModeY>(a, ntasks, b, s);
 }
 
+// vector columns per CTA tile of the segmented GEMM (grid.y = ceil(b / tile_nb))
+int tile_nb(int64_t b) { return b >= 64 ? 64 : (b >= 32 ? 32 : (b > 8 ? 16 : 8)); }
+
 void dispatch(const SegArgs& a, int ntasks, int64_t b, int mt, bool vec, int mode, cudaStream_t s) {
     if (b == 32 && vec && g_tune[2] > 0) {
         switch (g_tune[2]) {
@@ -1344,7 +1369,7 @@ void dispatch(const SegArgs& a, int ntasks, int64_t b, int mt, bool vec, int mod
                 return launch_ws_mode<32, 2, 2, 2>(a, ntasks, mode, s);
         }
     }
-    const int nb = b >= 64 ? 64 : (b >= 32 ? 32 : (b > 8 ? 16 : 8));
+    const int nb = tile_nb(b);
     if (nb == 64) {
         // 64 vectors in one tile: every stored block is streamed once per orientation
         if (mt == 64) launch_mode<64, 64, 4, 1>(a, ntasks, b, vec, mode, s);
@@ -1790,6 +1815,14 @@ int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
 extern "C" int h2b_tune(int which, int value) {
     if (which == 4) {   // symmetric few-vector path threshold (0 = off)
         h2b::g_small_b = value;
+        return 0;
+    }
+    if (which == 5) {   // entry order within a task (plans built afterwards)
+        h2b::g_entry_order = value;
+        return 0;
+    }
+    if (which == 6) {   // task order within a launch (plans built afterwards)
+        h2b::g_task_order = value;
         return 0;
     }
     if (which < 0 || which > 3) return -1;
