@@ -194,9 +194,13 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    int pe = tk.e_begin, pk = 0;   // producer cursor (entry, k offset)
-    auto issue = [&](int stage) {
-        const SegEntry e = args.entries[pe];
+    // producer cursor (entry, k offset); the next entry's descriptor is fetched as
+    // soon as the current one is consumed, so its load overlaps this chunk's DMMAs
+    int pe = tk.e_begin, pk = 0;
+    SegEntry e{};
+    if (pe < tk.e_end) e = args.entries[pe];
+    // issue one K chunk into `stage`; returns its metadata (k4 steps | trans << 8)
+    auto issue = [&](int stage) -> int {
         double* at = smem + stage * ST_SZ;
         double* bt = at + A_SZ;
         const int krem = min(KC, e.k - pk);
@@ -204,41 +208,43 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
         else load_kc<MT, KC, NT, VEC>(at, e.A + pk + int64_t(tk.row0) * e.lda, e.lda, krem, rows_here, tid);
         const double* sb = e.src == 0 ? args.src0 : (e.src == 1 ? args.src1 : args.src2);
         load_kc<NB, KC, NT, VEC>(bt, sb + e.b_unit * args.b + pk + int64_t(j0) * e.ldb, e.ldb, krem, ncols, tid);
+        const int meta = ((krem + 3) >> 2) | (e.trans << 8);
         pk += KC;
         if (pk >= e.k) {
             ++pe;
             pk = 0;
+            if (pe < tk.e_end) e = args.entries[pe];
         }
+        return meta;
     };
 
+    int qm[STAGES];   // metadata of the chunks in flight: qm[i] = chunk s + i
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) qm[s] = 0;
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nsteps) issue(s);
+        if (s < nsteps) qm[s] = issue(s);
         cp_async_commit();
     }
-    int ce = tk.e_begin, ck = 0;   // consumer cursor
     for (int s = 0; s < nsteps; ++s) {
         if constexpr (STAGES == 1) {
             // single buffer: the other CTAs resident on the SM hide this CTA's load latency
             __syncthreads();
-            issue(0);
+            qm[0] = issue(0);
             cp_async_commit();
             cp_async_wait<0>();
             __syncthreads();
         } else {
             cp_async_wait<STAGES - 2>();
             __syncthreads();
-            if (s + STAGES - 1 < nsteps) issue((s + STAGES - 1) % STAGES);
+            if (s + STAGES - 1 < nsteps) qm[STAGES - 1] = issue((s + STAGES - 1) % STAGES);
             cp_async_commit();
         }
-        const SegEntry& ec = args.entries[ce];
-        const bool trans = ec.trans;
-        const int ksteps = (min(KC, ec.k - ck) + 3) >> 2;
-        ck += KC;
-        if (ck >= ec.k) {
-            ++ce;
-            ck = 0;
-        }
+        const int meta = qm[0];
+#pragma unroll
+        for (int q = 0; q + 1 < STAGES; ++q) qm[q] = qm[q + 1];
+        const bool trans = meta >> 8;
+        const int ksteps = meta & 0xff;
         const double* at = smem + (s % STAGES) * ST_SZ;
         const double* bt = at + A_SZ;
         if (trans) chunk_mma<MT, KC, TM, TN, true>(at, bt, acc, offa_t, offb, ksteps);
@@ -252,6 +258,11 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
         const int m = (wm * TM + i) * 8 + g;
         if (m >= rows_here) continue;
         const int row = tk.row0 + m;
+        int64_t ur = 0;   // kModeY: user row of this internal row (loaded once per row)
+        if constexpr (MODE == kModeY) {
+            const int64_t ir = tk.out_unit + row;
+            ur = args.perm ? args.perm[ir] : ir;
+        }
 #pragma unroll
         for (int j = 0; j < TN; ++j)
 #pragma unroll
@@ -261,8 +272,6 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
                 const int64_t col = j0 + nn;
                 const double v = acc[i][j][h];
                 if constexpr (MODE == kModeY) {
-                    const int64_t ir = tk.out_unit + row;
-                    const int64_t ur = args.perm ? args.perm[ir] : ir;
                     double* p = args.out + ur + col * args.ldy;
                     *p = args.beta == 0.0 ? args.alpha * v : args.alpha * v + args.beta * *p;
                 } else {
@@ -821,8 +830,6 @@ struct PlanBuilder {
         for (auto& p : outs) maxrows = std::max(maxrows, p.rows);
         ld.mt = maxrows > 32 ? 64 : 32;
         ld.task_begin = int(tasks.size());
-        entries.reserve(entries.size() + pool.size());
-        tasks.reserve(tasks.size() + outs.size());
         bool vec = true, ue = true;
         for (auto& p : outs) {
             if (p.rows <= 0) continue;
@@ -928,7 +935,8 @@ void order_entries(std::vector<SegEntry>& pool, int e0, int e1, int src, int64_t
     if (g_entry_order == 0) return;
     int a = e0;
     while (a < e1 && pool[size_t(a)].src != src) ++a;
-    std::stable_sort(pool.begin() + a, pool.begin() + e1, [own](const SegEntry& x, const SegEntry& y) {
+    // partners are distinct within a task, so the (distance, b_unit) key is a strict order
+    std::sort(pool.begin() + a, pool.begin() + e1, [own](const SegEntry& x, const SegEntry& y) {
         const int64_t dx = std::llabs(x.b_unit - own), dy = std::llabs(y.b_unit - own);
         return dx != dy ? dx < dy : x.b_unit < y.b_unit;
     });
