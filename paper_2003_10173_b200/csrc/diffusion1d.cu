@@ -4,11 +4,15 @@
 //   coef_   [padded state row][6]   mdiag (A- diagonal), mult (L), wg, hb (carry weights), rdfac, beta (U)
 //   chunk_  [chunk][3]              G (forward carry gain), WG, HB (backward carry weights at the chunk start)
 //   u_      [step][k][source]       cached state at the physical nodes
-//   W       [padded state row][col] chunk-local solutions, columns = source-major (s * bb + j)
+//   W       [chunk][col][kLP] chunk-local solutions (a chunk's 32 rows contiguous per column,
+//           column stride kLP = 33, chunk stride wchunk(B) = B * 33 rounded up to even),
+//           columns = source-major (s * bb + j)
 //   zend/wstart/Yin/Xin [col][chunk] chunk aggregates and exact boundary carries
 // A state value is never stored explicitly: x_i = W_i + wg_i Yin(c_i) + hb_i Xin(c_i).
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 
 #include "diffusion1d.hpp"
 
@@ -21,6 +25,13 @@ constexpr int kCoef = 6;          // per row, as three double2: (mdiag, mult) (w
 int g_max_batch = 64;             // operator columns per internal batch (h2b_diff1d_tune)
 int g_cpb_max = 16;               // chunks per step CTA cap (h2b_diff1d_tune)
 enum { kMdiag = 0, kMult, kWg, kHb, kRdfac, kBeta };
+constexpr int kLP = kL + 1;       // column stride of a chunk in W: one padding double keeps the
+                                  // per-thread row walks of a warp bank-conflict free
+// doubles per chunk of W (even, so every chunk starts 16-byte aligned for the bulk copies)
+__host__ __device__ __forceinline__ int64_t wchunk(int B) { return (int64_t(B) * kLP + 1) & ~int64_t(1); }
+__device__ __forceinline__ int64_t wpos(int64_t row, int col, int B) {
+    return (row / kL) * wchunk(B) + int64_t(col) * kLP + (row % kL);
+}
 
 struct StepArgs {
     const double* __restrict__ coef;
@@ -51,7 +62,7 @@ __device__ __forceinline__ double carry_x(const double* __restrict__ coef, const
                                           const double* Xin, int64_t P, int B, int col, int64_t row) {
     const int64_t c = row / kL;
     const double* cf = coef + row * kCoef;
-    return fma(cf[kHb], Xin[col * P + c], fma(cf[kWg], Yin[col * P + c], W[row * B + col]));
+    return fma(cf[kHb], Xin[col * P + c], fma(cf[kWg], Yin[col * P + c], W[wpos(row, col, B)]));
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -108,16 +119,17 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
     const int nch = int(a.P - ch0 < cpb ? a.P - ch0 : cpb);
     const int64_t r0 = ch0 * kL;
     const int nrows = nch * kL;
-    double* tile = smem;                              // [cpb * kL][B]
-    double* cft = tile + size_t(cpb) * kL * B;        // [cpb * kL][kCoef]
+    const int64_t csz = wchunk(B);
+    double* tile = smem;                              // [cpb][B][kLP] (chunk stride csz)
+    double* cft = tile + size_t(cpb) * csz;           // [cpb * kL][kCoef]
     const bool prev = a.Wp != nullptr;
     if (threadIdx.x == 0) {
         mbar_init(&bar);
         const uint32_t cbytes = uint32_t(nrows) * kCoef * sizeof(double);
-        const uint32_t wbytes = prev ? uint32_t(nrows) * B * sizeof(double) : 0u;
+        const uint32_t wbytes = prev ? uint32_t(nch * csz) * sizeof(double) : 0u;
         mbar_expect_tx(&bar, cbytes + wbytes);
         bulk_g2s(cft, a.coef + r0 * kCoef, cbytes, &bar);
-        if (prev) bulk_g2s(tile, a.Wp + r0 * B, wbytes, &bar);
+        if (prev) bulk_g2s(tile, a.Wp + ch0 * csz, wbytes, &bar);
     }
     __syncthreads();
     // carries of the CTA's chunks and of its two neighbour chunks, [chunk + 1][col]
@@ -133,10 +145,10 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
             xs[q * B + col] = ok ? a.Xin[col * a.P + ch] : 0.0;
         }
     }
-    mbar_wait(&bar, 0);
-    __syncthreads();
     const int lc = threadIdx.x / B;
     const int col = threadIdx.x - lc * B;
+    mbar_wait(&bar, 0);
+    __syncthreads();
     // the neighbours' edge rows (outside the tile), finished from their carry form
     for (int e = threadIdx.x; prev && e < 2 * B; e += blockDim.x) {
         const int side = e / B, c = e - side * B;
@@ -145,58 +157,72 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
         if (row >= 0 && row < a.P * kL) {
             const double* cf = a.coef + row * kCoef;
             const int q = side == 0 ? 0 : nch + 1;
-            v = fma(cf[kHb], xs[q * B + c], fma(cf[kWg], ys[q * B + c], a.Wp[row * B + c]));
+            v = fma(cf[kHb], xs[q * B + c], fma(cf[kWg], ys[q * B + c], a.Wp[wpos(row, c, B)]));
         }
         edge[side * B + c] = v;
     }
+    // thread = (chunk lc, column col): its 32 rows are contiguous, tcol[i] = row s0 + i
+    double* tcol = tile + size_t(lc) * csz + size_t(col) * kLP;
+    const double* cf = cft + size_t(lc) * kL * kCoef;   // cf[i * kCoef + field]
     double xm = 0.0, xe = 0.0;
     if (lc < nch) {   // x_j from its carry form, in place
-        double* tcol = tile + size_t(lc) * kL * B + col;
-        const double* cf = cft + size_t(lc) * kL * kCoef;
         if (prev) {
             const double yc = ys[(lc + 1) * B + col], xc = xs[(lc + 1) * B + col];
-#pragma unroll 8
-            for (int i = 0; i < kL; ++i)
-                tcol[i * B] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, tcol[i * B]));
+#pragma unroll
+            for (int i = 0; i < kL; ++i) tcol[i] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, tcol[i]));
         } else {
-#pragma unroll 8
-            for (int i = 0; i < kL; ++i) tcol[i * B] = 0.0;
+#pragma unroll
+            for (int i = 0; i < kL; ++i) tcol[i] = 0.0;
         }
     }
     __syncthreads();
     if (lc < nch) {   // the neighbouring rows' x_j, before anyone overwrites its rows
-        xm = lc > 0 ? tile[(size_t(lc) * kL - 1) * B + col] : (prev ? edge[col] : 0.0);
-        xe = lc + 1 < nch ? tile[(size_t(lc) + 1) * kL * B + col] : (prev ? edge[B + col] : 0.0);
+        xm = lc > 0 ? tcol[-csz + kL - 1] : (prev ? edge[col] : 0.0);
+        xe = lc + 1 < nch ? tcol[csz] : (prev ? edge[B + col] : 0.0);
     }
     __syncthreads();
     if (lc < nch) {
         const int64_t ch = ch0 + lc;
         const int64_t s0 = ch * kL;
         const int src = col / a.bb;
-        const int jc = col - src * a.bb;
-        double* tcol = tile + size_t(lc) * kL * B + col;   // tcol[i * B] = row s0 + i
-        const double* cf = cft + size_t(lc) * kL * kCoef;  // cf[i * kCoef + field]
-        const int64_t k0 = s0 - a.row0;                    // physical node of the chunk's first row
+        const int64_t k0 = s0 - a.row0;                 // physical node of the chunk's first row
+        const bool phys = k0 >= 0 && k0 + kL <= a.n;    // every row of the chunk is a physical node
         if (prev) {   // consumers of x_j (loads first, then the read-modify-writes)
             if (MODE == 0 && a.Uout) {
 #pragma unroll 8
                 for (int i = 0; i < kL; ++i)
-                    if (k0 + i >= 0 && k0 + i < a.n) a.Uout[(k0 + i) * a.S + col] = tcol[i * B];
+                    if (k0 + i >= 0 && k0 + i < a.n) a.Uout[(k0 + i) * a.S + col] = tcol[i];
             } else if (MODE == 2) {   // acc_q += q (u(j+1) - u(j)), diffusion1d.hpp:329-332
+                if (phys) {
+                    const double* dp = a.du + k0 * a.S + src;
+                    double* ap = a.acc + k0 * B + col;
 #pragma unroll 1
-                for (int i0 = 0; i0 < kL; i0 += 8) {   // eight loads in flight, then the stores
-                    double d[8], ac[8];
+                    for (int i0 = 0; i0 < kL; i0 += 8) {   // eight loads in flight, then the stores
+                        double d[8], ac[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int64_t k = k0 + i0 + i;
-                        const bool ph = k >= 0 && k < a.n;
-                        d[i] = ph ? __ldg(a.du + k * a.S + src) : 0.0;
-                        ac[i] = ph ? a.acc[k * B + col] : 0.0;
+                        for (int i = 0; i < 8; ++i) {
+                            d[i] = __ldg(dp + (i0 + i) * a.S);
+                            ac[i] = ap[(i0 + i) * B];
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) ap[(i0 + i) * B] = fma(tcol[i0 + i], d[i], ac[i]);
                     }
+                } else {
+#pragma unroll 1
+                    for (int i0 = 0; i0 < kL; i0 += 8) {
+                        double d[8], ac[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int64_t k = k0 + i0 + i;
-                        if (k >= 0 && k < a.n) a.acc[k * B + col] = ac[i] + tcol[(i0 + i) * B] * d[i];
+                        for (int i = 0; i < 8; ++i) {
+                            const int64_t k = k0 + i0 + i;
+                            const bool ph = k >= 0 && k < a.n;
+                            d[i] = ph ? __ldg(a.du + k * a.S + src) : 0.0;
+                            ac[i] = ph ? a.acc[k * B + col] : 0.0;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int64_t k = k0 + i0 + i;
+                            if (k >= 0 && k < a.n) a.acc[k * B + col] = fma(tcol[i0 + i], d[i], ac[i]);
+                        }
                     }
                 }
             }
@@ -208,43 +234,77 @@ __global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
             for (int q = 0; q < a.nfrow; ++q) force |= (a.frow[q] - s0) >= 0 && (a.frow[q] - s0) < kL;
         }
         double zp = 0.0, xi = tcol[0];
+        if (MODE != 0 && !force && s0 >= 1 && s0 + kL < a.ns && (MODE != 1 || phys)) {
+            // interior chunk: both A- off-diagonals present on every row, no point forcing
+            const double mo = a.moff;
+            if constexpr (MODE == 1) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
+                const int jc = col - src * a.bb;
+                const double* np = a.nu + k0 * a.bb + jc;
+                const double* dp = a.du + k0 * a.S + src;
+                const double c = a.c;
 #pragma unroll 8
-        for (int i = 0; i < kL; ++i) {
-            const int64_t row = s0 + i;
-            const double xn = i + 1 < kL ? tcol[(i + 1) * B] : xe;
-            const double cu = row + 1 < a.ns ? a.moff : 0.0;
-            const double cl = row >= 1 && row < a.ns ? a.moff : 0.0;
-            double r = fma(cl, xm, fma(cu, xn, cf[i * kCoef + kMdiag] * xi));
-            const int64_t k = row - a.row0;
-            if (MODE == 1 && k >= 0 && k < a.n)   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
-                r -= a.c * (__ldg(a.nu + k * a.bb + jc) * __ldg(a.du + k * a.S + src));
-            if (force) {
-                if (MODE == 0) {   // point source of the column (:245-246)
-                    if (a.frow[col] == row) r += a.fval;
-                } else {   // receiver residual sources (:325-326)
-                    for (int q = 0; q < a.nfrow; ++q)
-                        if (a.frow[q] == row) r -= a.fval * __ldg(a.vr + q * B + col);
+                for (int i = 0; i < kL; ++i) {
+                    const double xn = i + 1 < kL ? tcol[i + 1] : xe;
+                    // same operation order as the general path (apply_minus, then the forcing)
+                    const double r = fma(mo, xm, fma(mo, xn, cf[i * kCoef + kMdiag] * xi)) -
+                                     c * (__ldg(np + i * a.bb) * __ldg(dp + i * a.S));
+                    zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
+                    tcol[i] = zp;
+                    xm = xi;
+                    xi = xn;
+                }
+            } else {
+#pragma unroll 8
+                for (int i = 0; i < kL; ++i) {
+                    const double xn = i + 1 < kL ? tcol[i + 1] : xe;
+                    const double r = fma(mo, xm, fma(mo, xn, cf[i * kCoef + kMdiag] * xi));
+                    zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
+                    tcol[i] = zp;
+                    xm = xi;
+                    xi = xn;
                 }
             }
-            // local forward elimination y_i = r_i - m_i y_{i-1} (zero carry-in)
-            zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
-            tcol[i * B] = zp;   // row i's x_j already lives in the window
-            xm = xi;
-            xi = xn;
+        } else {
+#pragma unroll 8
+            for (int i = 0; i < kL; ++i) {
+                const int64_t row = s0 + i;
+                const double xn = i + 1 < kL ? tcol[i + 1] : xe;
+                const double cu = row + 1 < a.ns ? a.moff : 0.0;
+                const double cl = row >= 1 && row < a.ns ? a.moff : 0.0;
+                double r = fma(cl, xm, fma(cu, xn, cf[i * kCoef + kMdiag] * xi));
+                const int64_t k = row - a.row0;
+                if (MODE == 1 && k >= 0 && k < a.n) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
+                    const int jc = col - src * a.bb;
+                    r -= a.c * (__ldg(a.nu + k * a.bb + jc) * __ldg(a.du + k * a.S + src));
+                }
+                if (force) {
+                    if (MODE == 0) {   // point source of the column (:245-246)
+                        if (a.frow[col] == row) r += a.fval;
+                    } else {   // receiver residual sources (:325-326)
+                        for (int q = 0; q < a.nfrow; ++q)
+                            if (a.frow[q] == row) r -= a.fval * __ldg(a.vr + q * B + col);
+                    }
+                }
+                // local forward elimination y_i = r_i - m_i y_{i-1} (zero carry-in)
+                zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
+                tcol[i] = zp;   // row i's x_j already lives in the window
+                xm = xi;
+                xi = xn;
+            }
         }
         a.zend[col * a.P + ch] = zp;
         // local back substitution x_i = y_i / d_i - beta_i x_{i+1} (zero carry-in)
         double w = zp * cf[(kL - 1) * kCoef + kRdfac];
-        tcol[(kL - 1) * B] = w;
-#pragma unroll 8
+        tcol[kL - 1] = w;
+#pragma unroll
         for (int i = kL - 2; i >= 0; --i) {
-            w = fma(-cf[i * kCoef + kBeta], w, cf[i * kCoef + kRdfac] * tcol[i * B]);
-            tcol[i * B] = w;
+            w = fma(-cf[i * kCoef + kBeta], w, cf[i * kCoef + kRdfac] * tcol[i]);
+            tcol[i] = w;
         }
         a.wstart[col * a.P + ch] = w;
     }
     __syncthreads();
-    if (threadIdx.x == 0) bulk_s2g(a.Wn + r0 * B, tile, uint32_t(nrows) * B * sizeof(double));
+    if (threadIdx.x == 0) bulk_s2g(a.Wn + ch0 * csz, tile, uint32_t(nch * csz) * sizeof(double));
 }
 
 struct Aff {   // v -> a v + b
@@ -492,15 +552,40 @@ struct Marcher {
         aggF.resize(size_t(nseg) * B * 2, st);
         aggB.resize(size_t(nseg) * B * 2, st);
         ca.nseg = nseg;
-        cpb = std::max(1, std::min(g_cpb_max, 256 / B));
-        smem = (size_t(cpb) * kL * (B + kCoef) + 2 * size_t(cpb + 2) * B + 2 * size_t(B)) * sizeof(double);
+        // chunks per CTA: the count that keeps the most (chunk, column) threads resident
+        // per SM under the shared-memory budget (ties: more chunks per CTA)
+        auto smem_for = [B](int q) {
+            return (size_t(q) * (wchunk(B) + kL * kCoef) + 2 * size_t(q + 2) * B + 2 * size_t(B)) * sizeof(double);
+        };
+        const int qmax = std::max(1, std::min(g_cpb_max, 256 / B));
+        static std::mutex mu;
+        static std::map<std::pair<int, int>, int> chosen;   // (B, cap) -> chunks per CTA
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = chosen.find({B, qmax});
+        if (it != chosen.end()) {
+            cpb = it->second;
+        } else {
+            int best = -1;
+            for (int q = 1; q <= qmax; ++q) {
+                const size_t sm = smem_for(q);
+                H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                int per_sm = 0;
+                H2B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cn_step_kernel<1>, q * B, sm));
+                if (per_sm * q * B >= best) {
+                    best = per_sm * q * B;
+                    cpb = q;
+                }
+            }
+            chosen[{B, qmax}] = cpb;
+        }
+        smem = smem_for(cpb);
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         ca.aggF = aggF.data();
         ca.aggB = aggB.data();
-        W[0].resize(size_t(P) * kL * B, st);
-        W[1].resize(size_t(P) * kL * B, st);
+        W[0].resize(size_t(P) * wchunk(B), st);
+        W[1].resize(size_t(P) * wchunk(B), st);
         a.coef = coef;
         a.P = P;
         a.B = B;
