@@ -346,7 +346,7 @@ __device__ Aff block_exscan(Aff v, bool rev, Aff* sm) {
     return pre;
 }
 
-constexpr int kSeg = 1024;   // chunks per carry-scan segment (= threads per block)
+constexpr int kSeg = 256;    // chunks per carry-scan segment (= threads per block)
 
 struct CarryArgs {
     const double* __restrict__ chunk;   // [P][3] G, WG, HB

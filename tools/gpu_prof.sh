@@ -14,4 +14,4 @@ ncu --set full --clock-control none --import-source on --kernel-name-base mangle
 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
     -k regex:"$KCOUP" -s $SKIP -c 1 -o gpurun_out/prof_coupling_${CFG}_$TAG $CMD > gpurun_out/ncu_full2_$TAG.log 2>&1
 echo "exit $?"
-tail -3 gpurun_out/plain_$TAG.log gpurun_out/ncu_full_$TAG.log gpurun_out/ncu_full2_$TAG.log
+tail -n 3 gpurun_out/plain_$TAG.log gpurun_out/ncu_full_$TAG.log gpurun_out/ncu_full2_$TAG.log

@@ -14,7 +14,7 @@ for c in cfg2 cfg2b1 cfg1 cfg4 cfg3 cfg3k cfg5; do
   echo "bench $c exit $?" >> gpurun_out/bench_${c}_$TAG.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_cfg2_ref_$TAG.json 2> gpurun_out/bench_cfg2_ref_$TAG.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench_cfg2_$TAG.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"seg_gemm|gather_blocked|sym_pass|csr_sum" -c 400 --csv --log-file gpurun_out/launches_bench_cfg2_$TAG.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench_$TAG.log 2>&1
 tail -n 2 gpurun_out/pytest_gpu_$TAG.txt gpurun_out/smoke_$TAG.txt
 for c in cfg2 cfg2b1 cfg1 cfg4 cfg3 cfg3k cfg5; do python -c "
