@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
     int qm[STAGES];   // metadata of the chunks in flight: qm[i] = chunk s + i
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) qm[s] = 0;
+    // programmatic dependent launch: everything above reads only the plan; the
+    // operands may come from the previous launch, so wait for it here (a no-op
+    // when the launch carries no programmatic dependency)
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nsteps) qm[s] = issue(s);
@@ -251,6 +255,8 @@ __global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
         else chunk_mma<MT, KC, TM, TN, false>(at, bt, acc, offa_n, offb, ksteps);
     }
     cp_async_wait<0>();
+    // the next launch may start its prologue once every CTA of this one is here
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     // epilogue
 #pragma unroll
@@ -774,6 +780,7 @@ struct LaunchDesc {
 // g_task_order 0 = longest first (stable), 1 = tree order
 int g_entry_order = 1;
 int g_task_order = 0;
+int g_pdl = 1;   // programmatic dependent launch of the segmented-GEMM launches
 
 struct HgemvPlan {
     uint64_t id = 0;   // unique per plan (graph cache key)
@@ -1305,7 +1312,21 @@ void launch_one(const SegArgs& a, int ntasks, int64_t b, cudaStream_t s) {
     }();
     (void)attr;
     dim3 grid(unsigned(ntasks), unsigned((b + NB - 1) / NB));
-    kern<<<grid, WM * WN * 32, smem, s>>>(a);
+    if (g_pdl) {   // overlap this launch's prologue with the previous kernel's tail
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(WM * WN * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        H2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    } else {
+        kern<<<grid, WM * WN * 32, smem, s>>>(a);
+    }
     H2B_LAUNCH();
 }
 
@@ -1831,6 +1852,10 @@ extern "C" int h2b_tune(int which, int value) {
     }
     if (which == 6) {   // task order within a launch (plans built afterwards)
         h2b::g_task_order = value;
+        return 0;
+    }
+    if (which == 7) {   // programmatic dependent launch on (1) / off (0)
+        h2b::g_pdl = value;
         return 0;
     }
     if (which < 0 || which > 3) return -1;
