@@ -4,9 +4,9 @@
 //   coef_   [padded state row][6]   mdiag (A- diagonal), mult (L), wg, hb (carry weights), rdfac, beta (U)
 //   chunk_  [chunk][3]              G (forward carry gain), WG, HB (backward carry weights at the chunk start)
 //   u_      [step][k][source]       cached state at the physical nodes
-//   W       [chunk][col][kLP] chunk-local solutions (a chunk's 32 rows contiguous per column,
-//           column stride kLP = 33, chunk stride wchunk(B) = B * 33 rounded up to even),
-//           columns = source-major (s * bb + j)
+//   W       [padded state row][col] chunk-local solutions, columns = source-major (s * bb + j);
+//           a step thread keeps its (chunk, column) rows in registers, and a warp's row
+//           accesses are contiguous runs over the columns
 //   zend/wstart/Yin/Xin [col][chunk] chunk aggregates and exact boundary carries
 // A state value is never stored explicitly: x_i = W_i + wg_i Yin(c_i) + hb_i Xin(c_i).
 #include <algorithm>
@@ -20,18 +20,22 @@ namespace h2b {
 
 namespace {
 
-constexpr int kL = 32;            // state rows per chunk (per thread)
+#ifndef STEP_MINB
+#define STEP_MINB 2
+#endif
+#ifndef STEP_KL
+#define STEP_KL 32
+#endif
+constexpr int kL = STEP_KL;
+#ifndef ACC_BATCH
+#define ACC_BATCH 8
+#endif
+constexpr int kAccBatch = ACC_BATCH;   // adjoint accumulator rows per load batch            // state rows per chunk (per thread)
 constexpr int kCoef = 6;          // per row, as three double2: (mdiag, mult) (wg, hb) (rdfac, beta)
 int g_max_batch = 64;             // operator columns per internal batch (h2b_diff1d_tune)
 int g_cpb_max = 16;               // chunks per step CTA cap (h2b_diff1d_tune)
 enum { kMdiag = 0, kMult, kWg, kHb, kRdfac, kBeta };
-constexpr int kLP = kL + 1;       // column stride of a chunk in W: one padding double keeps the
-                                  // per-thread row walks of a warp bank-conflict free
-// doubles per chunk of W (even, so every chunk starts 16-byte aligned for the bulk copies)
-__host__ __device__ __forceinline__ int64_t wchunk(int B) { return (int64_t(B) * kLP + 1) & ~int64_t(1); }
-__device__ __forceinline__ int64_t wpos(int64_t row, int col, int B) {
-    return (row / kL) * wchunk(B) + int64_t(col) * kLP + (row % kL);
-}
+__device__ __forceinline__ int64_t wpos(int64_t row, int col, int B) { return row * B + col; }
 
 struct StepArgs {
     const double* __restrict__ coef;
@@ -65,246 +69,169 @@ __device__ __forceinline__ double carry_x(const double* __restrict__ coef, const
     return fma(cf[kHb], Xin[col * P + c], fma(cf[kWg], Yin[col * P + c], W[wpos(row, col, B)]));
 }
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return uint32_t(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
-        "r"(phase)
-        : "memory");
-}
-// TMA 1D bulk copies (contiguous, 16-byte aligned, size a multiple of 16)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_addr(src)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-}
-
 // One Crank-Nicolson step for every (chunk, column): finish x_j from its
 // carry form, consume it (state store / adjoint accumulation), form the
 // right-hand side A- x_j + f_j (Stepper::apply_minus, diffusion1d.hpp:203-209,
 // and the forcing of :245-246, :302-303, :325-326), and solve the chunk locally
 // with zero boundary carries (TridiagSolver::solve_in_place, grid.hpp:67-73).
-// A CTA owns `cpb` consecutive chunks for all B columns: their W rows and row
-// coefficients are one contiguous range each, staged into shared memory by a
-// single TMA bulk copy; the eliminated values overwrite the tile in place and
-// the finished tile leaves with one bulk store. Thread = (chunk, column).
+// Thread = (chunk, column). The thread's 32 rows live in registers from the
+// load to the store, so every sweep is register arithmetic; a warp's loads and
+// stores of one row are contiguous runs over the columns. Shared memory holds
+// only the CTA's coefficient rows and the chunk-edge values the neighbouring
+// chunks' threads need (x at each chunk's first and last row).
 template <int MODE>
-__global__ void __launch_bounds__(256) cn_step_kernel(StepArgs a, int cpb) {
-    extern __shared__ __align__(128) double smem[];
-    __shared__ uint64_t bar;
+__global__ void __launch_bounds__(256, STEP_MINB) cn_step_kernel(StepArgs a, int cpb) {
+    extern __shared__ __align__(16) double smem[];
     const int B = a.B;
     const int64_t ch0 = int64_t(blockIdx.x) * cpb;
     const int nch = int(a.P - ch0 < cpb ? a.P - ch0 : cpb);
     const int64_t r0 = ch0 * kL;
-    const int nrows = nch * kL;
-    const int64_t csz = wchunk(B);
-    double* tile = smem;                              // [cpb][B][kLP] (chunk stride csz)
-    double* cft = tile + size_t(cpb) * csz;           // [cpb * kL][kCoef]
-    const bool prev = a.Wp != nullptr;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar);
-        const uint32_t cbytes = uint32_t(nrows) * kCoef * sizeof(double);
-        const uint32_t wbytes = prev ? uint32_t(nch * csz) * sizeof(double) : 0u;
-        mbar_expect_tx(&bar, cbytes + wbytes);
-        bulk_g2s(cft, a.coef + r0 * kCoef, cbytes, &bar);
-        if (prev) bulk_g2s(tile, a.Wp + ch0 * csz, wbytes, &bar);
-    }
-    __syncthreads();
-    // carries of the CTA's chunks and of its two neighbour chunks, [chunk + 1][col]
-    double* ys = cft + size_t(cpb) * kL * kCoef;
-    double* xs = ys + size_t(cpb + 2) * B;
-    double* edge = xs + size_t(cpb + 2) * B;   // [2][B]: x at rows r0 - 1 and r0 + nrows
-    if (prev) {
-        for (int e = threadIdx.x; e < (nch + 2) * B; e += blockDim.x) {
-            const int col = e / (nch + 2), q = e - col * (nch + 2);   // chunk fastest: contiguous per column
-            const int64_t ch = ch0 - 1 + q;
-            const bool ok = ch >= 0 && ch < a.P;
-            ys[q * B + col] = ok ? a.Yin[col * a.P + ch] : 0.0;
-            xs[q * B + col] = ok ? a.Xin[col * a.P + ch] : 0.0;
-        }
+    double* cft = smem;                              // [cpb * kL][kCoef]
+    double* xfirst = cft + size_t(cpb) * kL * kCoef;  // [cpb][B]: x_j at each chunk's first row
+    double* xlast = xfirst + size_t(cpb) * B;         // [cpb][B]: ... and last row
+    {
+        const double2* src = reinterpret_cast<const double2*>(a.coef + r0 * kCoef);
+        double2* dst = reinterpret_cast<double2*>(cft);
+        for (int e = threadIdx.x; e < nch * kL * kCoef / 2; e += blockDim.x) dst[e] = __ldg(src + e);
     }
     const int lc = threadIdx.x / B;
     const int col = threadIdx.x - lc * B;
-    mbar_wait(&bar, 0);
-    __syncthreads();
-    // the neighbours' edge rows (outside the tile), finished from their carry form
-    for (int e = threadIdx.x; prev && e < 2 * B; e += blockDim.x) {
-        const int side = e / B, c = e - side * B;
-        const int64_t row = side == 0 ? r0 - 1 : r0 + nrows;
-        double v = 0.0;
-        if (row >= 0 && row < a.P * kL) {
-            const double* cf = a.coef + row * kCoef;
-            const int q = side == 0 ? 0 : nch + 1;
-            v = fma(cf[kHb], xs[q * B + c], fma(cf[kWg], ys[q * B + c], a.Wp[wpos(row, c, B)]));
-        }
-        edge[side * B + c] = v;
+    const bool active = lc < nch;
+    const int64_t ch = ch0 + lc;
+    const int64_t s0 = ch * kL;
+    const bool prev = a.Wp != nullptr;
+    double w[kL];
+    double yc = 0.0, xc = 0.0, xm_out = 0.0, xe_out = 0.0;
+    if (active && prev) {
+#pragma unroll
+        for (int i = 0; i < kL; ++i) w[i] = a.Wp[(s0 + i) * B + col];
+        yc = a.Yin[col * a.P + ch];
+        xc = a.Xin[col * a.P + ch];
+        // the chunk-boundary neighbours outside this CTA, from their carry form
+        if (lc == 0 && ch >= 1) xm_out = carry_x(a.coef, a.Wp, a.Yin, a.Xin, a.P, B, col, s0 - 1);
+        if (lc == nch - 1 && ch + 1 < a.P) xe_out = carry_x(a.coef, a.Wp, a.Yin, a.Xin, a.P, B, col, s0 + kL);
     }
-    // thread = (chunk lc, column col): its 32 rows are contiguous, tcol[i] = row s0 + i
-    double* tcol = tile + size_t(lc) * csz + size_t(col) * kLP;
+    __syncthreads();   // coefficient rows staged
     const double* cf = cft + size_t(lc) * kL * kCoef;   // cf[i * kCoef + field]
-    double xm = 0.0, xe = 0.0;
-    if (lc < nch) {   // x_j from its carry form, in place
+    if (active) {   // x_j from its carry form
         if (prev) {
-            const double yc = ys[(lc + 1) * B + col], xc = xs[(lc + 1) * B + col];
 #pragma unroll
-            for (int i = 0; i < kL; ++i) tcol[i] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, tcol[i]));
+            for (int i = 0; i < kL; ++i) w[i] = fma(cf[i * kCoef + kHb], xc, fma(cf[i * kCoef + kWg], yc, w[i]));
         } else {
 #pragma unroll
-            for (int i = 0; i < kL; ++i) tcol[i] = 0.0;
+            for (int i = 0; i < kL; ++i) w[i] = 0.0;
         }
+        xfirst[lc * B + col] = w[0];
+        xlast[lc * B + col] = w[kL - 1];
     }
     __syncthreads();
-    if (lc < nch) {   // the neighbouring rows' x_j, before anyone overwrites its rows
-        xm = lc > 0 ? tcol[-csz + kL - 1] : (prev ? edge[col] : 0.0);
-        xe = lc + 1 < nch ? tcol[csz] : (prev ? edge[B + col] : 0.0);
-    }
-    __syncthreads();
-    if (lc < nch) {
-        const int64_t ch = ch0 + lc;
-        const int64_t s0 = ch * kL;
-        const int src = col / a.bb;
-        const int64_t k0 = s0 - a.row0;                 // physical node of the chunk's first row
-        const bool phys = k0 >= 0 && k0 + kL <= a.n;    // every row of the chunk is a physical node
-        if (prev) {   // consumers of x_j (loads first, then the read-modify-writes)
-            if (MODE == 0 && a.Uout) {
-#pragma unroll 8
-                for (int i = 0; i < kL; ++i)
-                    if (k0 + i >= 0 && k0 + i < a.n) a.Uout[(k0 + i) * a.S + col] = tcol[i];
-            } else if (MODE == 2) {   // acc_q += q (u(j+1) - u(j)), diffusion1d.hpp:329-332
-                if (phys) {
-                    const double* dp = a.du + k0 * a.S + src;
-                    double* ap = a.acc + k0 * B + col;
-#pragma unroll 1
-                    for (int i0 = 0; i0 < kL; i0 += 8) {   // eight loads in flight, then the stores
-                        double d[8], ac[8];
+    if (!active) return;   // no barrier below
+    double xm = lc > 0 ? xlast[(lc - 1) * B + col] : xm_out;
+    const double xe = lc + 1 < nch ? xfirst[(lc + 1) * B + col] : xe_out;
+    const int src = col / a.bb;
+    const int64_t k0 = s0 - a.row0;                 // physical node of the chunk's first row
+    const bool phys = k0 >= 0 && k0 + kL <= a.n;    // every row of the chunk is a physical node
+    if (prev) {   // consumers of x_j
+        if (MODE == 0 && a.Uout) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            d[i] = __ldg(dp + (i0 + i) * a.S);
-                            ac[i] = ap[(i0 + i) * B];
-                        }
+            for (int i = 0; i < kL; ++i)
+                if (k0 + i >= 0 && k0 + i < a.n) a.Uout[(k0 + i) * a.S + col] = w[i];
+        } else if (MODE == 2) {   // acc_q += q (u(j+1) - u(j)), diffusion1d.hpp:329-332
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) ap[(i0 + i) * B] = fma(tcol[i0 + i], d[i], ac[i]);
-                    }
-                } else {
-#pragma unroll 1
-                    for (int i0 = 0; i0 < kL; i0 += 8) {
-                        double d[8], ac[8];
+            for (int i0 = 0; i0 < kL; i0 += kAccBatch) {   // a batch of row pairs in flight, then the stores
+                double d[kAccBatch], ac[kAccBatch];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int64_t k = k0 + i0 + i;
-                            const bool ph = k >= 0 && k < a.n;
-                            d[i] = ph ? __ldg(a.du + k * a.S + src) : 0.0;
-                            ac[i] = ph ? a.acc[k * B + col] : 0.0;
-                        }
+                for (int i = 0; i < kAccBatch; ++i) {
+                    const int64_t k = k0 + i0 + i;
+                    const bool ph = phys || (k >= 0 && k < a.n);
+                    d[i] = ph ? __ldg(a.du + k * a.S + src) : 0.0;
+                    ac[i] = ph ? a.acc[k * B + col] : 0.0;
+                }
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int64_t k = k0 + i0 + i;
-                            if (k >= 0 && k < a.n) a.acc[k * B + col] = fma(tcol[i0 + i], d[i], ac[i]);
-                        }
-                    }
+                for (int i = 0; i < kAccBatch; ++i) {
+                    const int64_t k = k0 + i0 + i;
+                    if (phys || (k >= 0 && k < a.n)) a.acc[k * B + col] = fma(w[i0 + i], d[i], ac[i]);
                 }
             }
         }
-        bool force = false;   // a point source / receiver row inside this chunk
-        if (MODE == 0) {
-            force = (a.frow[col] - s0) >= 0 && (a.frow[col] - s0) < kL;
-        } else if (MODE == 2) {
-            for (int q = 0; q < a.nfrow; ++q) force |= (a.frow[q] - s0) >= 0 && (a.frow[q] - s0) < kL;
-        }
-        double zp = 0.0, xi = tcol[0];
-        if (MODE != 0 && !force && s0 >= 1 && s0 + kL < a.ns && (MODE != 1 || phys)) {
-            // interior chunk: both A- off-diagonals present on every row, no point forcing
-            const double mo = a.moff;
-            if constexpr (MODE == 1) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
-                const int jc = col - src * a.bb;
-                const double* np = a.nu + k0 * a.bb + jc;
-                const double* dp = a.du + k0 * a.S + src;
-                const double c = a.c;
-#pragma unroll 8
-                for (int i = 0; i < kL; ++i) {
-                    const double xn = i + 1 < kL ? tcol[i + 1] : xe;
-                    // same operation order as the general path (apply_minus, then the forcing)
-                    const double r = fma(mo, xm, fma(mo, xn, cf[i * kCoef + kMdiag] * xi)) -
-                                     c * (__ldg(np + i * a.bb) * __ldg(dp + i * a.S));
-                    zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
-                    tcol[i] = zp;
-                    xm = xi;
-                    xi = xn;
-                }
-            } else {
-#pragma unroll 8
-                for (int i = 0; i < kL; ++i) {
-                    const double xn = i + 1 < kL ? tcol[i + 1] : xe;
-                    const double r = fma(mo, xm, fma(mo, xn, cf[i * kCoef + kMdiag] * xi));
-                    zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
-                    tcol[i] = zp;
-                    xm = xi;
-                    xi = xn;
-                }
-            }
-        } else {
-#pragma unroll 8
+    }
+    bool force = false;   // a point source / receiver row inside this chunk
+    if (MODE == 0) {
+        force = (a.frow[col] - s0) >= 0 && (a.frow[col] - s0) < kL;
+    } else if (MODE == 2) {
+        for (int q = 0; q < a.nfrow; ++q) force |= (a.frow[q] - s0) >= 0 && (a.frow[q] - s0) < kL;
+    }
+    double zp = 0.0;
+    if (MODE != 0 && !force && s0 >= 1 && s0 + kL < a.ns && (MODE != 1 || phys)) {
+        // interior chunk: both A- off-diagonals on every row, no point forcing
+        const double mo = a.moff;
+        if constexpr (MODE == 1) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
+            const int jc = col - src * a.bb;
+            const double* np = a.nu + k0 * a.bb + jc;
+            const double* dp = a.du + k0 * a.S + src;
+            const double c = a.c;
+#pragma unroll
             for (int i = 0; i < kL; ++i) {
-                const int64_t row = s0 + i;
-                const double xn = i + 1 < kL ? tcol[i + 1] : xe;
-                const double cu = row + 1 < a.ns ? a.moff : 0.0;
-                const double cl = row >= 1 && row < a.ns ? a.moff : 0.0;
-                double r = fma(cl, xm, fma(cu, xn, cf[i * kCoef + kMdiag] * xi));
-                const int64_t k = row - a.row0;
-                if (MODE == 1 && k >= 0 && k < a.n) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
-                    const int jc = col - src * a.bb;
-                    r -= a.c * (__ldg(a.nu + k * a.bb + jc) * __ldg(a.du + k * a.S + src));
-                }
-                if (force) {
-                    if (MODE == 0) {   // point source of the column (:245-246)
-                        if (a.frow[col] == row) r += a.fval;
-                    } else {   // receiver residual sources (:325-326)
-                        for (int q = 0; q < a.nfrow; ++q)
-                            if (a.frow[q] == row) r -= a.fval * __ldg(a.vr + q * B + col);
-                    }
-                }
-                // local forward elimination y_i = r_i - m_i y_{i-1} (zero carry-in)
+                const double xi = w[i];
+                const double xn = i + 1 < kL ? w[i + 1] : xe;
+                // same operation order as the general path (apply_minus, then the forcing)
+                const double r = fma(mo, xm, fma(mo, xn, cf[i * kCoef + kMdiag] * xi)) -
+                                 c * (__ldg(np + i * a.bb) * __ldg(dp + i * a.S));
                 zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
-                tcol[i] = zp;   // row i's x_j already lives in the window
+                w[i] = zp;
                 xm = xi;
-                xi = xn;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kL; ++i) {
+                const double xi = w[i];
+                const double xn = i + 1 < kL ? w[i + 1] : xe;
+                const double r = fma(mo, xm, fma(mo, xn, cf[i * kCoef + kMdiag] * xi));
+                zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
+                w[i] = zp;
+                xm = xi;
             }
         }
-        a.zend[col * a.P + ch] = zp;
-        // local back substitution x_i = y_i / d_i - beta_i x_{i+1} (zero carry-in)
-        double w = zp * cf[(kL - 1) * kCoef + kRdfac];
-        tcol[kL - 1] = w;
+    } else {
 #pragma unroll
-        for (int i = kL - 2; i >= 0; --i) {
-            w = fma(-cf[i * kCoef + kBeta], w, cf[i * kCoef + kRdfac] * tcol[i]);
-            tcol[i] = w;
+        for (int i = 0; i < kL; ++i) {
+            const int64_t row = s0 + i;
+            const double xi = w[i];
+            const double xn = i + 1 < kL ? w[i + 1] : xe;
+            const double cu = row + 1 < a.ns ? a.moff : 0.0;
+            const double cl = row >= 1 && row < a.ns ? a.moff : 0.0;
+            double r = fma(cl, xm, fma(cu, xn, cf[i * kCoef + kMdiag] * xi));
+            const int64_t k = row - a.row0;
+            if (MODE == 1 && k >= 0 && k < a.n) {   // rhs -= c nu (u(j+1) - u(j)), diffusion1d.hpp:302-303
+                const int jc = col - src * a.bb;
+                r -= a.c * (__ldg(a.nu + k * a.bb + jc) * __ldg(a.du + k * a.S + src));
+            }
+            if (force) {
+                if (MODE == 0) {   // point source of the column (:245-246)
+                    if (a.frow[col] == row) r += a.fval;
+                } else {   // receiver residual sources (:325-326)
+                    for (int q = 0; q < a.nfrow; ++q)
+                        if (a.frow[q] == row) r -= a.fval * __ldg(a.vr + q * B + col);
+                }
+            }
+            // local forward elimination y_i = r_i - m_i y_{i-1} (zero carry-in)
+            zp = i == 0 ? r : fma(-cf[i * kCoef + kMult], zp, r);
+            w[i] = zp;
+            xm = xi;
         }
-        a.wstart[col * a.P + ch] = w;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) bulk_s2g(a.Wn + ch0 * csz, tile, uint32_t(nch * csz) * sizeof(double));
+    a.zend[col * a.P + ch] = zp;
+    // local back substitution x_i = y_i / d_i - beta_i x_{i+1} (zero carry-in)
+    double v = zp * cf[(kL - 1) * kCoef + kRdfac];
+    w[kL - 1] = v;
+#pragma unroll
+    for (int i = kL - 2; i >= 0; --i) {
+        v = fma(-cf[i * kCoef + kBeta], v, cf[i * kCoef + kRdfac] * w[i]);
+        w[i] = v;
+    }
+    a.wstart[col * a.P + ch] = v;
+#pragma unroll
+    for (int i = 0; i < kL; ++i) a.Wn[(s0 + i) * B + col] = w[i];
 }
 
 struct Aff {   // v -> a v + b
@@ -555,7 +482,7 @@ struct Marcher {
         // chunks per CTA: the count that keeps the most (chunk, column) threads resident
         // per SM under the shared-memory budget (ties: more chunks per CTA)
         auto smem_for = [B](int q) {
-            return (size_t(q) * (wchunk(B) + kL * kCoef) + 2 * size_t(q + 2) * B + 2 * size_t(B)) * sizeof(double);
+            return (size_t(q) * kL * kCoef + 2 * size_t(q) * B) * sizeof(double);
         };
         const int qmax = std::max(1, std::min(g_cpb_max, 256 / B));
         static std::mutex mu;
@@ -584,8 +511,8 @@ struct Marcher {
         H2B_CUDA(cudaFuncSetAttribute(cn_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         ca.aggF = aggF.data();
         ca.aggB = aggB.data();
-        W[0].resize(size_t(P) * wchunk(B), st);
-        W[1].resize(size_t(P) * wchunk(B), st);
+        W[0].resize(size_t(P) * kL * B, st);
+        W[1].resize(size_t(P) * kL * B, st);
         a.coef = coef;
         a.P = P;
         a.B = B;
