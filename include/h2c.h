@@ -305,6 +305,21 @@ int h2c_diff1d_state_field(h2c_diff1d d, int source, double* out);
 /* hessian_operator(include_tv) (:177-181); the operator keeps the problem alive */
 int h2c_diff1d_operator(h2c_diff1d d, int include_tv, h2c_operator* out);
 
+/* ---- Device black-box operator "surface<N>" (registry.hpp:89-101): the exact
+ *      minimal-surface Hessian (minimal_surface.hpp:100-140) at newton_state(steps) */
+typedef struct h2c_surface_s* h2c_surface;
+/* MinimalSurface(interior, rim) (minimal_surface.hpp:22-43) at newton_state(newton_steps) (:144-161) */
+int h2c_surface_create(int64_t interior, double rim, int newton_steps, h2c_surface* out);
+void h2c_surface_destroy(h2c_surface s);
+/* n = interior^2 unknowns, nonzeros of the assembled Hessian, grid spacing h */
+int h2c_surface_info(h2c_surface s, int64_t* n, int64_t* nnz, double* spacing);
+/* the interior surface the Hessian is taken at (n doubles, host) */
+int h2c_surface_state(h2c_surface s, double* out);
+/* y = H x (hessian_operator, :163-167): x and y n x b column-major DEVICE buffers (ld n) */
+int h2c_surface_hessvec(h2c_surface s, int64_t b, const double* x, double* y, void* stream);
+/* hessian_operator (:163-167); the operator keeps the problem alive */
+int h2c_surface_operator(h2c_surface s, h2c_operator* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -214,3 +214,9 @@ _sig("h2c_diff1d_hessvec", i32, H, i32, i64, vp, vp, vp)
 _sig("h2c_diff1d_state_field", i32, H, i32, vp)
 _sig("h2c_diff1d_operator", i32, H, i32, P(H))
 _sig("h2b_diff1d_tune", i32, i32, i32)
+_sig("h2c_surface_create", i32, i64, f64, i32, P(H))
+_sig("h2c_surface_destroy", None, H)
+_sig("h2c_surface_info", i32, H, P(i64), P(i64), P(f64))
+_sig("h2c_surface_state", i32, H, vp)
+_sig("h2c_surface_hessvec", i32, H, i64, vp, vp, vp)
+_sig("h2c_surface_operator", i32, H, P(H))

@@ -13,6 +13,7 @@
 #include "hara.hpp"
 #include "inversion.hpp"
 #include "diffusion1d.hpp"
+#include "surface.hpp"
 #include "serialize.hpp"
 #include "matrix.hpp"
 
@@ -970,6 +971,51 @@ int h2c_diff1d_operator(h2c_diff1d d, int include_tv, h2c_operator* out) {
     return guard([&] {
         need(d != nullptr && out != nullptr, "null argument");
         *out = new h2c_operator_s{h2b::diffusion_hessian_operator(d->d, include_tv != 0)};
+    });
+}
+
+struct h2c_surface_s {
+    std::shared_ptr<h2b::MinimalSurfaceDev> s;
+};
+
+int h2c_surface_create(int64_t interior, double rim, int newton_steps, h2c_surface* out) {
+    return guard([&] {
+        need(out != nullptr, "null argument");
+        auto s = std::make_shared<h2b::MinimalSurfaceDev>(interior, rim, newton_steps);
+        H2B_CUDA(cudaDeviceSynchronize());   // CSR uploads complete before any stream uses them
+        *out = new h2c_surface_s{std::move(s)};
+    });
+}
+
+void h2c_surface_destroy(h2c_surface s) { delete s; }
+
+int h2c_surface_info(h2c_surface s, int64_t* n, int64_t* nnz, double* spacing) {
+    return guard([&] {
+        need(s != nullptr, "null argument");
+        if (n) *n = s->s->n();
+        if (nnz) *nnz = s->s->nnz();
+        if (spacing) *spacing = s->s->spacing();
+    });
+}
+
+int h2c_surface_state(h2c_surface s, double* out) {
+    return guard([&] {
+        need(s != nullptr && out != nullptr, "null argument");
+        std::memcpy(out, s->s->state().data(), s->s->state().size() * sizeof(double));
+    });
+}
+
+int h2c_surface_hessvec(h2c_surface s, int64_t b, const double* x, double* y, void* stream) {
+    return guard([&] {
+        need(s != nullptr && x != nullptr && y != nullptr, "null argument");
+        s->s->hessvec(b, x, y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_surface_operator(h2c_surface s, h2c_operator* out) {
+    return guard([&] {
+        need(s != nullptr && out != nullptr, "null argument");
+        *out = new h2c_operator_s{h2b::surface_hessian_operator(s->s)};
     });
 }
 

@@ -1,11 +1,14 @@
 """Device PDE black-box operators (the reference's h2::oracles, SURVEY §8(f)
-row 2): the 1D diffusion density-inversion Hessian of BASELINE cfg3, computed
-on the B200 so HARA's operator applies never leave HBM.
+row 2), computed on the B200 so HARA's operator applies never leave HBM:
 
-Mirrors proj/include/h2/oracles/diffusion1d.hpp (Diffusion1D, :62-354) and
-the "diff1d-<n>" entry of make_oracle (registry.hpp:104-124). Only the
-evaluation-point Hessian (hessvec_at_target / hessian_operator) is built; the
-misfit, gradient and general-density Hessian are not on the HARA path.
+* the 1D diffusion density-inversion Hessian of BASELINE cfg3
+  (proj/include/h2/oracles/diffusion1d.hpp, Diffusion1D :62-354; registry
+  "diff1d-<n>", registry.hpp:104-124). Only the evaluation-point Hessian
+  (hessvec_at_target / hessian_operator) is built; the misfit, gradient and
+  general-density Hessian are not on the HARA path;
+* the minimal-surface Hessian "surface<N>" of cfg5 (minimal_surface.hpp,
+  registry.hpp:89-101): assembled once on the host, applied as a sparse
+  matrix in HBM.
 """
 import ctypes as C
 
@@ -101,12 +104,80 @@ class Diffusion1D:
         return out
 
 
+class MinimalSurface:
+    """MinimalSurface(interior, rim) (minimal_surface.hpp:22-43) with its Hessian
+    taken at newton_state(newton_steps) (:144-161, registry.hpp:92-93)."""
+
+    def __init__(self, interior, rim=0.5, newton_steps=0):
+        h = H()
+        check(lib.h2c_surface_create(int(interior), float(rim), int(newton_steps), C.byref(h)))
+        self._h = h
+        self.interior, self.rim, self.newton_steps = int(interior), float(rim), int(newton_steps)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.h2c_surface_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        n, nnz, h = C.c_int64(), C.c_int64(), C.c_double()
+        check(lib.h2c_surface_info(self._h, C.byref(n), C.byref(nnz), C.byref(h)))
+        return n.value, nnz.value, h.value
+
+    def n(self):
+        return self._info()[0]
+
+    def nnz(self):
+        return self._info()[1]
+
+    def spacing(self):
+        return self._info()[2]
+
+    def points(self):
+        """Grid2D(interior).points() (grid.hpp:38-48): (h i, h j), i fastest."""
+        g, h = self.interior, self.spacing()
+        i = np.tile(np.arange(1, g + 1), g)
+        j = np.repeat(np.arange(1, g + 1), g)
+        return np.stack([h * i, h * j], axis=1)
+
+    def state(self):
+        out = np.empty(self.n())
+        check(lib.h2c_surface_state(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def hessvec_device(self, x, y, b, stream=None):
+        """y = H x on device pointers (n x b column-major, ld n)."""
+        check(lib.h2c_surface_hessvec(self._h, int(b), x, y, stream))
+
+    def hessvec(self, x):
+        """y = H x on host arrays (n x b)."""
+        import torch
+        x = np.asarray(x, np.float64)
+        vec = x.ndim == 1
+        xm = x[:, None] if vec else x
+        if xm.shape[0] != self.n():
+            raise ValueError("hessvec: dimension mismatch")
+        xd = torch.from_numpy(np.ascontiguousarray(xm.T)).cuda()
+        yd = torch.empty_like(xd)
+        self.hessvec_device(xd.data_ptr(), yd.data_ptr(), xm.shape[1])
+        torch.cuda.synchronize()
+        y = yd.cpu().numpy().T
+        return y[:, 0] if vec else np.asfortranarray(y)
+
+    def hessian_operator(self):
+        """hessian_operator (:163-167): symmetric black box on the device."""
+        h = H()
+        check(lib.h2c_surface_operator(self._h, C.byref(h)))
+        return LinearOperator(h, self.n(), True, keep=self)
+
+
 class Oracle:
     """Oracle record of make_oracle (registry.hpp:58-81): op, points, leaf, mode, eta."""
 
-    def __init__(self, name, op, points, leaf, mode, eta, diffusion):
+    def __init__(self, name, op, points, leaf, mode, eta, diffusion=None, surface=None):
         self.name, self.op, self.points, self.leaf, self.mode, self.eta = name, op, points, leaf, mode, eta
         self.diffusion = diffusion
+        self.surface = surface
 
     def default_block_tree(self, leaf=None, eta=None):
         from .h2 import build_block_tree, build_cluster_tree
@@ -115,19 +186,24 @@ class Oracle:
 
 
 def make_oracle(name, config=None):
-    """make_oracle for "diff1d-<n>" (registry.hpp:104-124), with the same
-    override keys (steps, T, tp, t0, alpha, amp, beta, pad, tv, leaf, eta).
-    The surface / advdiff operators are not ported to the device."""
+    """make_oracle for "surface<N>" (registry.hpp:89-101; keys rim, newton_steps,
+    leaf, eta) and "diff1d-<n>" (registry.hpp:104-124; keys steps, T, tp, t0,
+    alpha, amp, beta, pad, tv, leaf, eta). The advdiff operator (sparse LU
+    solves) is not ported to the device."""
     from .h2 import Admissibility
     cfg = dict(config or {})
+    num = lambda k, d: float(cfg.get(k, d))
+    if name.startswith("surface"):
+        ms = MinimalSurface(int(name[7:]), num("rim", 0.5), int(cfg.get("newton_steps", 0)))
+        return Oracle(name, ms.hessian_operator(), ms.points(), int(cfg.get("leaf", 64)), Admissibility.strong,
+                      num("eta", 1.0), surface=ms)
     if not name.startswith("diff1d-"):
-        if name.startswith(("surface", "advdiff-")):
+        if name.startswith("advdiff-"):
             raise NotImplementedError(f"make_oracle: {name} has no device port")
         raise ValueError(f"unknown oracle {name}")
-    num = lambda k, d: float(cfg.get(k, d))
     d = Diffusion1D(n=int(name[7:]), steps=int(cfg.get("steps", 512)), final_time=num("T", 30.0),
                     t_p=num("tp", 1.0), t_0=num("t0", 0.0), alpha=num("alpha", 3e-5),
                     source_amplitude=num("amp", 1000.0), beta=num("beta", 1e-3), pad=num("pad", 0.5))
     tv = int(cfg.get("tv", 1)) != 0
     return Oracle(name, d.hessian_operator(tv), d.points(), int(cfg.get("leaf", 32)), Admissibility.weak,
-                  num("eta", 1.0), d)
+                  num("eta", 1.0), diffusion=d)
