@@ -281,12 +281,12 @@ template <bool SMEM>
 __global__ void __launch_bounds__(256) jacobi_kernel(const SvdJob* __restrict__ jobs) {
     extern __shared__ double sm[];
     __shared__ int rotated;
-    __shared__ int order[256];
     const SvdJob jb = jobs[blockIdx.x];
     const int r = jb.rows, c = jb.cols, ce = c + (c & 1);
     double* M = SMEM ? sm : jb.work;           // r x ce
     double* V = M + int64_t(r) * ce;           // ce x ce
     double* nrm = V + int64_t(ce) * ce;        // ce
+    int* order = reinterpret_cast<int*>(nrm + ce);   // c (selection order)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
     for (int64_t e = tid; e < int64_t(r) * ce; e += blockDim.x) {
         const int i = int(e % r), j = int(e / r);
@@ -572,13 +572,12 @@ void bqr(const std::vector<QrDesc>& d, cudaStream_t s) {
 void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     std::vector<SvdJob> sj, gj;
     size_t smax = 0, gtot = 0;
-    auto need = [](int r, int c) {
+    auto need = [](int r, int c) {   // doubles: M, V, norms, and the int selection order
         const size_t ce = size_t(c + (c & 1));
-        return size_t(r) * ce + ce * ce + ce;
+        return size_t(r) * ce + ce * ce + ce + ce / 2;
     };
     for (const SvdDesc& q : d) {
         if (q.rows <= 0 || q.cols <= 0) continue;
-        if (q.cols > 256) throw std::invalid_argument("bjacobi: more than 256 columns");
         SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr};
         const size_t nd = need(q.rows, q.cols);
         if (nd * sizeof(double) <= kSmemCap) {

@@ -313,3 +313,17 @@ def test_hybrid_low_rank_operator(cuda):
     assert hy.stats.consistent()
     pr = peel_construct(DenseOperator(a, True), bt, cfg)
     assert hy.stats.total <= pr.stats.total
+
+
+def test_peel_full_rank_blocks_above_256(cuda):
+    # a full-rank SPD operator: the level-1 sibling blocks (320 x 320) are sampled
+    # to rank 320, so the batched QR / Jacobi SVD of absorb_panel and recompress
+    # run on more than 256 columns (the reference has no such limit either)
+    n = 640
+    g = O.gaussian(91, n, n)
+    a = g @ g.T / n + np.eye(n)
+    bt, ref = tree1d(n, 16)
+    eps = 1e-8
+    res = peel_construct(DenseOperator(a, True), bt, PeelConfig(eps=eps))
+    assert max(res.matrix.rank_profile()) > 256
+    assert n2(dense(res.matrix, ref) - a) <= 3 * eps * n2(a)
