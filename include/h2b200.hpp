@@ -345,7 +345,7 @@ inline double estimate_relative_error(const LinearOperator& op, const H2Matrix& 
     return v;
 }
 
-// ---- h2::oracles (oracles/diffusion1d.hpp, registry.hpp): the cfg3 black box on the device ----
+// ---- h2::oracles (oracles/diffusion1d.hpp, minimal_surface.hpp, registry.hpp): device black boxes ----
 namespace oracles {
 
 struct Diffusion1DConfig {   // diffusion1d.hpp:62-73
@@ -414,13 +414,50 @@ private:
     std::shared_ptr<h2c_diff1d_s> h_;
 };
 
-struct Oracle {   // registry.hpp:58-81 (diffusion entries)
+class MinimalSurface {   // minimal_surface.hpp:22-175, Hessian at newton_state(steps) (registry.hpp:89-101)
+public:
+    explicit MinimalSurface(Index interior, double rim_amplitude = 0.5, int newton_steps = 0) : g_(interior) {
+        h2c_surface s = nullptr;
+        detail::check(h2c_surface_create(interior, rim_amplitude, newton_steps, &s));
+        h_ = std::shared_ptr<h2c_surface_s>(s, [](h2c_surface p) { h2c_surface_destroy(p); });
+    }
+    Index n() const { return g_ * g_; }
+    double spacing() const { return 1.0 / double(g_ + 1); }
+    PointSet points() const {   // Grid2D(interior).points() (grid.hpp:38-48), n x 2 column-major
+        std::vector<double> c(static_cast<size_t>(2 * n()));
+        for (Index j = 1; j <= g_; ++j)
+            for (Index i = 1; i <= g_; ++i) {
+                const Index r = (j - 1) * g_ + (i - 1);
+                c[size_t(r)] = spacing() * double(i);
+                c[size_t(r + n())] = spacing() * double(j);
+            }
+        return PointSet(n(), 2, c);
+    }
+    std::vector<double> state() const {   // the interior surface the Hessian is taken at
+        std::vector<double> m(static_cast<size_t>(n()));
+        detail::check(h2c_surface_state(h_.get(), m.data()));
+        return m;
+    }
+    // hessian_operator (:163-167): the operator keeps the problem alive
+    LinearOperator hessian_operator() const {
+        h2c_operator o = nullptr;
+        detail::check(h2c_surface_operator(h_.get(), &o));
+        return LinearOperator(o, n(), true, h_);
+    }
+
+private:
+    Index g_;
+    std::shared_ptr<h2c_surface_s> h_;
+};
+
+struct Oracle {   // registry.hpp:58-81 (surface and diffusion entries)
     std::string name;
     std::shared_ptr<LinearOperator> op;
     PointSet points{0, 1, {}};
     Index leaf = 32;
     Admissibility mode = Admissibility::weak;
     double eta = 1.0;
+    std::shared_ptr<MinimalSurface> surface;
     std::shared_ptr<Diffusion1D> diffusion;
     std::shared_ptr<const BlockTree> default_block_tree() const {
         auto ct = build_cluster_tree(points, leaf);
@@ -429,15 +466,26 @@ struct Oracle {   // registry.hpp:58-81 (diffusion entries)
 };
 
 using Config = std::map<std::string, std::string>;
-// make_oracle("diff1d-<n>", config) (registry.hpp:104-124); other oracles have no device port
+// make_oracle("surface<N>" | "diff1d-<n>", config) (registry.hpp:89-124); advdiff has no device port
 inline Oracle make_oracle(const std::string& name, const Config& config = {}) {
     auto num = [&](const char* k, double d) {
         auto it = config.find(k);
         return it == config.end() ? d : std::stod(it->second);
     };
+    if (name.rfind("surface", 0) == 0) {   // registry.hpp:89-101
+        Oracle o;
+        o.name = name;
+        o.surface = std::make_shared<MinimalSurface>(Index(std::stoll(name.substr(7))), num("rim", 0.5),
+                                                     int(num("newton_steps", 0)));
+        o.op = std::make_shared<LinearOperator>(o.surface->hessian_operator());
+        o.points = o.surface->points();
+        o.leaf = Index(num("leaf", 64));
+        o.mode = Admissibility::strong;
+        o.eta = num("eta", 1.0);
+        return o;
+    }
     if (name.rfind("diff1d-", 0) != 0) {
-        if (name.rfind("surface", 0) == 0 || name.rfind("advdiff-", 0) == 0)
-            throw std::logic_error("make_oracle: " + name + " has no device port");
+        if (name.rfind("advdiff-", 0) == 0) throw std::logic_error("make_oracle: " + name + " has no device port");
         throw std::invalid_argument("unknown oracle " + name);
     }
     Diffusion1DConfig dc;

@@ -139,11 +139,23 @@ TEST_CASE("diffusion oracle: registry, symmetric PSD Hessian, two marches per so
     CHECK(o.diffusion->pde_solves() - before == 6);
     bool threw = false;
     try {
-        oracles::make_oracle("surface16");
+        oracles::make_oracle("advdiff-16");
     } catch (const std::logic_error&) {
         threw = true;
     }
     CHECK(threw);
+    auto s = oracles::make_oracle("surface16");   // test_oracles.cpp:321-324
+    CHECK(s.op->dim() == 256);
+    CHECK(s.mode == Admissibility::strong);
+    CHECK(s.leaf == 64);
+    Matrix e = random_matrix(256, 2, rng);
+    const Matrix se = s.op->apply(e);
+    double sa = 0, sb = 0;
+    for (Index i = 0; i < 256; ++i) {
+        sa += e(i, 0) * se(i, 1);
+        sb += e(i, 1) * se(i, 0);
+    }
+    CHECK(std::abs(sa - sb) <= 1e-12 * std::abs(sb));
     // HARA on the device operator (the cfg3 pipeline at desk scale)
     auto res = peel_construct(*o.op, o.default_block_tree(), PeelConfig{1e-6});
     CHECK(estimate_relative_error(*o.op, res.matrix) <= 3e-6);
