@@ -1,7 +1,9 @@
 // ORACLE — TEST INFRASTRUCTURE ONLY. extern "C" access to the CPU
 // restatement for the Python parity tests and bench.py's cpu_baseline leg.
 // The product library never links this.
+#include <algorithm>
 #include <chrono>
+#include <random>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -375,6 +377,18 @@ int ora_gaussian(uint64_t seed, int64_t r, int64_t c, double* outp) {
         Matrix m(r, c);
         detail::fill_gaussian(m, rng);
         out(m, outp);
+    });
+}
+
+// std::shuffle of 0..n-1 with std::mt19937_64(seed): the observation pick of
+// AdvDiff2D::pick_observations (advdiff2d.hpp:112-124), with the same libstdc++
+int ora_shuffle(int64_t n, uint64_t seed, int64_t* outp) {
+    return guard([&] {
+        std::vector<int64_t> v(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) v[size_t(i)] = i;
+        std::mt19937_64 rng(seed);
+        std::shuffle(v.begin(), v.end(), rng);
+        std::memcpy(outp, v.data(), v.size() * sizeof(int64_t));
     });
 }
 

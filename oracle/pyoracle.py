@@ -58,6 +58,7 @@ _sig("ora_peel_dense", vp, vp, i32, f64, i64, i64, i64, u64, f64, P(vp), P(i64),
 _sig("ora_peel_h2", vp, vp, f64, u64, f64, P(vp), P(i64))
 _sig("ora_pnorm2_dense", vp, i64, i32, P(f64), P(i32))
 _sig("ora_gaussian", u64, i64, i64, vp)
+_sig("ora_shuffle", i64, u64, vp)
 _sig("ora_diff1d_create", i64, i64, f64, f64, f64, f64, f64, f64, f64, i32, vp, i64, P(vp))
 _lib.ora_diff1d_destroy.argtypes = [vp]
 _lib.ora_diff1d_destroy.restype = None
@@ -258,6 +259,13 @@ def pnorm2_dense(a, symmetric):
     v, it = f64(), i32()
     _check(_lib.ora_pnorm2_dense(_p(a), a.shape[0], int(symmetric), C.byref(v), C.byref(it)))
     return v.value, it.value
+
+
+def shuffle_indices(n, seed):
+    """std::shuffle of 0..n-1 with std::mt19937_64(seed) (the reference's libstdc++ stream)."""
+    out = np.empty(int(n), np.int64)
+    _check(_lib.ora_shuffle(int(n), int(seed), _p(out)))
+    return out
 
 
 def gaussian(seed, r, c):
