@@ -450,7 +450,67 @@ private:
     std::shared_ptr<h2c_surface_s> h_;
 };
 
-struct Oracle {   // registry.hpp:58-81 (surface and diffusion entries)
+struct AdvDiff2DConfig {   // advdiff2d.hpp:21-28
+    Index grid = 32;
+    double kappa = 1e-3;
+    double reaction = 0.5;
+    Index num_observations = 100;
+    double noise_rel = 0.01;
+    uint64_t obs_seed = 7;
+};
+
+class AdvDiff2D {   // advdiff2d.hpp:30-146: misfit Hessian of the stationary source inversion
+public:
+    explicit AdvDiff2D(AdvDiff2DConfig cfg = {}) : cfg_(cfg) {
+        h2c_advdiff_config c;
+        h2c_advdiff_config_default(&c);
+        c.grid = cfg_.grid;
+        c.kappa = cfg_.kappa;
+        c.reaction = cfg_.reaction;
+        c.num_observations = cfg_.num_observations;
+        c.noise_rel = cfg_.noise_rel;
+        c.obs_seed = cfg_.obs_seed;
+        h2c_advdiff a = nullptr;
+        detail::check(h2c_advdiff_create(&c, &a));
+        h_ = std::shared_ptr<h2c_advdiff_s>(a, [](h2c_advdiff p) { h2c_advdiff_destroy(p); });
+    }
+    Index n() const { return cfg_.grid * cfg_.grid; }
+    const AdvDiff2DConfig& config() const { return cfg_; }
+    double sigma() const {
+        double s = 0;
+        detail::check(h2c_advdiff_info(h_.get(), nullptr, &s, nullptr, nullptr));
+        return s;
+    }
+    long solves() const {
+        int64_t v = 0;
+        detail::check(h2c_advdiff_info(h_.get(), nullptr, nullptr, nullptr, &v));
+        return long(v);
+    }
+    PointSet points() const {   // Grid2D(grid).points() (grid.hpp:38-48), n x 2 column-major
+        const Index g = cfg_.grid;
+        const double h = 1.0 / double(g + 1);
+        std::vector<double> c(static_cast<size_t>(2 * n()));
+        for (Index j = 1; j <= g; ++j)
+            for (Index i = 1; i <= g; ++i) {
+                const Index r = (j - 1) * g + (i - 1);
+                c[size_t(r)] = h * double(i);
+                c[size_t(r + n())] = h * double(j);
+            }
+        return PointSet(n(), 2, c);
+    }
+    // hessian_operator (:66-68): the operator keeps the problem alive
+    LinearOperator hessian_operator() const {
+        h2c_operator o = nullptr;
+        detail::check(h2c_advdiff_operator(h_.get(), &o));
+        return LinearOperator(o, n(), true, h_);
+    }
+
+private:
+    AdvDiff2DConfig cfg_;
+    std::shared_ptr<h2c_advdiff_s> h_;
+};
+
+struct Oracle {   // registry.hpp:58-81
     std::string name;
     std::shared_ptr<LinearOperator> op;
     PointSet points{0, 1, {}};
@@ -459,6 +519,7 @@ struct Oracle {   // registry.hpp:58-81 (surface and diffusion entries)
     double eta = 1.0;
     std::shared_ptr<MinimalSurface> surface;
     std::shared_ptr<Diffusion1D> diffusion;
+    std::shared_ptr<AdvDiff2D> advdiff;
     std::shared_ptr<const BlockTree> default_block_tree() const {
         auto ct = build_cluster_tree(points, leaf);
         return build_block_tree(ct, ct, eta, mode);
@@ -466,7 +527,7 @@ struct Oracle {   // registry.hpp:58-81 (surface and diffusion entries)
 };
 
 using Config = std::map<std::string, std::string>;
-// make_oracle("surface<N>" | "diff1d-<n>", config) (registry.hpp:89-124); advdiff has no device port
+// make_oracle("surface<N>" | "diff1d-<n>" | "advdiff-<G>[-k..][-obs..]", config) (registry.hpp:83-154)
 inline Oracle make_oracle(const std::string& name, const Config& config = {}) {
     auto num = [&](const char* k, double d) {
         auto it = config.find(k);
@@ -484,10 +545,33 @@ inline Oracle make_oracle(const std::string& name, const Config& config = {}) {
         o.eta = num("eta", 1.0);
         return o;
     }
-    if (name.rfind("diff1d-", 0) != 0) {
-        if (name.rfind("advdiff-", 0) == 0) throw std::logic_error("make_oracle: " + name + " has no device port");
-        throw std::invalid_argument("unknown oracle " + name);
+    if (name.rfind("advdiff-", 0) == 0) {   // registry.hpp:125-150
+        AdvDiff2DConfig ac;
+        std::string rest = name.substr(8);
+        const auto dash = rest.find('-');
+        ac.grid = Index(std::stoll(rest.substr(0, dash)));
+        std::string tail = dash == std::string::npos ? "" : rest.substr(dash);
+        if (const auto at = tail.find("-obs"); at != std::string::npos) {
+            ac.num_observations = Index(std::stoll(tail.substr(at + 4)));
+            tail = tail.substr(0, at);
+        }
+        if (tail.rfind("-k", 0) == 0) ac.kappa = std::stod(tail.substr(2));
+        ac.kappa = num("kappa", ac.kappa);
+        ac.num_observations = Index(num("obs", double(ac.num_observations)));
+        ac.noise_rel = num("noise", ac.noise_rel);
+        ac.obs_seed = uint64_t(num("obs_seed", double(ac.obs_seed)));
+        ac.reaction = num("c", ac.reaction);
+        Oracle o;
+        o.name = name;
+        o.advdiff = std::make_shared<AdvDiff2D>(ac);
+        o.op = std::make_shared<LinearOperator>(o.advdiff->hessian_operator());
+        o.points = o.advdiff->points();
+        o.leaf = Index(num("leaf", 64));
+        o.mode = Admissibility::strong;
+        o.eta = num("eta", 1.0);
+        return o;
     }
+    if (name.rfind("diff1d-", 0) != 0) throw std::invalid_argument("unknown oracle " + name);
     Diffusion1DConfig dc;
     dc.n = Index(std::stoll(name.substr(7)));
     dc.steps = Index(num("steps", double(dc.steps)));

@@ -320,6 +320,29 @@ int h2c_surface_hessvec(h2c_surface s, int64_t b, const double* x, double* y, vo
 /* hessian_operator (:163-167); the operator keeps the problem alive */
 int h2c_surface_operator(h2c_surface s, h2c_operator* out);
 
+/* ---- Device black-box operator "advdiff-<G>" (registry.hpp:125-150): the misfit
+ *      Hessian of the stationary advection-diffusion source inversion (advdiff2d.hpp) */
+typedef struct h2c_advdiff_s* h2c_advdiff;
+typedef struct {
+    int64_t grid;                    /* unknowns per side */
+    double kappa, reaction;
+    int64_t num_observations;
+    double noise_rel;
+    uint64_t obs_seed;
+} h2c_advdiff_config;                /* AdvDiff2DConfig (advdiff2d.hpp:21-28) */
+void h2c_advdiff_config_default(h2c_advdiff_config* cfg);
+/* AdvDiff2D(cfg) (advdiff2d.hpp:35-40): operator, observation pick, noise calibration */
+int h2c_advdiff_create(const h2c_advdiff_config* cfg, h2c_advdiff* out);
+void h2c_advdiff_destroy(h2c_advdiff a);
+/* n, sigma, number of observations, solves counted as the reference counts them */
+int h2c_advdiff_info(h2c_advdiff a, int64_t* n, double* sigma, int64_t* num_observations, int64_t* solves);
+/* the sorted observation nodes (num_observations int64, host) */
+int h2c_advdiff_observations(h2c_advdiff a, int64_t* out);
+/* misfit_hessvec (:54-64): y = H x, x and y n x b column-major DEVICE buffers (ld n) */
+int h2c_advdiff_hessvec(h2c_advdiff a, int64_t b, const double* x, double* y, void* stream);
+/* hessian_operator (:66-68); the operator keeps the problem alive */
+int h2c_advdiff_operator(h2c_advdiff a, h2c_operator* out);
+
 #ifdef __cplusplus
 }
 #endif

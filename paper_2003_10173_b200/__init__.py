@@ -10,7 +10,7 @@ from .construction import (DenseOperator, H2Operator, HybridResult, LinearOperat
                            PeelConfig, PeelResult, SampleStats, estimate_relative_error, hybrid_construct,
                            make_operator, orthogonalize, peel_construct, pnorm_estimate, randomized_lowrank,
                            recompress)
-from .pde import Diffusion1D, MinimalSurface, Oracle, make_oracle
+from .pde import AdvDiff2D, Diffusion1D, MinimalSurface, Oracle, make_oracle
 from .inversion import (ConvergenceTrace, HInverseResult, ThresholdSchedule, desymmetrized, h_hyperpower,
                         h_newton_schulz, h_unrolled, hyperpower_sampler, low_rank_update, ns_sampler,
                         residual_norm, scaled_identity, scaled_identity_start, threshold_schedule,
@@ -24,4 +24,4 @@ __all__ = ["Admissibility", "BlockTree", "ClusterTree", "H2Matrix", "Ordering", 
            "hyperpower_sampler", "low_rank_update", "ns_sampler", "residual_norm", "scaled_identity",
            "scaled_identity_start", "threshold_schedule", "unrolled_sampler", "HybridResult", "LowRankFactor",
            "LowRankResult", "hybrid_construct", "randomized_lowrank", "serialize", "deserialize", "write_h2_file",
-           "read_h2_file", "io_error", "Diffusion1D", "MinimalSurface", "Oracle", "make_oracle"]
+           "read_h2_file", "io_error", "AdvDiff2D", "Diffusion1D", "MinimalSurface", "Oracle", "make_oracle"]

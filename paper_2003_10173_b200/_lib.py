@@ -220,3 +220,18 @@ _sig("h2c_surface_info", i32, H, P(i64), P(i64), P(f64))
 _sig("h2c_surface_state", i32, H, vp)
 _sig("h2c_surface_hessvec", i32, H, i64, vp, vp, vp)
 _sig("h2c_surface_operator", i32, H, P(H))
+
+
+class AdvDiffConfigC(C.Structure):
+    """h2c_advdiff_config (AdvDiff2DConfig, advdiff2d.hpp:21-28)."""
+    _fields_ = [("grid", i64), ("kappa", f64), ("reaction", f64), ("num_observations", i64), ("noise_rel", f64),
+                ("obs_seed", C.c_uint64)]
+
+
+_sig("h2c_advdiff_config_default", None, P(AdvDiffConfigC))
+_sig("h2c_advdiff_create", i32, P(AdvDiffConfigC), P(H))
+_sig("h2c_advdiff_destroy", None, H)
+_sig("h2c_advdiff_info", i32, H, P(i64), P(f64), P(i64), P(i64))
+_sig("h2c_advdiff_observations", i32, H, vp)
+_sig("h2c_advdiff_hessvec", i32, H, i64, vp, vp, vp)
+_sig("h2c_advdiff_operator", i32, H, P(H))

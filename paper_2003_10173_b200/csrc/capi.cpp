@@ -14,6 +14,7 @@
 #include "inversion.hpp"
 #include "diffusion1d.hpp"
 #include "surface.hpp"
+#include "advdiff.hpp"
 #include "serialize.hpp"
 #include "matrix.hpp"
 
@@ -1016,6 +1017,69 @@ int h2c_surface_operator(h2c_surface s, h2c_operator* out) {
     return guard([&] {
         need(s != nullptr && out != nullptr, "null argument");
         *out = new h2c_operator_s{h2b::surface_hessian_operator(s->s)};
+    });
+}
+
+struct h2c_advdiff_s {
+    std::shared_ptr<h2b::AdvDiff2DDev> a;
+};
+
+void h2c_advdiff_config_default(h2c_advdiff_config* cfg) {
+    if (!cfg) return;
+    const h2b::AdvDiffConfig d;
+    cfg->grid = d.grid;
+    cfg->kappa = d.kappa;
+    cfg->reaction = d.reaction;
+    cfg->num_observations = d.num_observations;
+    cfg->noise_rel = d.noise_rel;
+    cfg->obs_seed = d.obs_seed;
+}
+
+int h2c_advdiff_create(const h2c_advdiff_config* cfg, h2c_advdiff* out) {
+    return guard([&] {
+        need(cfg != nullptr && out != nullptr, "null argument");
+        h2b::AdvDiffConfig c;
+        c.grid = cfg->grid;
+        c.kappa = cfg->kappa;
+        c.reaction = cfg->reaction;
+        c.num_observations = cfg->num_observations;
+        c.noise_rel = cfg->noise_rel;
+        c.obs_seed = cfg->obs_seed;
+        *out = new h2c_advdiff_s{std::make_shared<h2b::AdvDiff2DDev>(c)};
+    });
+}
+
+void h2c_advdiff_destroy(h2c_advdiff a) { delete a; }
+
+int h2c_advdiff_info(h2c_advdiff a, int64_t* n, double* sigma, int64_t* num_observations, int64_t* solves) {
+    return guard([&] {
+        need(a != nullptr, "null argument");
+        if (n) *n = a->a->n();
+        if (sigma) *sigma = a->a->sigma();
+        if (num_observations) *num_observations = int64_t(a->a->observation_nodes().size());
+        if (solves) *solves = a->a->solves();
+    });
+}
+
+int h2c_advdiff_observations(h2c_advdiff a, int64_t* out) {
+    return guard([&] {
+        need(a != nullptr && out != nullptr, "null argument");
+        const auto& o = a->a->observation_nodes();
+        std::memcpy(out, o.data(), o.size() * sizeof(int64_t));
+    });
+}
+
+int h2c_advdiff_hessvec(h2c_advdiff a, int64_t b, const double* x, double* y, void* stream) {
+    return guard([&] {
+        need(a != nullptr && x != nullptr && y != nullptr, "null argument");
+        a->a->misfit_hessvec(b, x, y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_advdiff_operator(h2c_advdiff a, h2c_operator* out) {
+    return guard([&] {
+        need(a != nullptr && out != nullptr, "null argument");
+        *out = new h2c_operator_s{h2b::advdiff_hessian_operator(a->a)};
     });
 }
 

@@ -6,15 +6,18 @@ row 2), computed on the B200 so HARA's operator applies never leave HBM:
   "diff1d-<n>", registry.hpp:104-124). Only the evaluation-point Hessian
   (hessvec_at_target / hessian_operator) is built; the misfit, gradient and
   general-density Hessian are not on the HARA path;
-* the minimal-surface Hessian "surface<N>" of cfg5 (minimal_surface.hpp,
+* the minimal-surface Hessian "surface<N>" (minimal_surface.hpp,
   registry.hpp:89-101): assembled once on the host, applied as a sparse
-  matrix in HBM.
+  matrix in HBM;
+* the advection-diffusion misfit Hessian "advdiff-<G>" (advdiff2d.hpp,
+  registry.hpp:125-150): its observation factor G = (h^2/sigma) B A^{-1} is
+  formed once, and every application is y = G^T (G x) in HBM.
 """
 import ctypes as C
 
 import numpy as np
 
-from ._lib import Diff1DConfigC, H, check, lib
+from ._lib import AdvDiffConfigC, Diff1DConfigC, H, check, lib
 from .construction import LinearOperator
 
 
@@ -171,13 +174,86 @@ class MinimalSurface:
         return LinearOperator(h, self.n(), True, keep=self)
 
 
+class AdvDiff2D:
+    """AdvDiff2D(cfg) (advdiff2d.hpp:35-40); keyword names follow AdvDiff2DConfig (:21-28)."""
+
+    def __init__(self, grid=32, kappa=1e-3, reaction=0.5, num_observations=100, noise_rel=0.01, obs_seed=7):
+        c = AdvDiffConfigC()
+        lib.h2c_advdiff_config_default(C.byref(c))
+        c.grid, c.kappa, c.reaction = int(grid), float(kappa), float(reaction)
+        c.num_observations, c.noise_rel, c.obs_seed = int(num_observations), float(noise_rel), int(obs_seed)
+        h = H()
+        check(lib.h2c_advdiff_create(C.byref(c), C.byref(h)))
+        self._h = h
+        self.config = dict(grid=grid, kappa=kappa, reaction=reaction, num_observations=num_observations,
+                           noise_rel=noise_rel, obs_seed=obs_seed)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.h2c_advdiff_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        n, sg, no, sv = C.c_int64(), C.c_double(), C.c_int64(), C.c_int64()
+        check(lib.h2c_advdiff_info(self._h, C.byref(n), C.byref(sg), C.byref(no), C.byref(sv)))
+        return n.value, sg.value, no.value, sv.value
+
+    def n(self):
+        return self._info()[0]
+
+    def sigma(self):
+        return self._info()[1]
+
+    def solves(self):
+        return self._info()[3]
+
+    def observation_nodes(self):
+        out = np.empty(self._info()[2], np.int64)
+        check(lib.h2c_advdiff_observations(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def points(self):
+        """Grid2D(grid).points() (grid.hpp:38-48): (h i, h j), i fastest."""
+        g = int(self.config["grid"])
+        h = 1.0 / (g + 1)
+        i = np.tile(np.arange(1, g + 1), g)
+        j = np.repeat(np.arange(1, g + 1), g)
+        return np.stack([h * i, h * j], axis=1)
+
+    def hessvec_device(self, x, y, b, stream=None):
+        """y = H x on device pointers (n x b column-major, ld n)."""
+        check(lib.h2c_advdiff_hessvec(self._h, int(b), x, y, stream))
+
+    def misfit_hessvec(self, nu):
+        """misfit_hessvec (:54-64) on host arrays (n x b)."""
+        import torch
+        nu = np.asarray(nu, np.float64)
+        vec = nu.ndim == 1
+        xm = nu[:, None] if vec else nu
+        if xm.shape[0] != self.n():
+            raise ValueError("advdiff hessvec: dimension mismatch")
+        xd = torch.from_numpy(np.ascontiguousarray(xm.T)).cuda()
+        yd = torch.empty_like(xd)
+        self.hessvec_device(xd.data_ptr(), yd.data_ptr(), xm.shape[1])
+        torch.cuda.synchronize()
+        y = yd.cpu().numpy().T
+        return y[:, 0] if vec else np.asfortranarray(y)
+
+    def hessian_operator(self):
+        """hessian_operator (:66-68): symmetric black box on the device."""
+        h = H()
+        check(lib.h2c_advdiff_operator(self._h, C.byref(h)))
+        return LinearOperator(h, self.n(), True, keep=self)
+
+
 class Oracle:
     """Oracle record of make_oracle (registry.hpp:58-81): op, points, leaf, mode, eta."""
 
-    def __init__(self, name, op, points, leaf, mode, eta, diffusion=None, surface=None):
+    def __init__(self, name, op, points, leaf, mode, eta, diffusion=None, surface=None, advdiff=None):
         self.name, self.op, self.points, self.leaf, self.mode, self.eta = name, op, points, leaf, mode, eta
         self.diffusion = diffusion
         self.surface = surface
+        self.advdiff = advdiff
 
     def default_block_tree(self, leaf=None, eta=None):
         from .h2 import build_block_tree, build_cluster_tree
@@ -187,9 +263,9 @@ class Oracle:
 
 def make_oracle(name, config=None):
     """make_oracle for "surface<N>" (registry.hpp:89-101; keys rim, newton_steps,
-    leaf, eta) and "diff1d-<n>" (registry.hpp:104-124; keys steps, T, tp, t0,
-    alpha, amp, beta, pad, tv, leaf, eta). The advdiff operator (sparse LU
-    solves) is not ported to the device."""
+    leaf, eta), "diff1d-<n>" (registry.hpp:104-124; keys steps, T, tp, t0,
+    alpha, amp, beta, pad, tv, leaf, eta) and "advdiff-<G>[-k<kappa>][-obs<N>]"
+    (registry.hpp:125-150; keys kappa, obs, noise, obs_seed, c, leaf, eta)."""
     from .h2 import Admissibility
     cfg = dict(config or {})
     num = lambda k, d: float(cfg.get(k, d))
@@ -197,9 +273,24 @@ def make_oracle(name, config=None):
         ms = MinimalSurface(int(name[7:]), num("rim", 0.5), int(cfg.get("newton_steps", 0)))
         return Oracle(name, ms.hessian_operator(), ms.points(), int(cfg.get("leaf", 64)), Admissibility.strong,
                       num("eta", 1.0), surface=ms)
+    if name.startswith("advdiff-"):
+        rest = name[8:]
+        dash = rest.find("-")
+        grid = int(rest if dash < 0 else rest[:dash])
+        tail = "" if dash < 0 else rest[dash:]
+        kappa, obs = 1e-3, 100
+        at = tail.find("-obs")
+        if at >= 0:
+            obs = int(tail[at + 4:])
+            tail = tail[:at]
+        if tail.startswith("-k"):
+            kappa = float(tail[2:])
+        a = AdvDiff2D(grid=grid, kappa=num("kappa", kappa), reaction=num("c", 0.5),
+                      num_observations=int(cfg.get("obs", obs)), noise_rel=num("noise", 0.01),
+                      obs_seed=int(cfg.get("obs_seed", 7)))
+        return Oracle(name, a.hessian_operator(), a.points(), int(cfg.get("leaf", 64)), Admissibility.strong,
+                      num("eta", 1.0), advdiff=a)
     if not name.startswith("diff1d-"):
-        if name.startswith("advdiff-"):
-            raise NotImplementedError(f"make_oracle: {name} has no device port")
         raise ValueError(f"unknown oracle {name}")
     d = Diffusion1D(n=int(name[7:]), steps=int(cfg.get("steps", 512)), final_time=num("T", 30.0),
                     t_p=num("tp", 1.0), t_0=num("t0", 0.0), alpha=num("alpha", 3e-5),

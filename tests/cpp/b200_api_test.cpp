@@ -139,11 +139,18 @@ TEST_CASE("diffusion oracle: registry, symmetric PSD Hessian, two marches per so
     CHECK(o.diffusion->pde_solves() - before == 6);
     bool threw = false;
     try {
-        oracles::make_oracle("advdiff-16");
-    } catch (const std::logic_error&) {
+        oracles::make_oracle("nonsense");
+    } catch (const std::invalid_argument&) {
         threw = true;
     }
     CHECK(threw);
+    auto ad = oracles::make_oracle("advdiff-16-k1e-2-obs50");   // test_oracles.cpp:333-336
+    CHECK(ad.op->dim() == 256);
+    CHECK(ad.advdiff->config().kappa == 1e-2);
+    CHECK(ad.advdiff->config().num_observations == 50);
+    const long s0 = ad.advdiff->solves();
+    ad.op->apply(random_matrix(256, 2, rng));
+    CHECK(ad.advdiff->solves() - s0 == 2);
     auto s = oracles::make_oracle("surface16");   // test_oracles.cpp:321-324
     CHECK(s.op->dim() == 256);
     CHECK(s.mode == Admissibility::strong);

@@ -101,8 +101,6 @@ def test_registry_names_and_overrides(cuda):   # test_oracles.cpp:321-331
     assert o.leaf == 16
     assert o.mode == Admissibility.weak
     assert o.diffusion.steps == 32
-    with pytest.raises(NotImplementedError):
-        make_oracle("advdiff-16")
     with pytest.raises(ValueError):
         make_oracle("nonsense")
 
