@@ -81,6 +81,7 @@ AdvDiff2DDev::AdvDiff2DDev(const AdvDiffConfig& cfg) : c_(cfg) {
         for (int64_t i = 2; i < g; ++i) interior.push_back(at(i, j));
     if (c_.num_observations > int64_t(interior.size()))
         throw std::invalid_argument("advdiff: more observations than interior nodes");
+    if (c_.num_observations < 0) throw std::invalid_argument("advdiff: negative number of observations");
     std::mt19937_64 rng(c_.obs_seed);
     std::shuffle(interior.begin(), interior.end(), rng);
     obs_.assign(interior.begin(), interior.begin() + c_.num_observations);
@@ -118,11 +119,15 @@ AdvDiff2DDev::AdvDiff2DDev(const AdvDiffConfig& cfg) : c_(cfg) {
 void AdvDiff2DDev::misfit_hessvec(int64_t b, const double* x, double* y, cudaStream_t s) {
     if (b < 1) throw std::invalid_argument("advdiff hessvec: dimension mismatch");
     const int64_t N = n(), R = int64_t(obs_.size());
-    DeviceArray<double> z(size_t(std::max<int64_t>(R * b, 1)), s);
+    solves_ += 2;   // the reference's accounting: one forward and one adjoint solve (:54-64)
+    if (R == 0) {   // no observations: the misfit Hessian is zero
+        for (int64_t c = 0; c < b; ++c) H2B_CUDA(cudaMemsetAsync(y + c * N, 0, size_t(N) * sizeof(double), s));
+        return;
+    }
+    DeviceArray<double> z(size_t(R * b), s);
     // z = G x, y = G^T z (two batched-GEMM launches, split-K over the n rows of the first)
     la::bgemm({la::GemmDesc{G_.data(), x, z.data(), int(R), int(b), int(N), int(R), int(N), int(R), 0, 0, 1.0, 0.0}}, s);
     la::bgemm({la::GemmDesc{G_.data(), z.data(), y, int(N), int(b), int(R), int(R), int(R), int(N), 1, 0, 1.0, 0.0}}, s);
-    solves_ += 2;   // the reference's accounting: one forward and one adjoint solve (:54-64)
 }
 
 std::unique_ptr<DevOperator> advdiff_hessian_operator(std::shared_ptr<AdvDiff2DDev> a) {

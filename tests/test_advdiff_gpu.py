@@ -44,6 +44,8 @@ def test_zero_symmetry_psd_and_counter(cuda):   # test_oracles.cpp:259-292
         AdvDiff2D(grid=8, kappa=0.0)
     with pytest.raises(ValueError):
         AdvDiff2D(grid=8, num_observations=1000)
+    none = AdvDiff2D(grid=8, num_observations=0)   # no observations: a zero misfit Hessian
+    assert np.count_nonzero(none.misfit_hessvec(np.ones((64, 2)))) == 0
 
 
 def test_numerical_rank_grows_with_observations(cuda):   # test_oracles.cpp:294-310
