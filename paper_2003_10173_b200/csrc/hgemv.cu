@@ -161,7 +161,17 @@ __device__ __forceinline__ void chunk_mma(const double* __restrict__ at, const d
 }
 
 template <int MT, int NB, int WM, int WN, int STAGES, int KC, bool VEC, int MODE>
-__global__ void __launch_bounds__(WM * WN * 32) seg_gemm_kernel(SegArgs args) {
+#ifndef SEG32_MINB
+#define SEG32_MINB 12
+#endif
+#ifndef SEG64_MINB
+#define SEG64_MINB 4
+#endif
+// residency is the latency hiding: single-buffered 32-row CTAs run up to 12 per SM,
+// double-buffered 64-row CTAs (55 KB of smem) 4 per SM
+__global__ void __launch_bounds__(WM * WN * 32, (MT == 32 && STAGES == 1) ? SEG32_MINB
+                                                  : ((MT == 64 && STAGES == 2 && NB == 32) ? SEG64_MINB : 1))
+    seg_gemm_kernel(SegArgs args) {
     constexpr int NT = WM * WN * 32;
     constexpr int KP = KC + 4;
     constexpr int A_SZ = MT * KP, B_SZ = NB * KP, ST_SZ = A_SZ + B_SZ;
