@@ -750,8 +750,20 @@ __global__ void gather_blocked_kernel(const double* __restrict__ x, int64_t ldx,
                                       int64_t b, double* __restrict__ xint) {
     const int64_t beg = leaf_begin[blockIdx.x];
     const int m = leaf_m[blockIdx.x];
-    const int64_t total = int64_t(m) * b;
     double* dst = xint + beg * b;
+    if (m <= int(blockDim.x)) {
+        // thread -> (row i, first column j0): the row's user index is loaded once,
+        // then every column step is one independent load and one contiguous store
+        const int per = int(blockDim.x) / m;   // columns per pass
+        const int i = threadIdx.x % m, j0 = threadIdx.x / m;
+        if (j0 >= per) return;
+        const int64_t r = perm ? perm[beg + i] : beg + i;
+        const double* src = x + r;
+#pragma unroll 4
+        for (int64_t j = j0; j < b; j += per) dst[i + j * m] = __ldg(src + j * ldx);
+        return;
+    }
+    const int64_t total = int64_t(m) * b;
     for (int64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
         const int i = int(idx % m);
         const int64_t j = idx / m;
