@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstring>
+#include <memory>
 #include <numeric>
 
 #include "la.hpp"
@@ -471,7 +473,11 @@ void qr_direct(const std::vector<QrDesc>& d, cudaStream_t s) {
     if (!sj.empty()) {
         DevVec<QrJob> dj(sj, s);
         const size_t bytes = smax * sizeof(double);
-        H2B_CUDA(cudaFuncSetAttribute(qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
+        static const bool qr_attr = [] {   // once per process: the attribute call is a driver round trip
+            H2B_CUDA(cudaFuncSetAttribute(qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
+            return true;
+        }();
+        (void)qr_attr;
         qr_kernel<true><<<unsigned(sj.size()), 256, bytes, s>>>(dj.p);
         H2B_LAUNCH();
     }
@@ -590,7 +596,11 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     }
     if (!sj.empty()) {
         DevVec<SvdJob> dj(sj, s);
-        H2B_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
+        static const bool jacobi_attr = [] {
+            H2B_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
+            return true;
+        }();
+        (void)jacobi_attr;
         jacobi_kernel<true><<<unsigned(sj.size()), 256, smax * sizeof(double), s>>>(dj.p);
         H2B_LAUNCH();
     }
