@@ -69,6 +69,13 @@ __device__ __forceinline__ double carry_x(const double* __restrict__ coef, const
     return fma(cf[kHb], Xin[col * P + c], fma(cf[kWg], Yin[col * P + c], W[wpos(row, col, B)]));
 }
 
+// programmatic dependent launch: the march kernels are launched with the
+// programmatic-serialization attribute, so a kernel's launch and prologue
+// overlap its predecessor's tail; it waits here before touching the
+// predecessor's outputs (a no-op without the attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // One Crank-Nicolson step for every (chunk, column): finish x_j from its
 // carry form, consume it (state store / adjoint accumulation), form the
 // right-hand side A- x_j + f_j (Stepper::apply_minus, diffusion1d.hpp:203-209,
@@ -94,6 +101,7 @@ __global__ void __launch_bounds__(256, STEP_MINB) cn_step_kernel(StepArgs a, int
         double2* dst = reinterpret_cast<double2*>(cft);
         for (int e = threadIdx.x; e < nch * kL * kCoef / 2; e += blockDim.x) dst[e] = __ldg(src + e);
     }
+    pdl_wait();   // W, Yin, Xin come from the previous step's kernels
     const int lc = threadIdx.x / B;
     const int col = threadIdx.x - lc * B;
     const bool active = lc < nch;
@@ -230,6 +238,7 @@ __global__ void __launch_bounds__(256, STEP_MINB) cn_step_kernel(StepArgs a, int
         w[i] = v;
     }
     a.wstart[col * a.P + ch] = v;
+    pdl_trigger();
 #pragma unroll
     for (int i = 0; i < kL; ++i) a.Wn[(s0 + i) * B + col] = w[i];
 }
@@ -334,6 +343,7 @@ __device__ Aff warp_compose(const double* agg, int q0, int q1, bool desc) {
 
 __global__ void __launch_bounds__(kSeg) carry_fwd_reduce_kernel(CarryArgs a) {
     __shared__ Aff sm[32];
+    pdl_wait();
     const int seg = blockIdx.x, col = blockIdx.y;
     const Aff f = fwd_map(a, col, int64_t(seg) * kSeg + threadIdx.x);
     const Aff pre = block_exscan(f, false, sm);
@@ -346,6 +356,7 @@ __global__ void __launch_bounds__(kSeg) carry_fwd_reduce_kernel(CarryArgs a) {
 
 __global__ void __launch_bounds__(kSeg) carry_fwd_scan_kernel(CarryArgs a) {
     __shared__ Aff sm[32];
+    pdl_wait();
     __shared__ Aff run_s;
     const int seg = blockIdx.x, col = blockIdx.y;
     const int64_t c = int64_t(seg) * kSeg + threadIdx.x;
@@ -368,6 +379,7 @@ __global__ void __launch_bounds__(kSeg) carry_fwd_scan_kernel(CarryArgs a) {
 
 __global__ void __launch_bounds__(kSeg) carry_bwd_scan_kernel(CarryArgs a) {
     __shared__ Aff sm[32];
+    pdl_wait();
     __shared__ Aff run_s;
     const int seg = blockIdx.x, col = blockIdx.y;
     const int64_t c = int64_t(seg) * kSeg + threadIdx.x;
@@ -464,6 +476,23 @@ double ricker_wavelet(double t, double t_p) {   // ricker.hpp:12-19
 
 int grid_for(int64_t threads, int block) { return int((threads + block - 1) / block); }
 
+// launch with programmatic stream serialization (see pdl_wait)
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    H2B_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+    H2B_LAUNCH();
+}
+
 // the two-kernel Crank-Nicolson step over B columns, with its buffers
 struct Marcher {
     DeviceArray<double> W[2], zend, wstart, Yin, Xin, aggF, aggB;
@@ -542,22 +571,16 @@ struct Marcher {
     void step(bool has_prev, double* vr_out) {
         a.Wp = has_prev ? W[cur].data() : nullptr;
         a.Wn = W[cur ^ 1].data();
-        if (a.mode == 0)
-            cn_step_kernel<0><<<grid_for(a.P, cpb), cpb * a.B, smem, s>>>(a, cpb);
-        else if (a.mode == 1)
-            cn_step_kernel<1><<<grid_for(a.P, cpb), cpb * a.B, smem, s>>>(a, cpb);
-        else
-            cn_step_kernel<2><<<grid_for(a.P, cpb), cpb * a.B, smem, s>>>(a, cpb);
-        H2B_LAUNCH();
+        const dim3 gs(unsigned(grid_for(a.P, cpb))), bs(unsigned(cpb * a.B));
+        if (a.mode == 0) launch_pdl(cn_step_kernel<0>, gs, bs, smem, s, a, cpb);
+        else if (a.mode == 1) launch_pdl(cn_step_kernel<1>, gs, bs, smem, s, a, cpb);
+        else launch_pdl(cn_step_kernel<2>, gs, bs, smem, s, a, cpb);
         ca.W = a.Wn;
         ca.vr_out = vr_out;
         const dim3 g(unsigned(ca.nseg), unsigned(a.B));
-        carry_fwd_reduce_kernel<<<g, kSeg, 0, s>>>(ca);
-        H2B_LAUNCH();
-        carry_fwd_scan_kernel<<<g, kSeg, 0, s>>>(ca);
-        H2B_LAUNCH();
-        carry_bwd_scan_kernel<<<g, kSeg, 0, s>>>(ca);
-        H2B_LAUNCH();
+        launch_pdl(carry_fwd_reduce_kernel, g, dim3(kSeg), 0, s, ca);
+        launch_pdl(carry_fwd_scan_kernel, g, dim3(kSeg), 0, s, ca);
+        launch_pdl(carry_bwd_scan_kernel, g, dim3(kSeg), 0, s, ca);
         cur ^= 1;
     }
     const double* Wcur() const { return W[cur].data(); }
