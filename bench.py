@@ -218,7 +218,7 @@ def stage5_roofline(args, m, n, b, F5, stages):
         achieved = dom["gbytes"] / (dom["ms"] / 1e3)
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "peak_source": hbm_src}
-    kname = ("seg_gemm_kernel<64,32,2,2,2,32,VEC,kModeY> (leaf expansion + dense near-field)" if b > 2 else
+    kname = ("seg_gemm_kernel<64,32,4,1,2,32,VEC,kModeY> (leaf expansion + dense near-field)" if b > 2 else
              "sym_pass64_kernel (dense near-field, each canonical block streamed once) + seg_gemm leaf expansion "
              "+ csr_sum")
     roof.update({"kernel": kname, "share_of_step": dom["ms"] / sum(s["ms"] for s in stages.values()),
