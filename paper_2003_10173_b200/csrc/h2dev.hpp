@@ -76,9 +76,17 @@ struct HgemvGraph {
     Key key, last;
     cudaGraphExec_t exec = nullptr;
     cudaStream_t cap = nullptr;
+    // few-vector path: the dense near-field block pass runs on `lo` (least
+    // priority) beside the sweep chain on `hi` (greatest priority)
+    cudaStream_t hi = nullptr, lo = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ~HgemvGraph() {
         if (exec) cudaGraphExecDestroy(exec);
         if (cap) cudaStreamDestroy(cap);
+        if (hi) cudaStreamDestroy(hi);
+        if (lo) cudaStreamDestroy(lo);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
     }
 };
 

@@ -1290,6 +1290,20 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
 
 double g_plan_build_ms = 0;   // host wall time spent building plans (diagnostics)
 int g_small_b = 2;            // symmetric few-vector path for b <= this (0 = off)
+// few-vector path: run the dense near-field block pass (depends only on the
+// gathered x) on a least-priority stream concurrently with the latency-bound
+// sweep chain on a greatest-priority stream (0 = one stream)
+int g_dense_overlap = 1;
+
+// lazily create the fork/join streams and events of the overlapped few-vector path
+void ensure_side_streams(HgemvGraph& g) {
+    if (g.hi) return;
+    int least = 0, greatest = 0;
+    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    H2B_CUDA(cudaStreamCreateWithPriority(&g.hi, cudaStreamNonBlocking, greatest));
+    H2B_CUDA(cudaStreamCreateWithPriority(&g.lo, cudaStreamNonBlocking, least));
+    for (cudaEvent_t& e : g.ev) H2B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
 
 std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
     std::lock_guard<std::mutex> g(h.plan_mu);
@@ -1474,6 +1488,31 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                 EventTimer* timer, const HgemvPlan* dplan = nullptr, int phases = 3);
 }  // namespace
 
+namespace {
+// captured kernel nodes: the dense near-field block pass at least priority, every
+// other kernel (the sweep chain it overlaps) at greatest priority
+void set_node_priorities(cudaGraph_t graph) {
+    int least = 0, greatest = 0;
+    H2B_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    size_t nn = 0;
+    H2B_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    H2B_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    const void* lo1 = reinterpret_cast<const void*>(sym_pass64_kernel<1>);
+    const void* lo2 = reinterpret_cast<const void*>(sym_pass64_kernel<2>);
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        H2B_CUDA(cudaGraphNodeGetType(nd, &ty));
+        if (ty != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp{};
+        H2B_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+        cudaLaunchAttributeValue v{};
+        v.priority = (kp.func == lo1 || kp.func == lo2) ? least : greatest;
+        H2B_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
+    }
+}
+}  // namespace
+
 void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
            double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws) {
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
@@ -1520,7 +1559,12 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
         throw;
     }
     H2B_CUDA(cudaStreamEndCapture(g.cap, &graph));
-    H2B_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    unsigned long long iflags = 0;
+    if (g.hi) {   // keep the overlapped few-vector path's priorities inside the graph
+        set_node_priorities(graph);
+        iflags = cudaGraphInstantiateFlagUseNodePriority;
+    }
+    H2B_CUDA(cudaGraphInstantiateWithFlags(&g.exec, graph, iflags));
     cudaGraphDestroy(graph);
     g.key = k;
     H2B_CUDA(cudaGraphLaunch(g.exec, stream));
@@ -1590,6 +1634,20 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1), stream);
     if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
     const int* perm = user_order ? plan->perm->data() : nullptr;
+    if (plan->scratch_rows > 0 && ws.scratch.size() < size_t(plan->scratch_rows * b))
+        ws.scratch.resize(size_t(plan->scratch_rows * b), stream);
+    // few-vector path, unsharded, untimed: fork the sweep chain onto the greatest-priority
+    // stream and the dense block pass (after the gather) onto the least-priority one;
+    // both join back into the caller's stream before the dense slot sums / at the end
+    HgemvGraph& sg = ws.graph;
+    const cudaStream_t user_stream = stream;
+    const bool overlap = g_dense_overlap && plan->sym64 && phases == 3 && !timer && plan->num_leaves > 0;
+    if (overlap) {
+        ensure_side_streams(sg);
+        H2B_CUDA(cudaEventRecord(sg.ev[0], user_stream));
+        H2B_CUDA(cudaStreamWaitEvent(sg.hi, sg.ev[0], 0));
+        stream = sg.hi;
+    }
     if ((phases & 1) && plan->num_leaves > 0) {
         if (timer) timer->mark(stream);
         gather_blocked_kernel<<<plan->num_leaves, 256, 0, stream>>>(x, ldx, perm, plan->leaf_begin.data(),
@@ -1600,8 +1658,10 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
             timer->out->push_back({0, 0.f, 0.0, 16.0 * double(n * b)});
         }
     }
-    if (plan->scratch_rows > 0 && ws.scratch.size() < size_t(plan->scratch_rows * b))
-        ws.scratch.resize(size_t(plan->scratch_rows * b), stream);
+    if (overlap) {   // the dense pass may start once x is gathered
+        H2B_CUDA(cudaEventRecord(sg.ev[1], stream));
+        H2B_CUDA(cudaStreamWaitEvent(sg.lo, sg.ev[1], 0));
+    }
     for (const LaunchDesc& ld : plan->launches) {
         if (!(phases & (1 << ld.phase))) continue;
         if (ld.kind != 0) {
@@ -1616,13 +1676,18 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                 if (b == 1) sym_pass32_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
                 else sym_pass32_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
             } else if (ld.kind == 3 && plan->sym64) {
-                if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
-                else sym_pass64_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
+                const cudaStream_t ds = overlap ? sg.lo : stream;
+                if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, ds>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
+                else sym_pass64_kernel<2><<<grid, 256, 0, ds>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
             } else if (ld.kind == 1 || ld.kind == 3) {
                 const double* src = ld.kind == 1 ? ws.xhat.data() : ws.xint.data();
                 if (b == 1) sym_pass_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
                 else sym_pass_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
             } else {
+                if (overlap && ld.kind == 4) {   // dense slot sums wait for the dense pass
+                    H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
+                    H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[2], 0));
+                }
                 csr_sum_kernel<<<grid, 256, 0, stream>>>(plan->csr_units.data() + ld.item_begin, nitems, plan->csr_slots.data(),
                                                          ws.scratch.data(), b, ld.kind == 2 ? 0 : 1,
                                                          ld.kind == 2 ? ws.yhat.data() : y, perm, ldy, alpha);
@@ -1655,6 +1720,12 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                          (reinterpret_cast<uintptr_t>(ws.xint.data()) % 16 == 0);
         dispatch(a, ntasks, b, ld.mt, vec, ld.mode, stream);
         if (timer) timer->mark(stream);
+    }
+    if (overlap) {   // join both side streams back into the caller's stream
+        H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
+        H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[2], 0));
+        H2B_CUDA(cudaEventRecord(sg.ev[3], stream));
+        H2B_CUDA(cudaStreamWaitEvent(user_stream, sg.ev[3], 0));
     }
 }
 }  // namespace
@@ -1878,6 +1949,10 @@ extern "C" int h2b_tune(int which, int value) {
     }
     if (which == 7) {   // programmatic dependent launch on (1) / off (0)
         h2b::g_pdl = value;
+        return 0;
+    }
+    if (which == 8) {   // few-vector path: dense pass concurrent with the sweeps (1) / serial (0)
+        h2b::g_dense_overlap = value;
         return 0;
     }
     if (which < 0 || which > 3) return -1;

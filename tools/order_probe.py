@@ -3,7 +3,8 @@
   python tools/order_probe.py [--config cfg2] [--combos 0:0,1:0,1:1] [--reps 10]
 
 Each combo "e:t[:f]" sets h2b_tune(5, e) (entry order inside a task) and h2b_tune(6, t)
-(task order inside a launch), h2b_tune(7, f) (programmatic dependent launch), builds a fresh matrix (plans are cached per matrix),
+(task order inside a launch), h2b_tune(7, f) (programmatic dependent launch), h2b_tune(8, o)
+(few-vector path: dense pass concurrent with the sweeps), builds a fresh matrix (plans are cached per matrix),
 and prints per-stage CUDA-event times plus the whole-hgemv time of CUDA-graph
 replays. Every combo is checked against the first one (round-off only).
 Run under ncu with --kernel-name regex to read the DRAM bytes per combo.
@@ -44,7 +45,8 @@ def main():
     y = torch.empty(b, n, dtype=torch.float64, device="cuda").t()
     y0 = None
     for combo in a.combos.split(","):
-        e, t, f = (list(int(q) for q in combo.split(":")) + [1])[:3]
+        e, t, f, o = (list(int(q) for q in combo.split(":")) + [1, 1])[:4]
+        lib.h2b_tune(8, o)
         lib.h2b_tune(5, e)
         lib.h2b_tune(6, t)
         lib.h2b_tune(7, f)
@@ -69,11 +71,12 @@ def main():
         s1.record()
         torch.cuda.synchronize()
         ms = s0.elapsed_time(s1) / a.reps
-        print(f"entry {e} task {t} pdl {f}: hgemv {ms:.3f} ms  {line}  maxdiff {diff:.1e}", flush=True)
+        print(f"entry {e} task {t} pdl {f} overlap {o}: hgemv {ms:.3f} ms  {line}  maxdiff {diff:.1e}", flush=True)
         del m
     lib.h2b_tune(5, 1)
     lib.h2b_tune(6, 0)
     lib.h2b_tune(7, 1)
+    lib.h2b_tune(8, 1)
 
 
 if __name__ == "__main__":
