@@ -591,17 +591,32 @@ __global__ void __launch_bounds__(256) sym_pass32_kernel(const SymBlock* __restr
     }
     const bool want_w = d.w_off >= 0;
     double* w = want_w ? scratch + d.w_off * b : nullptr;
-    for (int j0 = 0; j0 < C; j0 += 16) {
+    // C <= 32: issue both 16-column halves' block and x loads before any reduction, so a
+    // warp's whole 8 KB block is in flight at once (one HBM latency round, not two)
+    double2 av[2][8];
+    double xv[2][8][B];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = 16 * h + 2 * k + half;
+            const bool vj = j < C;
+            av[h][k] = (vr && vj) ? __ldg(reinterpret_cast<const double2*>(d.A + int64_t(j) * d.lda + rr))
+                                  : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < B; ++q) xv[h][k][q] = vj ? __ldg(xs + j + q * C) : 0.0;
+        }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int j0 = 16 * h;
+        if (j0 >= C) break;
         double p[8][B];   // p[k]: partial of column j0 + 2k + half
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const int j = j0 + 2 * k + half;
-            const bool vj = j < C;
-            double2 a = make_double2(0.0, 0.0);
-            if (vr && vj) a = __ldg(reinterpret_cast<const double2*>(d.A + int64_t(j) * d.lda + rr));
+            const double2 a = av[h][k];
 #pragma unroll
             for (int q = 0; q < B; ++q) {
-                const double xj = vj ? __ldg(xs + j + q * C) : 0.0;
+                const double xj = xv[h][k][q];
                 ua[q] = fma(a.x, xj, ua[q]);
                 ub[q] = fma(a.y, xj, ub[q]);
                 p[k][q] = fma(a.x, xa[q], a.y * xb[q]);
@@ -815,7 +830,7 @@ struct HgemvPlan {
     DeviceArray<CsrUnit> csr_units;
     DeviceArray<int64_t> csr_slots;
     int64_t scratch_rows = 0;
-    bool sym32 = false;   // every coupling block has <= 32 even rows, 16-byte aligned
+    bool sym32 = false;   // every coupling block has <= 32 even rows and <= 32 columns, 16-byte aligned
     bool sym64 = false;   // every dense block has <= 64 even rows, 16-byte aligned
     std::once_flag accounted;
     DeviceArray<SegTask> tasks;
@@ -1109,7 +1124,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         sym_stage(bt.adm, h.s_off, h.S.data(), true, outs_v, outs_r, outs_u);
         bool ok32 = true;
         for (const SymBlock& sb : sblocks)
-            ok32 = ok32 && sb.R <= 32 && sb.R % 2 == 0 && sb.lda % 2 == 0 &&
+            ok32 = ok32 && sb.R <= 32 && sb.C <= 32 && sb.R % 2 == 0 && sb.lda % 2 == 0 &&
                    (reinterpret_cast<uintptr_t>(sb.A) % 16) == 0;
         plan->sym32 = ok32;
     }
