@@ -361,7 +361,7 @@ int h2c_hgemv_stage_times(h2c_matrix h, int transpose, int ordering, int64_t n, 
         need(h != nullptr && count != nullptr, "null argument");
         std::vector<h2b::StageRecord> rec;
         h2b::hgemv_timed(*h->h, transpose != 0, ordering == 0, n, b, x, ldx, y, ldy, 1.0, 0.0,
-                         static_cast<cudaStream_t>(stream), h->ws, rec);
+                         static_cast<cudaStream_t>(stream), h->ws_for(static_cast<cudaStream_t>(stream)), rec);
         *count = int(rec.size());
         for (int i = 0; i < int(rec.size()) && i < max_records; ++i) {
             if (stage) stage[i] = rec[size_t(i)].stage;

@@ -68,9 +68,14 @@ struct HgemvGraph {
         const double* x = nullptr;
         double* y = nullptr;
         double alpha = 0, beta = 0;
+        // the captured launches bake in the workspace buffers and the runtime
+        // knobs: a resized workspace or a toggled knob must not replay
+        const double *xint = nullptr, *xhat = nullptr, *yhat = nullptr, *scratch = nullptr;
+        uint64_t knobs = 0;
         bool operator==(const Key& o) const {
             return plan == o.plan && transpose == o.transpose && user == o.user && n == o.n && b == o.b &&
-                   ldx == o.ldx && ldy == o.ldy && x == o.x && y == o.y && alpha == o.alpha && beta == o.beta;
+                   ldx == o.ldx && ldy == o.ldy && x == o.x && y == o.y && alpha == o.alpha && beta == o.beta &&
+                   xint == o.xint && xhat == o.xhat && yhat == o.yhat && scratch == o.scratch && knobs == o.knobs;
         }
     };
     Key key, last;

@@ -1528,6 +1528,25 @@ void set_node_priorities(cudaGraph_t graph) {
 }
 }  // namespace
 
+namespace {
+// grow the per-stream scratch to what `plan` needs at b columns (before a graph
+// key is formed: a resize frees the old buffers a captured graph would replay)
+void reserve_workspace(const HgemvPlan& plan, int64_t n, int64_t b, cudaStream_t stream, Workspace& ws) {
+    const size_t need_x = size_t(n * b), need_u = size_t(plan.coef_up * b), need_d = size_t(plan.coef_down * b);
+    if (ws.xint.size() < need_x) ws.xint.resize(need_x, stream);
+    if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1), stream);
+    if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
+    if (plan.scratch_rows > 0 && ws.scratch.size() < size_t(plan.scratch_rows * b))
+        ws.scratch.resize(size_t(plan.scratch_rows * b), stream);
+}
+// the runtime knobs that change the launch sequence of an hgemv
+uint64_t knob_signature() {
+    uint64_t s = uint64_t(g_pdl & 0xff) | uint64_t(g_dense_overlap & 0xff) << 8;
+    for (int i = 0; i < 4; ++i) s |= uint64_t(g_tune[i] & 0xff) << (16 + 8 * i);
+    return s;
+}
+}  // namespace
+
 void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
            double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws) {
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
@@ -1536,6 +1555,7 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     if (h.shard_nranks > 0)
         throw std::invalid_argument("hgemv: this matrix holds one row-subtree shard; use the sharded hgemv");
     auto plan = select_plan(h, transpose, b);
+    reserve_workspace(*plan, n, b, stream, ws);
     HgemvGraph& g = ws.graph;
     HgemvGraph::Key k;
     k.plan = plan->id;
@@ -1549,6 +1569,11 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     k.y = y;
     k.alpha = alpha;
     k.beta = beta;
+    k.xint = ws.xint.data();
+    k.xhat = ws.xhat.data();
+    k.yhat = ws.yhat.data();
+    k.scratch = ws.scratch.data();
+    k.knobs = knob_signature();
     if (g.exec && g.key == k) {
         H2B_CUDA(cudaGraphLaunch(g.exec, stream));
         return;
@@ -1644,13 +1669,9 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     std::shared_ptr<HgemvPlan> own_plan;
     if (!dplan) own_plan = select_plan(h, transpose, b);
     const HgemvPlan* plan = dplan ? dplan : own_plan.get();
-    const size_t need_x = size_t(n * b), need_u = size_t(plan->coef_up * b), need_d = size_t(plan->coef_down * b);
-    if (ws.xint.size() < need_x) ws.xint.resize(need_x, stream);
-    if (ws.xhat.size() < std::max<size_t>(need_u, 1)) ws.xhat.resize(std::max<size_t>(need_u, 1), stream);
-    if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
+    reserve_workspace(*plan, n, b, stream, ws);
+    const size_t need_d = size_t(plan->coef_down * b);
     const int* perm = user_order ? plan->perm->data() : nullptr;
-    if (plan->scratch_rows > 0 && ws.scratch.size() < size_t(plan->scratch_rows * b))
-        ws.scratch.resize(size_t(plan->scratch_rows * b), stream);
     // few-vector path, unsharded, untimed: fork the sweep chain onto the greatest-priority
     // stream and the dense block pass (after the gather) onto the least-priority one;
     // both join back into the caller's stream before the dense slot sums / at the end
@@ -1938,11 +1959,10 @@ void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, in
 }
 
 int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
-    (void)b;
-    auto plan = get_plan(h, transpose);
-    int c = 1;   // gather
+    auto plan = select_plan(h, transpose, b);   // the plan hgemv actually runs at this b
+    int c = plan->num_leaves > 0 ? 1 : 0;       // gather
     for (const LaunchDesc& ld : plan->launches)
-        if (ld.task_end > ld.task_begin) ++c;
+        if (ld.kind == 0 ? ld.task_end > ld.task_begin : ld.item_end > ld.item_begin) ++c;
     return c;
 }
 

@@ -11,6 +11,7 @@ import ctypes as C
 import numpy as np
 
 from ._lib import H, check, lib
+from .h2 import col_major_geom
 
 
 def partition_owner(bt, nranks):
@@ -65,12 +66,13 @@ class DistPlan:
         return v.value
 
     def begin(self, x, sendbuf, b, stream=None):
-        check(lib.h2c_dist_hgemv_begin(self._h, int(b), x.data_ptr(), x.stride(1) if x.dim() == 2 else x.shape[0],
-                                       sendbuf.data_ptr(), stream))
+        _, ldx = col_major_geom(x)
+        check(lib.h2c_dist_hgemv_begin(self._h, int(b), x.data_ptr(), ldx, sendbuf.data_ptr(), stream))
 
     def end(self, recvbuf, y, b, alpha=1.0, beta=0.0, stream=None):
-        check(lib.h2c_dist_hgemv_end(self._h, int(b), recvbuf.data_ptr(), y.data_ptr(),
-                                     y.stride(1) if y.dim() == 2 else y.shape[0], float(alpha), float(beta), stream))
+        _, ldy = col_major_geom(y)
+        check(lib.h2c_dist_hgemv_end(self._h, int(b), recvbuf.data_ptr(), y.data_ptr(), ldy, float(alpha),
+                                     float(beta), stream))
 
 
 class ShardedHgemv:

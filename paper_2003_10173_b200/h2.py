@@ -16,6 +16,21 @@ import numpy as np
 from ._lib import H, check, lib
 
 
+def col_major_geom(t):
+    """(columns, leading dimension) of a column-major n x b tensor or a 1-D vector.
+
+    A contiguous (n, 1) tensor has strides (1, 1); its leading dimension is n."""
+    if t.dim() == 1:
+        return 1, t.shape[0]
+    if t.dim() != 2:
+        raise ValueError("hgemv: tensors must be 1-D or 2-D")
+    if t.shape[1] > 1 and t.stride(0) != 1:
+        raise ValueError("hgemv: tensors must be column-major (stride(0) == 1)")
+    if t.shape[1] == 1:
+        return 1, max(t.stride(1), t.shape[0])
+    return t.shape[1], t.stride(1)
+
+
 class Admissibility(enum.IntEnum):
     strong = 0
     weak = 1
@@ -309,12 +324,7 @@ class H2Matrix:
     def hgemv(self, x, y, transpose=False, ordering=Ordering.user, alpha=1.0, beta=0.0, stream=None):
         """Device path: y = alpha op(H) x + beta y on CUDA tensors (column-major
         n x b, i.e. stride(0) == 1, or 1-D)."""
-        def geom(t):
-            if t.dim() == 1:
-                return 1, t.shape[0]
-            if t.stride(0) != 1:
-                raise ValueError("hgemv: tensors must be column-major (stride(0) == 1)")
-            return t.shape[1], t.stride(1)
+        geom = col_major_geom
         if x.dtype != y.dtype or str(x.dtype) != "torch.float64":
             raise ValueError("hgemv: float64 tensors required")
         b, ldx = geom(x)

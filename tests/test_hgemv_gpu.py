@@ -184,3 +184,65 @@ def test_few_vector_dense_overlap_bitwise(cuda, b):
     assert torch.equal(out[0], out[1])
     expect = -0.75 * ora.matvec(x) + 0.5 * y0
     assert rel(out[1].cpu().numpy(), expect) <= TOL
+
+
+def test_graph_cache_survives_workspace_resize(cuda):
+    """b=1 twice (second call captures a graph), then b=64 on
+    the same workspace (grows and frees its buffers), then b=1 again with the
+    same x / y pointers must not replay the stale graph."""
+    import torch
+    pts = O.grid2d(48, 48)
+    ora, m, _ = pair(pts, 32, False, True, 8, seed=4)
+    n = pts.shape[0]
+    X = torch.zeros(64, n, dtype=torch.float64, device=cuda)
+    Y = torch.zeros(64, n, dtype=torch.float64, device=cuda)
+    x64 = O.gaussian(41, n, 64)
+    X[:, :] = torch.from_numpy(x64.T.copy())
+    x1, y1 = X[:1].T, Y[:1].T          # (n, 1) views sharing the first column's storage
+    xa, ya = X.T, Y.T
+    for b, xv, yv in ((1, x1, y1), (1, x1, y1), (64, xa, ya), (1, x1, y1), (1, x1, y1)):
+        yv.zero_()
+        m.hgemv(xv, yv)
+        torch.cuda.synchronize()
+        expect = ora.matvec(x64[:, :b])
+        assert rel(yv.cpu().numpy(), expect) <= TOL, b
+
+
+def test_column_vector_tensor_leading_dimension(cuda):
+    """A contiguous (n, 1) tensor has strides (1, 1); its leading dimension is n."""
+    import torch
+    pts = O.grid2d(20, 20)
+    ora, m, _ = pair(pts, 16, False, True, 6, seed=6)
+    n = pts.shape[0]
+    x = O.gaussian(43, n, 1)
+    xt = torch.from_numpy(x.copy()).to(cuda)
+    assert xt.stride() == (1, 1)
+    yt = torch.zeros(n, 1, dtype=torch.float64, device=cuda)
+    m.hgemv(xt, yt)
+    torch.cuda.synchronize()
+    assert rel(yt.cpu().numpy(), ora.matvec(x)) <= TOL
+
+
+def test_knob_toggle_does_not_replay_stale_graph(cuda):
+    """the graph key includes the runtime knobs (dense overlap)."""
+    import torch
+    from paper_2003_10173_b200._lib import lib
+    pts = O.grid2d(48, 48)
+    ora, m, _ = pair(pts, 32, False, True, 8, seed=8)
+    n = pts.shape[0]
+    x = O.gaussian(44, n, 1)
+    xt = torch.from_numpy(x.copy()).to(cuda)
+    yt = torch.zeros(n, 1, dtype=torch.float64, device=cuda)
+    outs = []
+    try:
+        for knob in (1, 1, 0, 0, 1):
+            lib.h2b_tune(8, knob)
+            yt.zero_()
+            m.hgemv(xt, yt)
+            torch.cuda.synchronize()
+            outs.append(yt.cpu().numpy().copy())
+    finally:
+        lib.h2b_tune(8, 1)
+    for o in outs:
+        assert rel(o, ora.matvec(x)) <= TOL
+        assert np.array_equal(o, outs[0])
