@@ -8,8 +8,20 @@
 #include <string>
 #include <thread>
 
+#ifdef ORA_REFERENCE_HEADERS
+// oracle/_ref build: the UNCHANGED reference headers (/root/reference/proj/
+// include/h2 + tests/test_support.hpp, compiled where they lie) over the
+// Eigen-API shim in oracle/eigen_shim. Same ora_* ABI as the restatement, so
+// the Python checker can load either library.
+#include "h2/algebra.hpp"
+#include "h2/construction.hpp"
+#include "h2/inversion.hpp"
+#include "h2/serialize.hpp"
+#include <test_support.hpp>   // the reference's, via -I$(REF)/tests (not ./test_support.hpp)
+#else
 #include "diffusion1d.hpp"
 #include "test_support.hpp"
+#endif
 
 using namespace h2;
 
@@ -97,6 +109,18 @@ int ora_tree_arrays(ora_tree* t, int64_t* perm, int64_t* begin, int64_t* end, in
         }
         for (size_t i = 0; i < bt.admissible_leaves().size(); ++i) adm[i] = bt.admissible_leaves()[i];
         for (size_t i = 0; i < bt.dense_leaves().size(); ++i) dense[i] = bt.dense_leaves()[i];
+    });
+}
+
+// per-node bounding boxes (point_set.hpp:68-70 BBox, cluster_tree.hpp:178-190), 3 per node
+int ora_tree_boxes(ora_tree* t, double* lo, double* hi) {
+    return guard([&] {
+        const auto& ct = *t->ct;
+        for (int v = 0; v < ct.num_nodes(); ++v)
+            for (int a = 0; a < 3; ++a) {
+                lo[3 * v + a] = ct.node(v).box.lo[size_t(a)];
+                hi[3 * v + a] = ct.node(v).box.hi[size_t(a)];
+            }
     });
 }
 
@@ -392,6 +416,7 @@ int ora_shuffle(int64_t n, uint64_t seed, int64_t* outp) {
     });
 }
 
+#ifndef ORA_REFERENCE_HEADERS
 // ---- diffusion1d Hessian at the target (oracle/diffusion1d.hpp) ----
 struct ora_diff1d {
     h2ora::Diff1DOracle d;
@@ -459,6 +484,8 @@ int ora_peel_diff1d(ora_tree* t, ora_diff1d* d, int include_tv, double eps, uint
         *o = new ora_h2{std::move(r.matrix)};
     });
 }
+
+#endif  // ORA_REFERENCE_HEADERS
 
 }  // extern "C"
 

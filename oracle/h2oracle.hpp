@@ -51,20 +51,34 @@ struct BBox {
     std::array<double, 3> lo{{0, 0, 0}}, hi{{0, 0, 0}};
     int dim = 0;
     double extent(int a) const { return hi[size_t(a)] - lo[size_t(a)]; }
-    double diameter() const {   // point_set.hpp:72-76
-        double s = 0;
-        // explicit fma: the reference builds with -march=native (CMakeLists.txt:10,18-20)
-        // and GCC contracts s += e*e, which decides exact admissibility ties on grids
-        for (int a = 0; a < dim; ++a) s = std::fma(extent(a), extent(a), s);
-        return std::sqrt(s);
+    // point_set.hpp:72-76 / 79-86 as the reference's Release build evaluates
+    // them (g++ 13 -O3 -march=native, proj/CMakeLists.txt:3-20, x86-64): the
+    // d<=3 loop is vectorised two lanes wide, so the first two squares are
+    // rounded and summed without contraction and a third is fused,
+    // fma(x2, x2, x0^2 + x1^2). Pinned by compiling the reference's own
+    // headers (oracle/_ref, tests/test_ref_parity.py); exact admissibility
+    // ties on grids depend on it (cfg4: 5,690,728 admissible leaves).
+    static double rsq(double x) {
+        double p = x * x;
+        asm("" : "+m"(p));   // keep the product rounded (no contraction into the add)
+        return p;
     }
-    double distance(const BBox& o) const {   // point_set.hpp:79-86
-        double s = 0;
-        for (int a = 0; a < dim; ++a) {
-            const double g = std::max({0.0, o.lo[size_t(a)] - hi[size_t(a)], lo[size_t(a)] - o.hi[size_t(a)]});
-            s = std::fma(g, g, s);
-        }
-        return std::sqrt(s);
+    static double release_sq_sum(const double* x, int d) {
+        if (d == 1) return rsq(x[0]);
+        double s = rsq(x[0]) + rsq(x[1]);
+        if (d == 3) s = std::fma(x[2], x[2], s);
+        return s;
+    }
+    double diameter() const {
+        double e[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a) e[a] = extent(a);
+        return std::sqrt(release_sq_sum(e, dim));
+    }
+    double distance(const BBox& o) const {
+        double g[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a)
+            g[a] = std::max({0.0, o.lo[size_t(a)] - hi[size_t(a)], lo[size_t(a)] - o.hi[size_t(a)]});
+        return std::sqrt(release_sq_sum(g, dim));
     }
     int longest_axis() const {   // point_set.hpp:96-102 (strictly larger wins)
         int best = 0;

@@ -12,7 +12,11 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "build", "liboracle.so")
+# oracle/pyref.py executes this same source with _LIB_OVERRIDE set to the
+# reference-compiled library (oracle/_ref/libh2ref.so: the reference's own
+# headers over the Eigen shim), which exports the same ora_* ABI.
+_REF_BUILD = "_LIB_OVERRIDE" in globals()
+LIB_PATH = globals().get("_LIB_OVERRIDE") or os.path.join(_HERE, "build", "liboracle.so")
 
 
 def build():
@@ -20,7 +24,12 @@ def build():
 
 
 if not os.path.exists(LIB_PATH):
-    build()
+    if _REF_BUILD:
+        subprocess.run(["make", "-s", "-C", _HERE, "ref"], check=True)
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built and /root/reference is absent")
+    else:
+        build()
 
 _lib = C.CDLL(LIB_PATH)
 vp, i32, i64, u64, f64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double
@@ -28,6 +37,8 @@ P = C.POINTER
 
 
 def _sig(name, *args):
+    if _REF_BUILD and not hasattr(_lib, name):
+        return   # restatement-only entry (e.g. the diffusion oracle)
     f = getattr(_lib, name)
     f.restype = i32
     f.argtypes = list(args)
@@ -39,6 +50,7 @@ _lib.ora_tree_destroy.argtypes = [vp]
 _lib.ora_tree_destroy.restype = None
 _sig("ora_tree_info", vp, P(i64), P(i32), P(i32), P(i32), P(i32), P(i32))
 _sig("ora_tree_arrays", vp, *([vp] * 12))
+_sig("ora_tree_boxes", vp, vp, vp)
 _sig("ora_random_h2", vp, i32, i64, u64, P(vp))
 _sig("ora_zero", vp, i32, P(vp))
 _sig("ora_fixed_rank_h2", vp, i64, u64, i32, P(vp))
@@ -60,8 +72,9 @@ _sig("ora_pnorm2_dense", vp, i64, i32, P(f64), P(i32))
 _sig("ora_gaussian", u64, i64, i64, vp)
 _sig("ora_shuffle", i64, u64, vp)
 _sig("ora_diff1d_create", i64, i64, f64, f64, f64, f64, f64, f64, f64, i32, vp, i64, P(vp))
-_lib.ora_diff1d_destroy.argtypes = [vp]
-_lib.ora_diff1d_destroy.restype = None
+if hasattr(_lib, "ora_diff1d_destroy"):
+    _lib.ora_diff1d_destroy.argtypes = [vp]
+    _lib.ora_diff1d_destroy.restype = None
 _sig("ora_diff1d_info", vp, P(i64), P(i64), P(f64), P(f64), P(i64))
 _sig("ora_diff1d_hessvec", vp, i64, vp, vp, i32, i32)
 _sig("ora_diff1d_state", vp, i32, vp)
@@ -126,6 +139,13 @@ class Tree:
         _check(_lib.ora_tree_arrays(h, *[_p(a) for a in (self.perm, self.begin, self.end, self.level, self.parent,
                                                           self.child0, self.child1, self.brow, self.bcol, self.btag,
                                                           self.adm, self.dense)]))
+
+    def boxes(self):
+        """(lo, hi), each num_nodes x 3 (unused axes 0)."""
+        lo = np.zeros((self.num_nodes, 3))
+        hi = np.zeros((self.num_nodes, 3))
+        _check(_lib.ora_tree_boxes(self._h, _p(lo), _p(hi)))
+        return lo, hi
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -100,22 +100,40 @@ int64_t ClusterTree::max_leaf_size() const {
     return m;
 }
 
+namespace {
+// x*x rounded to double and opaque to the optimiser, so no later add can be
+// contracted into an FMA with it
+inline double rounded_square(double x) {
+    double p = x * x;
+    asm("" : "+m"(p));
+    return p;
+}
+// sum of squares of the (<= 3) box extents / gaps exactly as the reference's
+// Release build evaluates point_set.hpp:72-76 / 79-86 (g++ 13 -O3
+// -march=native on x86-64, proj/CMakeLists.txt:3-20): the loop is vectorised
+// two lanes wide, so the first two squares are rounded and added without
+// contraction, and a third term is fused as fma(x2, x2, x0^2 + x1^2).
+// Verified against the reference headers compiled unchanged (oracle/_ref):
+// cfg4's block tree then matches the reference's counts exactly.
+inline double release_sq_sum(const double* x, int dim) {
+    if (dim == 1) return rounded_square(x[0]);
+    double s = rounded_square(x[0]) + rounded_square(x[1]);
+    if (dim == 3) s = std::fma(x[2], x[2], s);
+    return s;
+}
+}  // namespace
+
 double ClusterTree::diameter(int v) const {
-    double s = 0;
-    for (int a = 0; a < dim; ++a) {
-        const double e = hi[size_t(3 * v + a)] - lo[size_t(3 * v + a)];
-        s = std::fma(e, e, s);   // contracted like the reference's -march=native build
-    }
-    return std::sqrt(s);
+    double e[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) e[a] = hi[size_t(3 * v + a)] - lo[size_t(3 * v + a)];
+    return std::sqrt(release_sq_sum(e, dim));
 }
 
 double ClusterTree::distance(int v, int w) const {
-    double s = 0;
-    for (int a = 0; a < dim; ++a) {
-        const double g = std::max({0.0, lo[size_t(3 * w + a)] - hi[size_t(3 * v + a)], lo[size_t(3 * v + a)] - hi[size_t(3 * w + a)]});
-        s = std::fma(g, g, s);
-    }
-    return std::sqrt(s);
+    double g[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a)
+        g[a] = std::max({0.0, lo[size_t(3 * w + a)] - hi[size_t(3 * v + a)], lo[size_t(3 * v + a)] - hi[size_t(3 * w + a)]});
+    return std::sqrt(release_sq_sum(g, dim));
 }
 
 std::shared_ptr<ClusterTree> build_cluster_tree(const double* coords, int64_t n, int dim, int64_t leaf_size) {
