@@ -191,6 +191,47 @@ int h2c_peel_construct(h2c_operator op, h2c_block_tree bt, const h2c_peel_config
 /* estimate_relative_error(op, h, op_norm) (construction.hpp:537-546) */
 int h2c_estimate_relative_error(h2c_operator op, h2c_matrix h, double op_norm, double* out);
 
+/* ---- block-level construction primitives (construction.hpp:137-198) ----
+ * The reference threads one std::mt19937_64 through its samplers by reference;
+ * h2c_rng is that stream (normals drawn exactly as detail::fill_gaussian). */
+typedef struct h2c_rng_s* h2c_rng;
+int h2c_rng_create(uint64_t seed, h2c_rng* out);
+void h2c_rng_destroy(h2c_rng r);
+/* sample_block_column(op, ct, t, s, count, rng) (construction.hpp:137-148):
+ * omega_s (|s| x count, ld |s|) and y_t = op(Omega) on the rows of t
+ * (|t| x count, ld |t|); device buffers, cluster (internal) row order */
+int h2c_sample_block_column(h2c_operator op, h2c_cluster_tree ct, int t, int s, int64_t count, h2c_rng rng,
+                            double* omega_s, double* y_t, void* stream);
+/* adaptive_block_factorization(op, ct, t, s, eps_block, cfg) (construction.hpp:156-198);
+ * BlockFactor (:150-154): u (|t| x rank, orthonormal), v (|s| x rank), err_est.
+ * A rank above cfg->max_rank returns H2C_MAX_RANK_ERROR (max_rank_error). */
+typedef struct h2c_block_factor_s* h2c_block_factor;
+int h2c_adaptive_block_factorization(h2c_operator op, h2c_cluster_tree ct, int t, int s, double eps_block,
+                                     const h2c_peel_config* cfg, h2c_block_factor* out);
+int h2c_block_factor_info(h2c_block_factor f, int64_t* rows_u, int64_t* rows_v, int64_t* rank, double* err_est);
+/* u, v to host buffers (column-major, cluster row order) */
+int h2c_block_factor_download(h2c_block_factor f, double* u, double* v);
+void h2c_block_factor_destroy(h2c_block_factor f);
+
+/* ---- algebra and diagnostics (algebra.hpp:119-137, 323-332; h2_matrix.hpp:128-196, 308-404) */
+/* local_low_rank_update(h, t, s, U, V, eps): U (|t| x k, ld ldu), V (|s| x k, ld ldv)
+ * device factors in cluster (internal) row order, added on the (t, s) region
+ * (a block-tree node), then recompressed to eps */
+int h2c_local_low_rank_update(h2c_matrix h, int t, int s, int64_t k, const double* U, int64_t ldu, const double* V,
+                              int64_t ldv, double eps, h2c_matrix* out);
+/* frobenius_norm(h): requires orthonormal bases (H2C_INVALID_ARGUMENT otherwise) */
+int h2c_frobenius_norm(h2c_matrix h, double* out);
+/* H2Matrix::to_dense(cap): n x n host buffer, column-major, user ordering;
+ * H2C_INVALID_ARGUMENT when n > cap */
+int h2c_to_dense(h2c_matrix h, int64_t cap, double* a);
+/* H2Matrix::validate(ortho_cap) -> ValidationReport: *num_violations, the
+ * messages '\n'-separated into `messages` (truncated to message_bytes incl.
+ * the terminator), rank_profile() into level_max_rank (up to max_levels;
+ * *num_levels = depth + 1) and storage() as {dense, leaf_basis, transfer,
+ * coupling} reals. Any output pointer may be NULL. */
+int h2c_validate(h2c_matrix h, int64_t ortho_cap, int* num_violations, char* messages, int64_t message_bytes,
+                 int64_t* level_max_rank, int max_levels, int* num_levels, int64_t* storage);
+
 /* ---- row-subtree sharded hgemv (one process per GPU) ------
  * Rank r of P (power of two) owns the subtree under the r-th node of tree level
  * log2 P; levels above are replicated. One hgemv = begin (owned upsweep, pack

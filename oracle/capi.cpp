@@ -383,6 +383,68 @@ int ora_peel_h2(ora_tree* t, ora_h2* src, double eps, uint64_t seed, double norm
     });
 }
 
+// sample_block_column(DenseOperator(a), ct, t, s, count, mt19937_64(seed))
+// (construction.hpp:137-148): omega_s |s| x count, y_t |t| x count
+int ora_sample_block_column(ora_tree* t, const double* a, int symmetric, int tt, int ss, int64_t count, uint64_t seed,
+                            double* omega_s, double* y_t) {
+    return guard([&] {
+        const Index n = t->ct->n();
+        DenseOperator op(wrap(a, n, n), symmetric != 0);
+        std::mt19937_64 rng(seed);
+        auto [om, y] = sample_block_column(op, *t->ct, tt, ss, count, rng);
+        out(om, omega_s);
+        out(y, y_t);
+    });
+}
+
+// adaptive_block_factorization(DenseOperator(a), ct, t, s, eps_block, cfg)
+// (construction.hpp:156-198); u, v sized |t| x (|t| + b), |s| x (|t| + b) by
+// the caller; *cols = columns the operator applied
+int ora_adaptive_block_factorization(ora_tree* t, const double* a, int symmetric, int tt, int ss, double eps_block,
+                                     int64_t b, int64_t p, int64_t max_rank, uint64_t seed, double* u, double* v,
+                                     int64_t* rank, double* err_est, int64_t* cols) {
+    return guard([&] {
+        const Index n = t->ct->n();
+        DenseOperator op(wrap(a, n, n), symmetric != 0);
+        PeelConfig cfg;
+        cfg.sample_block_size = b;
+        cfg.oversampling = p;
+        cfg.max_rank = max_rank;
+        cfg.seed = seed;
+        op.reset_counter();
+        BlockFactor f = adaptive_block_factorization(op, *t->ct, tt, ss, eps_block, cfg);
+        *rank = f.rank;
+        *err_est = f.err_est;
+        *cols = op.columns_applied();
+        out(f.u, u);
+        out(f.v, v);
+    });
+}
+
+// local_low_rank_update(h, t, s, U, V, eps) (algebra.hpp:323-332); U |t| x k, V |s| x k
+int ora_local_low_rank_update(ora_h2* h, int tt, int ss, int64_t k, const double* U, const double* V, double eps,
+                              ora_h2** o) {
+    return guard([&] {
+        const auto& ct = *h->h.tree;
+        *o = new ora_h2{local_low_rank_update(h->h, tt, ss, wrap(U, ct.node(tt).size(), k),
+                                              wrap(V, ct.node(ss).size(), k), eps)};
+    });
+}
+
+// H2Matrix::validate(ortho_cap) (h2_matrix.hpp:308-404): violation count,
+// rank_profile (depth + 1 entries) and storage {dense, leaf, transfer, coupling}
+int ora_validate(ora_h2* h, int64_t ortho_cap, int* num_violations, int64_t* level_max_rank, int64_t* storage) {
+    return guard([&] {
+        auto rep = h->h.validate(ortho_cap);
+        *num_violations = int(rep.violations.size());
+        for (size_t i = 0; i < rep.level_max_rank.size(); ++i) level_max_rank[i] = rep.level_max_rank[i];
+        storage[0] = rep.storage.dense_reals;
+        storage[1] = rep.storage.leaf_basis_reals;
+        storage[2] = rep.storage.transfer_reals;
+        storage[3] = rep.storage.coupling_reals;
+    });
+}
+
 // pnorm_estimate(op, 2) of a dense operator (linear_operator.hpp:127-153)
 int ora_pnorm2_dense(const double* a, int64_t n, int symmetric, double* v, int* iters) {
     return guard([&] {

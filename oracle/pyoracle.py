@@ -69,6 +69,11 @@ _sig("ora_frobenius_norm", vp, P(f64))
 _sig("ora_peel_dense", vp, vp, i32, f64, i64, i64, i64, u64, f64, P(vp), P(i64), vp, vp, P(i32))
 _sig("ora_peel_h2", vp, vp, f64, u64, f64, P(vp), P(i64))
 _sig("ora_pnorm2_dense", vp, i64, i32, P(f64), P(i32))
+_sig("ora_sample_block_column", vp, vp, i32, i32, i32, i64, u64, vp, vp)
+_sig("ora_adaptive_block_factorization", vp, vp, i32, i32, i32, f64, i64, i64, i64, u64, vp, vp, P(i64), P(f64),
+     P(i64))
+_sig("ora_local_low_rank_update", vp, i32, i32, i64, vp, vp, f64, P(vp))
+_sig("ora_validate", vp, i64, P(i32), vp, vp)
 _sig("ora_gaussian", u64, i64, i64, vp)
 _sig("ora_shuffle", i64, u64, vp)
 _sig("ora_diff1d_create", i64, i64, f64, f64, f64, f64, f64, f64, f64, i32, vp, i64, P(vp))
@@ -247,6 +252,21 @@ class H2:
         _check(_lib.ora_low_rank_update(self._h, X.shape[1], _p(X), _p(Y), float(eps), C.byref(h)))
         return H2(h, self.tree)
 
+    def local_low_rank_update(self, t, s, U, V, eps):
+        U = np.asfortranarray(U, np.float64)
+        V = np.asfortranarray(V, np.float64)
+        h = vp()
+        _check(_lib.ora_local_low_rank_update(self._h, int(t), int(s), U.shape[1], _p(U), _p(V), float(eps),
+                                              C.byref(h)))
+        return H2(h, self.tree)
+
+    def validate(self, ortho_cap=4096):
+        nv = i32()
+        prof = np.zeros(self.tree.depth + 1, np.int64)
+        st = np.zeros(4, np.int64)
+        _check(_lib.ora_validate(self._h, int(ortho_cap), C.byref(nv), _p(prof), _p(st)))
+        return nv.value, prof.tolist(), st.tolist()
+
     def frobenius_norm(self):
         v = f64()
         _check(_lib.ora_frobenius_norm(self._h, C.byref(v)))
@@ -272,6 +292,35 @@ def peel_h2(tree, src, eps=1e-4, seed=42, norm_scale=0.0):
     tot = i64()
     _check(_lib.ora_peel_h2(tree._h, src._h, float(eps), int(seed), float(norm_scale), C.byref(h), C.byref(tot)))
     return H2(h, tree), tot.value
+
+
+def sample_block_column(tree, a, symmetric, t, s, count, seed):
+    """sample_block_column over DenseOperator(a) with a fresh mt19937_64(seed)."""
+    a = np.asfortranarray(a, np.float64)
+    ms = int(tree.end[s] - tree.begin[s])
+    mt = int(tree.end[t] - tree.begin[t])
+    om = np.empty((ms, count), order="F")
+    y = np.empty((mt, count), order="F")
+    _check(_lib.ora_sample_block_column(tree._h, _p(a), int(symmetric), int(t), int(s), int(count), int(seed),
+                                        _p(om), _p(y)))
+    return om, y
+
+
+def adaptive_block_factorization(tree, a, symmetric, t, s, eps_block, b=16, p=10, max_rank=0, seed=42):
+    """-> (u, v, rank, err_est, columns applied) (construction.hpp:156-198)."""
+    a = np.asfortranarray(a, np.float64)
+    ms = int(tree.end[s] - tree.begin[s])
+    mt = int(tree.end[t] - tree.begin[t])
+    kc = mt + b
+    u = np.empty(mt * kc)
+    v = np.empty(ms * kc)
+    k, e, cols = i64(), f64(), i64()
+    _check(_lib.ora_adaptive_block_factorization(tree._h, _p(a), int(symmetric), int(t), int(s), float(eps_block),
+                                                 int(b), int(p), int(max_rank), int(seed), _p(u), _p(v), C.byref(k),
+                                                 C.byref(e), C.byref(cols)))
+    k = k.value
+    return (u[:mt * k].reshape((mt, k), order="F"), v[:ms * k].reshape((ms, k), order="F"), k, e.value,
+            cols.value)
 
 
 def pnorm2_dense(a, symmetric):

@@ -190,6 +190,17 @@ def check(rc):   # noqa: F811  (extends the mapping with io_error)
     _check_base(rc)
 
 
+_sig("h2c_rng_create", i32, C.c_uint64, P(H))
+_sig("h2c_rng_destroy", None, H)
+_sig("h2c_sample_block_column", i32, H, H, i32, i32, i64, H, vp, vp, vp)
+_sig("h2c_adaptive_block_factorization", i32, H, H, i32, i32, f64, P(PeelConfigC), P(H))
+_sig("h2c_block_factor_info", i32, H, P(i64), P(i64), P(i64), P(f64))
+_sig("h2c_block_factor_download", i32, H, vp, vp)
+_sig("h2c_block_factor_destroy", None, H)
+_sig("h2c_local_low_rank_update", i32, H, i32, i32, i64, vp, i64, vp, i64, f64, P(H))
+_sig("h2c_frobenius_norm", i32, H, P(f64))
+_sig("h2c_to_dense", i32, H, i64, vp)
+_sig("h2c_validate", i32, H, i64, P(i32), C.c_char_p, i64, vp, i32, P(i32), vp)
 _sig("h2c_serialize_size", i32, H, P(i64))
 _sig("h2c_serialize", i32, H, vp, i64)
 _sig("h2c_deserialize", i32, vp, i64, P(H), P(H))

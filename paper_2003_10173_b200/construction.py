@@ -176,6 +176,87 @@ def estimate_relative_error(op, m, op_norm=0.0):
     return v.value
 
 
+def frobenius_norm(m):
+    """frobenius_norm(h) (algebra.hpp:119-137); needs orthonormal bases."""
+    v = C.c_double()
+    check(lib.h2c_frobenius_norm(m._h, C.byref(v)))
+    return v.value
+
+
+def local_low_rank_update(m, t, s, U, V, eps):
+    """local_low_rank_update(h, t, s, U_blk, V_blk, eps) (algebra.hpp:323-332):
+    U (|t| x k), V (|s| x k) host arrays in cluster (internal) row order."""
+    import torch
+    U = np.asarray(U, np.float64)
+    V = np.asarray(V, np.float64)
+    U = U[:, None] if U.ndim == 1 else U
+    V = V[:, None] if V.ndim == 1 else V
+    ct = m.blocks.tree
+    if U.shape[0] != ct.size(t) or V.shape[0] != ct.size(s) or U.shape[1] != V.shape[1]:
+        raise ValueError("local update: factor dimensions do not match clusters")
+    k = U.shape[1]
+    ud = torch.from_numpy(np.ascontiguousarray(U.T)).cuda()
+    same = U.shape == V.shape and np.array_equal(U.view(np.uint64), V.view(np.uint64))
+    vd = ud if same else torch.from_numpy(np.ascontiguousarray(V.T)).cuda()
+    out = H()
+    check(lib.h2c_local_low_rank_update(m._h, int(t), int(s), k, ud.data_ptr(), max(U.shape[0], 1), vd.data_ptr(),
+                                        max(V.shape[0], 1), float(eps), C.byref(out)))
+    torch.cuda.synchronize()
+    return H2Matrix(out, m.blocks)
+
+
+class Rng:
+    """The std::mt19937_64 stream the reference threads through its samplers."""
+
+    def __init__(self, seed):
+        self._h = H()
+        check(lib.h2c_rng_create(int(seed), C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.h2c_rng_destroy(self._h)
+            self._h = None
+
+
+def sample_block_column(op, ct, t, s, count, rng):
+    """sample_block_column(op, ct, t, s, count, rng) (construction.hpp:137-148) ->
+    (Omega restricted to s, op(Omega) restricted to t), host arrays in cluster order."""
+    import torch
+    ms, mt = ct.size(s), ct.size(t)
+    om = torch.empty((max(int(count), 0), ms), dtype=torch.float64, device="cuda")
+    y = torch.empty((max(int(count), 0), mt), dtype=torch.float64, device="cuda")
+    check(lib.h2c_sample_block_column(op._h, ct._h, int(t), int(s), int(count), rng._h, om.data_ptr(), y.data_ptr(),
+                                      None))
+    torch.cuda.synchronize()
+    return om.cpu().numpy().T, y.cpu().numpy().T
+
+
+@dataclasses.dataclass
+class BlockFactor:   # construction.hpp:150-154
+    u: np.ndarray
+    v: np.ndarray
+    rank: int
+    err_est: float
+
+
+def adaptive_block_factorization(op, ct, t, s, eps_block, cfg=None):
+    """adaptive_block_factorization(op, ct, t, s, eps_block, cfg) (construction.hpp:156-198)."""
+    cfg = cfg or PeelConfig()
+    c = _cfg_c(cfg)
+    h = H()
+    check(lib.h2c_adaptive_block_factorization(op._h, ct._h, int(t), int(s), float(eps_block), C.byref(c),
+                                               C.byref(h)))
+    try:
+        ru, rv, k, e = C.c_int64(), C.c_int64(), C.c_int64(), C.c_double()
+        check(lib.h2c_block_factor_info(h, C.byref(ru), C.byref(rv), C.byref(k), C.byref(e)))
+        u = np.empty((ru.value, k.value), order="F")
+        v = np.empty((rv.value, k.value), order="F")
+        check(lib.h2c_block_factor_download(h, u.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
+    finally:
+        lib.h2c_block_factor_destroy(h)
+    return BlockFactor(u, v, int(k.value), float(e.value))
+
+
 def _cfg_c(cfg):
     return PeelConfigC(float(cfg.eps), int(cfg.sample_block_size), int(cfg.oversampling), int(cfg.max_rank),
                        int(cfg.seed), float(cfg.norm_scale), int(cfg.crossover_rank_cap), int(cfg.rng))

@@ -17,6 +17,7 @@
 #include "advdiff.hpp"
 #include "serialize.hpp"
 #include "matrix.hpp"
+#include "blockops.hpp"
 
 struct h2c_cluster_tree_s {
     std::shared_ptr<h2b::ClusterTree> t;
@@ -48,6 +49,13 @@ struct h2c_lowrank_s {
 };
 struct h2c_operator_s {
     std::unique_ptr<h2b::DevOperator> op;
+};
+struct h2c_rng_s {
+    std::mt19937_64 g;
+};
+struct h2c_block_factor_s {
+    h2b::BlockFactorDev f;
+    int64_t rows_u = 0, rows_v = 0;
 };
 
 namespace {
@@ -1080,6 +1088,104 @@ int h2c_advdiff_operator(h2c_advdiff a, h2c_operator* out) {
     return guard([&] {
         need(a != nullptr && out != nullptr, "null argument");
         *out = new h2c_operator_s{h2b::advdiff_hessian_operator(a->a)};
+    });
+}
+
+
+// ---- block-level construction primitives (construction.hpp:137-198) -------------
+int h2c_rng_create(uint64_t seed, h2c_rng* out) {
+    return guard([&] {
+        need(out != nullptr, "null output handle");
+        *out = new h2c_rng_s{std::mt19937_64(seed)};
+    });
+}
+void h2c_rng_destroy(h2c_rng r) { delete r; }
+
+int h2c_sample_block_column(h2c_operator op, h2c_cluster_tree ct, int t, int s, int64_t count, h2c_rng rng,
+                            double* omega_s, double* y_t, void* stream) {
+    return guard([&] {
+        need(op != nullptr && ct != nullptr && rng != nullptr, "null argument");
+        need(omega_s != nullptr && y_t != nullptr, "null output buffer");
+        need(op->op->dim() == ct->t->n, "sample_block_column: operator and tree sizes differ");
+        h2b::sample_block_column(*op->op, *ct->t, t, s, count, rng->g, omega_s, y_t,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_adaptive_block_factorization(h2c_operator op, h2c_cluster_tree ct, int t, int s, double eps_block,
+                                     const h2c_peel_config* cfg, h2c_block_factor* out) {
+    return guard([&] {
+        need(op != nullptr && ct != nullptr && out != nullptr, "null argument");
+        need(op->op->dim() == ct->t->n, "adaptive_block_factorization: operator and tree sizes differ");
+        auto f = std::make_unique<h2c_block_factor_s>();
+        f->f = h2b::adaptive_block_factorization(*op->op, *ct->t, t, s, eps_block, to_cfg(cfg), nullptr);
+        f->rows_u = ct->t->size(t);
+        f->rows_v = ct->t->size(s);
+        *out = f.release();
+    });
+}
+int h2c_block_factor_info(h2c_block_factor f, int64_t* rows_u, int64_t* rows_v, int64_t* rank, double* err_est) {
+    return guard([&] {
+        need(f != nullptr, "null block factor");
+        if (rows_u) *rows_u = f->rows_u;
+        if (rows_v) *rows_v = f->rows_v;
+        if (rank) *rank = f->f.rank;
+        if (err_est) *err_est = f->f.err_est;
+    });
+}
+int h2c_block_factor_download(h2c_block_factor f, double* u, double* v) {
+    return guard([&] {
+        need(f != nullptr, "null block factor");
+        const size_t nu = size_t(f->rows_u * f->f.rank), nv = size_t(f->rows_v * f->f.rank);
+        if (u && nu) H2B_CUDA(cudaMemcpy(u, f->f.u.data(), nu * sizeof(double), cudaMemcpyDeviceToHost));
+        if (v && nv) H2B_CUDA(cudaMemcpy(v, f->f.v.data(), nv * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+void h2c_block_factor_destroy(h2c_block_factor f) { delete f; }
+
+// ---- algebra and diagnostics -------------------------------------------------------
+int h2c_local_low_rank_update(h2c_matrix h, int t, int s, int64_t k, const double* U, int64_t ldu, const double* V,
+                              int64_t ldv, double eps, h2c_matrix* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        *out = wrap_matrix(h2b::local_low_rank_update(*h->h, t, s, k, U, ldu, V, ldv, eps, nullptr));
+    });
+}
+int h2c_frobenius_norm(h2c_matrix h, double* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        *out = h2b::frobenius_norm(*h->h, nullptr);
+    });
+}
+int h2c_to_dense(h2c_matrix h, int64_t cap, double* a) {
+    return guard([&] {
+        need(h != nullptr && a != nullptr, "null argument");
+        h2b::to_dense(*h->h, cap, a, nullptr);
+    });
+}
+int h2c_validate(h2c_matrix h, int64_t ortho_cap, int* num_violations, char* messages, int64_t message_bytes,
+                 int64_t* level_max_rank, int max_levels, int* num_levels, int64_t* storage) {
+    return guard([&] {
+        need(h != nullptr, "null matrix");
+        const h2b::ValidationReportDev r = h2b::validate(*h->h, ortho_cap, nullptr);
+        if (num_violations) *num_violations = int(r.violations.size());
+        if (messages && message_bytes > 0) {
+            std::string all;
+            for (size_t i = 0; i < r.violations.size(); ++i) all += (i ? "\n" : "") + r.violations[i];
+            const size_t nb = std::min<size_t>(all.size(), size_t(message_bytes - 1));
+            std::memcpy(messages, all.data(), nb);
+            messages[nb] = 0;
+        }
+        if (num_levels) *num_levels = int(r.level_max_rank.size());
+        if (level_max_rank)
+            for (int i = 0; i < max_levels && i < int(r.level_max_rank.size()); ++i)
+                level_max_rank[i] = r.level_max_rank[size_t(i)];
+        if (storage) {
+            storage[0] = r.storage.dense_reals;
+            storage[1] = r.storage.leaf_basis_reals;
+            storage[2] = r.storage.transfer_reals;
+            storage[3] = r.storage.coupling_reals;
+        }
     });
 }
 

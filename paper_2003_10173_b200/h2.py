@@ -9,6 +9,7 @@ reference takes an Eigen Matrix by value, device torch tensors where a
 caller wants to stay on the GPU.
 """
 import ctypes as C
+import dataclasses
 import enum
 
 import numpy as np
@@ -192,6 +193,27 @@ def build_block_tree(rows, cols, eta, mode=Admissibility.strong):
 _PARTS = ("U", "E", "V", "F", "S", "D")
 
 
+@dataclasses.dataclass
+class StorageReport:   # h2_matrix.hpp:25-31
+    dense_reals: int
+    leaf_basis_reals: int
+    transfer_reals: int
+    coupling_reals: int
+
+    def total(self):
+        return self.dense_reals + self.leaf_basis_reals + self.transfer_reals + self.coupling_reals
+
+
+@dataclasses.dataclass
+class ValidationReport:   # h2_matrix.hpp:33-38
+    violations: list
+    level_max_rank: list
+    storage: StorageReport
+
+    def ok(self):
+        return not self.violations
+
+
 class H2Matrix:
     """Device-resident H^2 matrix (h2_matrix.hpp:40-306)."""
 
@@ -334,6 +356,29 @@ class H2Matrix:
         s = stream.cuda_stream if stream is not None else None
         check(lib.h2c_hgemv(self._h, int(transpose), int(ordering), x.shape[0], b, x.data_ptr(), ldx,
                             y.data_ptr(), ldy, float(alpha), float(beta), s))
+
+    def to_dense(self, cap=8192):
+        """H2Matrix::to_dense(cap) (h2_matrix.hpp:128-163): n x n, user ordering
+        (computed on the device as the operator applied to identity panels)."""
+        a = np.empty((self.n, self.n), order="F")
+        check(lib.h2c_to_dense(self._h, int(cap), _ptr(a)))
+        return a
+
+    def validate(self, ortho_cap=4096):
+        """H2Matrix::validate(ortho_cap) (h2_matrix.hpp:308-404) -> ValidationReport."""
+        nv, nl = C.c_int(), C.c_int()
+        buf = C.create_string_buffer(8192)
+        prof = np.zeros(128, np.int64)
+        st = np.zeros(4, np.int64)
+        check(lib.h2c_validate(self._h, int(ortho_cap), C.byref(nv), buf, len(buf), _ptr(prof), len(prof),
+                               C.byref(nl), _ptr(st)))
+        msgs = [m for m in buf.value.decode().split("\n") if m] if nv.value else []
+        return ValidationReport(msgs, prof[:nl.value].tolist(),
+                                StorageReport(int(st[0]), int(st[1]), int(st[2]), int(st[3])))
+
+    def storage(self):
+        """H2Matrix::storage() (h2_matrix.hpp:167-187)."""
+        return self.validate(ortho_cap=0).storage
 
     def add_diagonal(self, value):
         """In place H <- H + value I (diagonal dense leaves)."""
