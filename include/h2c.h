@@ -196,6 +196,9 @@ int h2c_estimate_relative_error(h2c_operator op, h2c_matrix h, double op_norm, d
  * h2c_rng is that stream (normals drawn exactly as detail::fill_gaussian). */
 typedef struct h2c_rng_s* h2c_rng;
 int h2c_rng_create(uint64_t seed, h2c_rng* out);
+/* rows x cols normals from the stream, column-major host buffer (a fresh
+ * normal_distribution per call, exactly detail::fill_gaussian; host only) */
+int h2c_rng_fill_gaussian(h2c_rng r, int64_t rows, int64_t cols, double* out);
 void h2c_rng_destroy(h2c_rng r);
 /* sample_block_column(op, ct, t, s, count, rng) (construction.hpp:137-148):
  * omega_s (|s| x count, ld |s|) and y_t = op(Omega) on the rows of t

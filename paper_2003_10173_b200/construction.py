@@ -212,6 +212,12 @@ class Rng:
         self._h = H()
         check(lib.h2c_rng_create(int(seed), C.byref(self._h)))
 
+    def gaussian(self, rows, cols):
+        """detail::fill_gaussian of a rows x cols block (construction.hpp:81-85)."""
+        out = np.empty((int(rows), int(cols)), order="F")
+        check(lib.h2c_rng_fill_gaussian(self._h, int(rows), int(cols), out.ctypes.data_as(C.c_void_p)))
+        return out
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib.h2c_rng_destroy(self._h)

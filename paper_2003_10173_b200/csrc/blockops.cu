@@ -9,6 +9,7 @@
 #include "blockops.hpp"
 #include "inversion.hpp"
 #include "matrix.hpp"
+#include "refstream.hpp"
 
 namespace h2b {
 
@@ -28,12 +29,9 @@ void check_node(const ClusterTree& ct, int v, const char* what) {
     if (v < 0 || v >= ct.num_nodes()) throw std::invalid_argument(std::string(what) + ": cluster id out of range");
 }
 
-// the reference normal stream (construction.hpp:81-85): a fresh
-// normal_distribution over the caller's mt19937_64, column-major
+// the reference normal stream (construction.hpp:81-85), |rows| x cols packed
 void fill_gaussian(double* m, int64_t rows, int64_t cols, std::mt19937_64& rng) {
-    std::normal_distribution<double> g(0, 1);
-    for (int64_t j = 0; j < cols; ++j)
-        for (int64_t i = 0; i < rows; ++i) m[i + j * rows] = g(rng);
+    ref_fill_gaussian(m, rows, cols, rows, rng);
 }
 
 // dst[idx[i] + j * ldd] = src[i + j * lds]   (scatter = 1)

@@ -18,6 +18,7 @@
 #include "serialize.hpp"
 #include "matrix.hpp"
 #include "blockops.hpp"
+#include "refstream.hpp"
 
 struct h2c_cluster_tree_s {
     std::shared_ptr<h2b::ClusterTree> t;
@@ -1100,6 +1101,13 @@ int h2c_rng_create(uint64_t seed, h2c_rng* out) {
     });
 }
 void h2c_rng_destroy(h2c_rng r) { delete r; }
+int h2c_rng_fill_gaussian(h2c_rng r, int64_t rows, int64_t cols, double* out) {
+    return guard([&] {
+        need(r != nullptr && (out != nullptr || rows * cols == 0), "null argument");
+        need(rows >= 0 && cols >= 0, "negative size");
+        h2b::ref_fill_gaussian(out, rows, cols, rows, r->g);
+    });
+}
 
 int h2c_sample_block_column(h2c_operator op, h2c_cluster_tree ct, int t, int s, int64_t count, h2c_rng rng,
                             double* omega_s, double* y_t, void* stream) {

@@ -14,6 +14,7 @@
 #include "hara.hpp"
 #include "la.hpp"
 #include "matrix.hpp"
+#include "refstream.hpp"
 
 namespace h2b {
 
@@ -88,12 +89,9 @@ const BasisDev& col_basis(const H2Dev& h) { return h.symmetric ? h.row : h.col; 
 
 std::vector<int> int32_perm(const ClusterTree& ct) { return std::vector<int>(ct.perm.begin(), ct.perm.end()); }
 
-// host-side reference normal stream (fill_gaussian, construction.hpp:81-85):
-// a fresh normal_distribution per call over the shared mt19937_64
+// host-side reference normal stream (fill_gaussian, construction.hpp:81-85)
 void fill_gaussian(double* m, int64_t rows, int64_t cols, int64_t ld, std::mt19937_64& rng) {
-    std::normal_distribution<double> g(0, 1);
-    for (int64_t j = 0; j < cols; ++j)
-        for (int64_t i = 0; i < rows; ++i) m[i + j * ld] = g(rng);
+    ref_fill_gaussian(m, rows, cols, ld, rng);
 }
 
 // device Gaussian panel rows [r0, r0 + rows) x [0, cols) of an n-row matrix
@@ -162,10 +160,8 @@ NormEstimate pnorm2_estimate(DevOperator& op, cudaStream_t s, int max_iter, doub
     const int64_t n = op.dim();
     const int b = int(std::min<int64_t>(3, n));
     std::mt19937_64 rng(0x9E3779B97F4A7C15ull);
-    std::normal_distribution<double> g(0, 1);
     std::vector<double> vh(size_t(n * b));
-    for (int j = 0; j < b; ++j)
-        for (int64_t i = 0; i < n; ++i) vh[size_t(i + j * n)] = g(rng);
+    ref_fill_gaussian(vh.data(), n, b, n, rng);   // linear_operator.hpp:134-138
     DBuf v0(size_t(n * b), s), v(size_t(n * b), s), y(size_t(n * b), s), z(size_t(n * b), s);
     H2B_CUDA(cudaMemcpyAsync(v0.data(), vh.data(), vh.size() * sizeof(double), cudaMemcpyHostToDevice, s));
     thin_q_dev(v0.data(), n, b, v.data(), s);

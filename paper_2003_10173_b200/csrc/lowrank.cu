@@ -9,6 +9,7 @@
 #include <curand_kernel.h>
 
 #include "hara.hpp"
+#include "refstream.hpp"
 #include "inversion.hpp"
 #include "la.hpp"
 
@@ -79,8 +80,7 @@ LowRankResultDev randomized_lowrank(DevOperator& op, double eps, int64_t max_ran
         DBuf om(size_t(n * panel), s), y(size_t(n * panel), s);
         if (cfg.rng == 0) {   // fill_gaussian(omega, rng) (construction.hpp:81-85)
             omh.resize(size_t(n * panel));
-            std::normal_distribution<double> g(0, 1);
-            for (auto& v : omh) v = g(rng);
+            ref_fill_gaussian(omh.data(), n, panel, n, rng);
             H2B_CUDA(cudaMemcpyAsync(om.data(), omh.data(), omh.size() * sizeof(double), cudaMemcpyHostToDevice, s));
         } else {
             const int64_t cnt = n * panel;
