@@ -11,6 +11,8 @@
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may use it.
 // ============================================================================
 #include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 #include <limits>
 #include <map>
@@ -785,6 +787,11 @@ inline H2Matrix recompress(const H2Matrix& h, double eps) {   // algebra.hpp:144
                 const double tau = eps * svd.S[0] / level_corr;
                 Index r = 0;
                 while (r < Index(svd.S.size()) && svd.S[size_t(r)] > tau) ++r;
+                if (std::getenv("H2_TRACE_RECOMPRESS"))
+                    std::fprintf(stderr, "trunc side=%d v=%d k=%ld c=%ld s0=%.17g tau=%.17g r=%ld lo=%.17g hi=%.17g\n",
+                                 int(row_side), v, long(k), long(cols), svd.S[0], tau, long(r),
+                                 r > 0 ? svd.S[size_t(r - 1)] : -1.0,
+                                 r < Index(svd.S.size()) ? svd.S[size_t(r)] : -1.0);
                 w[size_t(v)] = svd.U.leftCols(r);
                 p[size_t(v)] = detail::lq_reduce(gv);
             }
@@ -1119,6 +1126,11 @@ inline void absorb_panel(BlockRange& blk, Matrix panel, double keep_tol, Index p
     ThinSVD svd(panel);
     Index kept = 0;
     while (kept < Index(svd.S.size()) && svd.S[size_t(kept)] > keep_tol) ++kept;
+    if (std::getenv("H2_TRACE_ABSORB"))   // diagnostics: one line per absorbed panel
+        std::fprintf(stderr, "absorb t=%d s=%d q=%ld b=%ld tol=%.17g kept=%ld lo=%.17g hi=%.17g\n", blk.t, blk.s,
+                     long(blk.q.cols()), long(b), keep_tol, long(kept),
+                     kept > 0 ? svd.S[size_t(kept - 1)] : -1.0,
+                     kept < Index(svd.S.size()) ? svd.S[size_t(kept)] : -1.0);
     if (max_rank > 0 && blk.q.cols() + kept > max_rank)
         throw max_rank_error("adaptive factorization: block rank exceeds max_rank", blk.q);
     if (kept > 0) {
@@ -1318,7 +1330,17 @@ inline PeelResult peel_construct(const LinearOperator& op, std::shared_ptr<const
                 if (ranges2[i].rank() > 0) detail::apply_local_update(partial, ranges2[i].t, ranges2[i].s, ranges2[i].q, v2[i]);
             }
         }
+        if (const char* dp = std::getenv("H2_PEEL_DUMP")) {   // diagnostics: dense partial per level
+            Matrix a = partial.to_dense();
+            std::string f = std::string(dp) + "_ora_u" + std::to_string(level) + ".bin";
+            if (FILE* fp = std::fopen(f.c_str(), "wb")) { std::fwrite(a.data(), 8, size_t(a.size()), fp); std::fclose(fp); }
+        }
         partial = recompress(partial, 0.5 * cfg.eps);
+        if (const char* dp = std::getenv("H2_PEEL_DUMP")) {
+            Matrix a = partial.to_dense();
+            std::string f = std::string(dp) + "_ora_r" + std::to_string(level) + ".bin";
+            if (FILE* fp = std::fopen(f.c_str(), "wb")) { std::fwrite(a.data(), 8, size_t(a.size()), fp); std::fclose(fp); }
+        }
         stats.add_level({level, Index(pairs.size()) * (sym ? 1 : 2), max_rank_seen, op.columns_applied() - before});
     }
     before = op.columns_applied();

@@ -333,7 +333,23 @@ struct ThinSVD {
             HouseholderQR qr(a.transpose());   // a^T = Q R  =>  a = R^T Q^T
             jacobi_left(qr.R(m).transpose(), U, S);
         }
-        (void)want_u;
+        if (want_u) canonical_signs(U);
+    }
+    // each column's largest-magnitude entry (lowest row on ties) positive: the
+    // sign convention the device SVD uses (la.cu canon_sign_kernel), so HARA's
+    // O(eps) cross terms -- and its later decisions -- agree with the device path
+    static void canonical_signs(Matrix& u) {
+        for (Index j = 0; j < u.cols(); ++j) {
+            Index bi = 0;
+            double best = -1.0;
+            for (Index i = 0; i < u.rows(); ++i)
+                if (std::abs(u(i, j)) > best) {
+                    best = std::abs(u(i, j));
+                    bi = i;
+                }
+            if (u.rows() > 0 && u(bi, j) < 0)
+                for (Index i = 0; i < u.rows(); ++i) u(i, j) = -u(i, j);
+        }
     }
 };
 

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 
@@ -15,6 +17,8 @@
 #include "la.hpp"
 #include "matrix.hpp"
 #include "refstream.hpp"
+#include "blockops.hpp"
+#include <string>
 
 namespace h2b {
 
@@ -44,6 +48,8 @@ double g_phase_ms[16];   // 8 orthogonalize, 9 truncation bases, 10 projection (
 // phase timers drain the stream only when enabled (h2b_hara_phase_sync): a
 // synchronisation per phase would otherwise stall the device at every phase end
 int g_phase_sync = 0;
+const bool g_trace_absorb = std::getenv("H2_TRACE_ABSORB") != nullptr;
+const bool g_trace_recompress = std::getenv("H2_TRACE_RECOMPRESS") != nullptr;
 struct Phase {
     int id;
     cudaStream_t s;
@@ -422,6 +428,9 @@ Truncation truncation_bases(const H2Dev& g, bool row_side, double eps, double le
         int r = 0;
         while (r < ns && sv[r] > tau) ++r;
         tr.rank[size_t(v)] = r;
+        if (g_trace_recompress)
+            std::fprintf(stderr, "trunc side=%d v=%d k=%d c=%d s0=%.17g tau=%.17g r=%d lo=%.17g hi=%.17g\n",
+                         int(row_side), v, k, c, sv[0], tau, r, r > 0 ? sv[r - 1] : -1.0, r < ns ? sv[r] : -1.0);
     }
     tr.U = std::move(U);
     return tr;
@@ -830,6 +839,9 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
                 throw max_rank_error("adaptive factorization: block rank exceeds max_rank");
             kept[q] = kk;
             need_cap = std::max(need_cap, r.rank + kk);
+            if (g_trace_absorb)   // diagnostics (H2_TRACE_ABSORB): one line per absorbed panel
+                std::fprintf(stderr, "absorb t=%d s=%d q=%d b=%ld tol=%.17g kept=%d lo=%.17g hi=%.17g\n", r.t, r.s,
+                             r.rank, long(panel), keep_tol, kk, kk > 0 ? sv[kk - 1] : -1.0, kk < p ? sv[kk] : -1.0);
         }
         if (need_cap > cap) {
             int nc = cap;
@@ -927,10 +939,23 @@ PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, 
             for (auto [t, u] : pairs) mirrored.emplace_back(u, t);
             group(mirrored);
         }
+        auto dump = [&](const char* tag) {   // diagnostics (H2_PEEL_DUMP=prefix): dense partial per level
+            const char* dp = std::getenv("H2_PEEL_DUMP");
+            if (!dp) return;
+            std::vector<double> a(size_t(ct.n * ct.n));
+            to_dense(*partial, ct.n, a.data(), s);
+            std::string f = std::string(dp) + "_gpu_" + tag + std::to_string(level) + ".bin";
+            if (FILE* fp = std::fopen(f.c_str(), "wb")) {
+                std::fwrite(a.data(), 8, a.size(), fp);
+                std::fclose(fp);
+            }
+        };
+        dump("u");
         {
             Phase ph(6, s);
             partial = recompress(*partial, 0.5 * cfg.eps, s);
         }
+        dump("r");
         stats.add_level({level, int64_t(pairs.size()) * (sym ? 1 : 2), max_rank_seen, op.columns_applied() - before});
     }
     // dense diagonal leaves (:357-376): indicator columns, residual apply, symmetrise, add

@@ -617,6 +617,44 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     }
 }
 
+// canonical sign of each left singular vector: the entry of largest magnitude
+// (lowest row on ties) is made positive. Singular vectors are unique only up
+// to sign, and HARA's shared transposed pass (construction.hpp:272-289) mixes
+// the bases of different pairs, so its O(eps) cross terms -- and through them
+// later rank / sample decisions -- depend on the convention. The CPU
+// restatement and the reference build in oracle/_ref use the same rule.
+struct SignJob {
+    double* U;
+    int m, p, ldu;
+};
+__global__ void __launch_bounds__(256) canon_sign_kernel(const SignJob* __restrict__ jobs) {
+    const SignJob j = jobs[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = warp; c < j.p; c += nw) {
+        double* u = j.U + int64_t(c) * j.ldu;
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = lane; i < j.m; i += 32) {
+            const double a = fabs(u[i]);
+            if (a > best) {
+                best = a;
+                bi = i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_down_sync(0xffffffffu, best, o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        bi = __shfl_sync(0xffffffffu, bi, 0);
+        if (bi < j.m && u[bi] < 0.0)
+            for (int i = lane; i < j.m; i += 32) u[i] = -u[i];
+    }
+}
+
 void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
     // wide (m <= c): A^T = Q R (R m x m); left(A) = right(R) -> Jacobi(R).V
     // tall (m > c):  A = Q R (R c x c);   left(A) = Q * right(R^T) -> Q * Jacobi(R^T).V
@@ -677,6 +715,14 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
     bcopy(last, s);
     bjacobi(svs, s);
     bgemm(gm, s);
+    std::vector<SignJob> sg;
+    for (const LeftSvdDesc& q : d)
+        if (q.m > 0 && q.c > 0 && q.U) sg.push_back(SignJob{q.U, q.m, std::min(q.m, q.c), q.ldu});
+    if (!sg.empty()) {
+        DevVec<SignJob> dj(sg, s);
+        canon_sign_kernel<<<unsigned(sg.size()), 256, 0, s>>>(dj.p);
+        H2B_LAUNCH();
+    }
 }
 
 }  // namespace la

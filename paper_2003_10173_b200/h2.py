@@ -360,7 +360,8 @@ class H2Matrix:
     def to_dense(self, cap=8192):
         """H2Matrix::to_dense(cap) (h2_matrix.hpp:128-163): n x n, user ordering
         (computed on the device as the operator applied to identity panels)."""
-        a = np.empty((self.n, self.n), order="F")
+        n = self.n()
+        a = np.empty((n, n), order="F")
         check(lib.h2c_to_dense(self._h, int(cap), _ptr(a)))
         return a
 
