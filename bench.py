@@ -147,16 +147,52 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(args):
+    """`--gpus N` without a torchrun environment: re-launch this command as N
+    ranks under torch.distributed.run (one process per GPU, NCCL). Fails loudly
+    when the node has fewer than N GPUs -- never falls back to one GPU."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if args.impl == "b200" and world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return   # the reference arm is the host CPU port: rank 0 alone does the work
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} requested but this node has {have} CUDA device(s); "
+                 f"refusing to run (no single-GPU fallback)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
     if world > 1:
+        import torch
         import torch.distributed as dist
+        if args.impl != "reference":
+            have = torch.cuda.device_count()
+            if local >= have:
+                sys.exit(f"bench.py: rank {rank} has LOCAL_RANK {local} but only {have} CUDA device(s)")
+            torch.cuda.set_device(local)
         backend = "nccl" if args.impl != "reference" else "gloo"
         dist.init_process_group(backend=backend)
         pg = dist
+        print(f"bench.py: rank {rank}/{world} on cuda:{local} backend={backend}", file=sys.stderr, flush=True)
     return world, rank, local, pg
 
 
@@ -337,6 +373,13 @@ def run_b200(args, cfg, world, rank, local, dist):
 
     # end-to-end through the public host-buffer API (pinned x in, y out)
     xp = x_host.pin_memory()
+    if sharded is not None:
+        ob, orows = sharded.plan.owned_begin, sharded.plan.owned_rows
+        perm = np.asarray(ct.perm)
+        xop = torch.from_numpy(np.ascontiguousarray(x_host.numpy()[:, perm[ob:ob + orows]])).pin_memory()
+        yop = torch.empty_like(xop).pin_memory()
+        Xo = xop.to(dev)
+        Yo = torch.empty_like(Xo)
     yps = [torch.empty_like(xp).pin_memory() for _ in range(3)]
     streams = [torch.cuda.Stream(dev) for _ in range(3)]
 
@@ -347,9 +390,10 @@ def run_b200(args, cfg, world, rank, local, dist):
             check(lib.h2c_matvec_host_async(m._h, 0, 0, n, b, xp.data_ptr(), yps[i % 3].data_ptr(),
                                             streams[i % 3].cuda_stream))
         else:
-            X.copy_(xp, non_blocking=True)
-            sharded(X.t(), Y.t())
-            yps[0].copy_(Y, non_blocking=True)
+            # each rank's slice of x / y (its owned rows, cluster order) lives in pinned host memory
+            Xo.copy_(xop, non_blocking=True)
+            sharded(Xo.t(), Yo.t(), owned=True)
+            yop.copy_(Yo, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
 
     def e2e_run(k):
@@ -383,11 +427,13 @@ def run_b200(args, cfg, world, rank, local, dist):
         for _ in range(3):
             check(lib.h2c_matvec_host(m._h, 0, 0, n, b, xp.data_ptr(), yps[0].data_ptr()))
         ts = (time.perf_counter() - t0) / 3
+    io_rows = n if sharded is None else sharded.plan.owned_rows * world
     e2e = {"value": F / te / 1e9, "unit": "GFLOP/s", "ms_per_step": te * 1e3,
-           "h2d_bytes_per_step": 8 * n * b, "d2h_bytes_per_step": 8 * n * b,
+           "h2d_bytes_per_step": 8 * io_rows * b, "d2h_bytes_per_step": 8 * io_rows * b,
            "path": ("h2c_matvec_host_async on 3 rotating streams: per step pinned host x -> HBM, hgemv, "
                     "HBM -> pinned host y (copies of one step overlap the hgemv of the next)") if sharded is None else
-                   "per rank: pinned host x -> HBM, sharded hgemv (NCCL all-to-all), HBM -> pinned host y",
+                   "per rank: its owned rows of x (pinned host, cluster order) -> HBM, sharded hgemv (NCCL "
+                   "all-to-all overlapped with the local near field), owned rows of y -> pinned host",
            "warmup_s": tw,
            "sync_call": None if ts is None else {"value": F / ts / 1e9, "ms_per_step": ts * 1e3,
                                                  "path": "h2c_matvec_host (H2D, hgemv, D2H, wait; no overlap)"}}
@@ -728,6 +774,11 @@ def main():
                     help="dram bytes/launch of the dominant kernel from an ncu --set full capture "
                          "(default for cfg2: the committed capture, profiles/ncu_full_cfg2_r01_v6.txt)")
     args = ap.parse_args()
+    # NCCL communicator setup (ranks, rings / NVLS) on stderr; stdout carries only the JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    launch_ranks(args)
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     cfg = CONFIGS[args.config]

@@ -253,6 +253,18 @@ int h2c_dist_plan_launches(h2c_dist_plan p, int* launches);
 /* x: full n x b user-order device matrix (only owned rows are read) */
 int h2c_dist_hgemv_begin(h2c_dist_plan p, int64_t b, const double* x, int64_t ldx, double* sendbuf, void* stream);
 /* y: full n x b user-order device matrix (only owned rows are written: y = alpha H x + beta y) */
+/* optional, between begin and end while the caller's exchange is in flight:
+ * the near-field products whose source rows this rank owns (kept in the plan's
+ * workspace; end() runs them itself when this was not called) */
+int h2c_dist_hgemv_local(h2c_dist_plan p, int64_t b, void* stream);
+/* begin / end on this rank's OWN rows only: x and y hold the owned_rows rows
+ * (h2c_dist_plan_counts) in cluster (internal) order, leading dimensions >=
+ * owned_rows -- the layout of an application that keeps each rank's slice of
+ * the vectors resident on its GPU */
+int h2c_dist_hgemv_begin_owned(h2c_dist_plan p, int64_t b, const double* x_owned, int64_t ldx, double* sendbuf,
+                               void* stream);
+int h2c_dist_hgemv_end_owned(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y_owned, int64_t ldy,
+                             double alpha, double beta, void* stream);
 int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha,
                        double beta, void* stream);
 /* host-only partition metadata (no device needed): owner rank per cluster node

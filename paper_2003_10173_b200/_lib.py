@@ -138,6 +138,9 @@ _sig("h2c_dist_plan_destroy", None, H)
 _sig("h2c_dist_plan_counts", i32, H, vp, vp, P(i64), P(i64))
 _sig("h2c_dist_plan_launches", i32, H, P(i32))
 _sig("h2c_dist_hgemv_begin", i32, H, i64, vp, i64, vp, vp)
+_sig("h2c_dist_hgemv_local", i32, H, i64, vp)
+_sig("h2c_dist_hgemv_begin_owned", i32, H, i64, vp, i64, vp, vp)
+_sig("h2c_dist_hgemv_end_owned", i32, H, i64, vp, vp, i64, f64, f64, vp)
 _sig("h2c_dist_hgemv_end", i32, H, i64, vp, vp, i64, f64, f64, vp)
 _sig("h2c_partition_owner", i32, H, i32, vp)
 _sig("h2c_partition_exchange", i32, H, i32, i32, vp, i32, i32, i32, P(i64), vp, vp, vp)

@@ -598,12 +598,36 @@ int h2c_dist_hgemv_begin(h2c_dist_plan p, int64_t b, const double* x, int64_t ld
     });
 }
 
+int h2c_dist_hgemv_local(h2c_dist_plan p, int64_t b, void* stream) {
+    return guard([&] {
+        need(p != nullptr, "null plan");
+        need(b >= 1, "dist hgemv: need at least one column");
+        h2b::dist_hgemv_local(*p->p, b, static_cast<cudaStream_t>(stream));
+    });
+}
 int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha,
                        double beta, void* stream) {
     return guard([&] {
         need(p != nullptr && y != nullptr, "null argument");
         need(b >= 1, "matvec: need at least one column");
         h2b::dist_hgemv_end(*p->p, b, recvbuf, y, ldy, alpha, beta, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_dist_hgemv_begin_owned(h2c_dist_plan p, int64_t b, const double* x_owned, int64_t ldx, double* sendbuf,
+                               void* stream) {
+    return guard([&] {
+        need(p != nullptr && x_owned != nullptr, "null argument");
+        need(b >= 1, "matvec: need at least one column");
+        h2b::dist_hgemv_begin(*p->p, b, x_owned, ldx, sendbuf, static_cast<cudaStream_t>(stream), true);
+    });
+}
+int h2c_dist_hgemv_end_owned(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y_owned, int64_t ldy,
+                             double alpha, double beta, void* stream) {
+    return guard([&] {
+        need(p != nullptr && y_owned != nullptr, "null argument");
+        need(b >= 1, "matvec: need at least one column");
+        h2b::dist_hgemv_end(*p->p, b, recvbuf, y_owned, ldy, alpha, beta, static_cast<cudaStream_t>(stream), true);
     });
 }
 

@@ -70,12 +70,13 @@ struct HgemvGraph {
         double alpha = 0, beta = 0;
         // the captured launches bake in the workspace buffers and the runtime
         // knobs: a resized workspace or a toggled knob must not replay
-        const double *xint = nullptr, *xhat = nullptr, *yhat = nullptr, *scratch = nullptr;
+        const double *xint = nullptr, *xhat = nullptr, *yhat = nullptr, *scratch = nullptr, *ypart = nullptr;
         uint64_t knobs = 0;
         bool operator==(const Key& o) const {
             return plan == o.plan && transpose == o.transpose && user == o.user && n == o.n && b == o.b &&
                    ldx == o.ldx && ldy == o.ldy && x == o.x && y == o.y && alpha == o.alpha && beta == o.beta &&
-                   xint == o.xint && xhat == o.xhat && yhat == o.yhat && scratch == o.scratch && knobs == o.knobs;
+                   xint == o.xint && xhat == o.xhat && yhat == o.yhat && scratch == o.scratch && ypart == o.ypart &&
+                   knobs == o.knobs;
         }
     };
     Key key, last;
@@ -98,6 +99,7 @@ struct HgemvGraph {
 struct Workspace {
     DeviceArray<double> xint, xhat, yhat;
     DeviceArray<double> scratch;   // per-block products of the symmetric few-vector path
+    DeviceArray<double> ypart;     // split stage 5: near-field partial sums (internal blocked order)
     DeviceArray<double> hx, hy;   // staging of the host-buffer entry point
     HgemvGraph graph;
 };
@@ -153,11 +155,18 @@ std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nra
 void dist_counts(const DistPlan& p, std::vector<int64_t>& send_rows, std::vector<int64_t>& recv_rows);
 // phase A: gather owned x rows, owned upsweep, pack the send buffer
 // (peers in rank order, each peer's items contiguous; b columns per row)
-void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, double* sendbuf, cudaStream_t s);
+// owned = true: x holds only this rank's rows, in cluster (internal) order
+// (dist_owned_rows), instead of the full user-ordered vectors
+void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, double* sendbuf, cudaStream_t s,
+                      bool owned = false);
+// optional, between begin and end while the exchange is in flight: the
+// near-field products whose source rows this rank owns (into the workspace)
+void dist_hgemv_local(DistPlan& p, int64_t b, cudaStream_t s);
 // phase B: unpack the receive buffer, replicated top upsweep, couplings,
-// downsweep, leaf + near-field for owned rows of y (user order)
+// downsweep, leaf + remaining near-field for owned rows of y (user order);
+// runs the local near field itself if dist_hgemv_local was not called
 void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha, double beta,
-                    cudaStream_t s);
+                    cudaStream_t s, bool owned = false);
 int64_t dist_owned_rows(const DistPlan& p, int64_t* begin);
 int dist_launch_count(const DistPlan& p);
 

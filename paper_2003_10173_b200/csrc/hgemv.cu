@@ -286,8 +286,9 @@ __global__ void __launch_bounds__(WM * WN * 32, (MT == 32 && STAGES == 1) ? SEG3
                 const int nn = (wn * TN + j) * 8 + 2 * t4 + h;
                 if (nn >= ncols) continue;
                 const int64_t col = j0 + nn;
-                const double v = acc[i][j][h];
+                double v = acc[i][j][h];
                 if constexpr (MODE == kModeY) {
+                    if (args.yadd) v += args.yadd[tk.out_unit * args.b + row + col * tk.rows];
                     double* p = args.out + ur + col * args.ldy;
                     *p = args.beta == 0.0 ? args.alpha * v : args.alpha * v + args.beta * *p;
                 } else {
@@ -454,8 +455,9 @@ __global__ void __launch_bounds__((WM * WN + 1) * 32, MINB) ws_gemm_kernel(SegAr
                 for (int h = 0; h < 2; ++h) {
                     const int nn = (wn * TN + j) * 8 + 2 * t4 + h;
                     if (nn >= ncols) continue;
-                    const double v = acc[i][j][h];
+                    double v = acc[i][j][h];
                     if constexpr (MODE == kModeY) {
+                        if (args.yadd) v += args.yadd[tk.out_unit * args.b + row + int64_t(nn) * tk.rows];
                         const int64_t ir = tk.out_unit + row;
                         const int64_t ur = args.perm ? args.perm[ir] : ir;
                         double* p = args.out + ur + int64_t(nn) * args.ldy;
@@ -805,7 +807,9 @@ struct LaunchDesc {
     // column of B operands read / outputs written
     double flops_per_col = 0, payload_bytes = 0, bsrc_per_col = 0, out_per_col = 0;
     int stage = 0;            // 1 leaf up, 2 transfer up, 3 coupling, 4 downsweep, 5 leaf+dense
-    int phase = 0;            // sharded hgemv: 0 before the exchange, 1 after
+    int phase = 0;            // sharded hgemv: 0 before the exchange, 1 after, 2 local-source near field
+    bool side = false;        // split near field (5d): may run on the side stream beside the sweeps
+    bool yadd = false;        // leaf expansion (5u): adds the split near-field partial sums
     // 0 segmented GEMM; symmetric few-vector path: 1 block pass over couplings,
     // 2 slot sums into y-hat, 3 block pass over dense blocks, 4 slot sums into y
     int kind = 0;
@@ -832,6 +836,9 @@ struct HgemvPlan {
     int64_t scratch_rows = 0;
     bool sym32 = false;   // every coupling block has <= 32 even rows and <= 32 columns, 16-byte aligned
     bool sym64 = false;   // every dense block has <= 64 even rows, 16-byte aligned
+    // stage 5 split: the near field (5d) writes blocked partial sums to the
+    // workspace's ypart, the leaf expansion (5u) adds them in its epilogue
+    bool split = false;
     std::once_flag accounted;
     DeviceArray<SegTask> tasks;
     DeviceArray<SegEntry> entries;
@@ -990,7 +997,7 @@ double g_plan_sync_ms = 0;   // of which: the closing device synchronisation (di
 double g_plan_part_ms[4];    // diagnostics: task lists / U E products / uploads / count of builds
 
 std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const DistSpec* ds = nullptr,
-                                      bool small = false) {
+                                      bool small = false, bool split = false) {
     const ClusterTree& ct = h.tree();
     // sharded plans keep only this rank's outputs: its subtree (owner == rank)
     // plus the replicated top levels (owner < 0)
@@ -1210,21 +1217,31 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     }
     lap(1);
     // stage 3b + 4: leaves  y_t = alpha (U_t yhat_t + (U_t E_t) yhat_parent + sum op(D) X_s) + beta y_t
+    // split plans move the near-field entries whose source x rows are local
+    // (all of them on one GPU; this rank's own leaves when sharded) into a
+    // separate launch (5d) that writes blocked partial sums to ypart and
+    // depends only on the gather, so it can run beside the sweeps (one GPU)
+    // or while the exchange is in flight (sharded); the leaf expansion (5u)
+    // adds ypart in its epilogue before the single user-order scatter
+    split = split && !small;
+    plan->split = split;
     {
-        EntryCsr by_leaf(nn);
+        auto near_here = [&](int src) { return split && (!ds || ds->owner[size_t(src)] == ds->rank); };
+        EntryCsr by_leaf(nn), by_near(nn);
         for (int t : ct.leaves) by_leaf.count(t, ue_off[size_t(t)] >= 0 ? 2 : 1);
         for (size_t i = 0; i < bt.dense.size() && !small; ++i) {
             const int b = bt.dense[i];
             if (!h.stores(b)) continue;
             const int r = bt.row[size_t(b)], c = bt.col[size_t(b)];
             if (!swap) {
-                by_leaf.count(r);
-                if (h.symmetric && r != c) by_leaf.count(c);
+                (near_here(c) ? by_near : by_leaf).count(r);
+                if (h.symmetric && r != c) (near_here(r) ? by_near : by_leaf).count(c);
             } else {
-                by_leaf.count(c);
+                (near_here(r) ? by_near : by_leaf).count(c);
             }
         }
         by_leaf.finish_count();
+        by_near.finish_count();
         for (int t : ct.leaves) {
             const int k = down.rank[size_t(t)], m = int(ct.size(t));
             by_leaf.add(t, make_entry(down.leaf.data() + down.leaf_off[size_t(t)], m, k, false, 2, cd[size_t(t)], k));
@@ -1240,21 +1257,40 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
             const double* D = h.D.data() + h.d_off[i];
             const int mr = int(ct.size(r)), mc = int(ct.size(c));
             if (!swap) {
-                by_leaf.add(r, make_entry(D, mr, mc, false, 0, ct.begin[size_t(c)], mc));
-                if (h.symmetric && r != c) by_leaf.add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
+                (near_here(c) ? by_near : by_leaf).add(r, make_entry(D, mr, mc, false, 0, ct.begin[size_t(c)], mc));
+                if (h.symmetric && r != c)
+                    (near_here(r) ? by_near : by_leaf).add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
             } else {
-                by_leaf.add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
+                (near_here(r) ? by_near : by_leaf).add(c, make_entry(D, mr, mr, true, 0, ct.begin[size_t(r)], mr));
             }
         }
-        for (int t : ct.leaves)
+        for (int t : ct.leaves) {
             order_entries(by_leaf.pool, by_leaf.start[size_t(t)], by_leaf.start[size_t(t) + 1], 0, ct.begin[size_t(t)]);
+            order_entries(by_near.pool, by_near.start[size_t(t)], by_near.start[size_t(t) + 1], 0, ct.begin[size_t(t)]);
+        }
+        if (split) {   // 5d: every owned leaf gets a task (an empty one writes zeros)
+            outs.clear();
+            for (int t : ct.leaves) {
+                if (!own(t)) continue;
+                const int m = int(ct.size(t));
+                outs.push_back(P{m, m, ct.begin[size_t(t)], by_near.start[size_t(t)], by_near.start[size_t(t) + 1]});
+            }
+            const int saved = pb.phase;
+            const size_t nl = pb.launches.size();
+            pb.phase = 2;
+            pb.emit(outs, by_near.pool, kModeSet, 4, 5);
+            pb.phase = saved;
+            if (pb.launches.size() > nl) pb.launches.back().side = !ds;
+        }
         outs.clear();
         for (int t : ct.leaves) {
             if (!own(t)) continue;
             const int m = int(ct.size(t));
             outs.push_back(P{m, m, ct.begin[size_t(t)], by_leaf.start[size_t(t)], by_leaf.start[size_t(t) + 1]});
         }
+        const size_t nl = pb.launches.size();
         pb.emit(outs, by_leaf.pool, kModeY, 3, 5);
+        if (split && pb.launches.size() > nl) pb.launches.back().yadd = true;
     }
     if (small) {
         std::vector<int> lv, lr;
@@ -1309,6 +1345,9 @@ int g_small_b = 2;            // symmetric few-vector path for b <= this (0 = of
 // gathered x) on a least-priority stream concurrently with the latency-bound
 // sweep chain on a greatest-priority stream (0 = one stream)
 int g_dense_overlap = 1;
+// stage-5 split on one GPU (h2b_tune 9): the near field runs on the side
+// stream beside the sweeps and the leaf expansion adds its partial sums
+int g_dense_split = 1;
 
 // lazily create the fork/join streams and events of the overlapped few-vector path
 void ensure_side_streams(HgemvGraph& g) {
@@ -1324,9 +1363,10 @@ std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
     std::lock_guard<std::mutex> g(h.plan_mu);
     if (h.symmetric) transpose = false;   // op(H) = H: one plan serves both
     auto& p = h.plan[transpose ? 1 : 0];
-    if (!p) {
+    const bool split = g_dense_split != 0;
+    if (!p || p->split != split) {
         const auto t0 = std::chrono::steady_clock::now();
-        p = build_plan(h, transpose);
+        p = build_plan(h, transpose, nullptr, false, split);
         g_plan_build_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     return p;
@@ -1500,7 +1540,7 @@ struct EventTimer {
 };
 void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
                 double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws,
-                EventTimer* timer, const HgemvPlan* dplan = nullptr, int phases = 3);
+                EventTimer* timer, const HgemvPlan* dplan = nullptr, int phases = 7);
 }  // namespace
 
 namespace {
@@ -1538,10 +1578,11 @@ void reserve_workspace(const HgemvPlan& plan, int64_t n, int64_t b, cudaStream_t
     if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
     if (plan.scratch_rows > 0 && ws.scratch.size() < size_t(plan.scratch_rows * b))
         ws.scratch.resize(size_t(plan.scratch_rows * b), stream);
+    if (plan.split && ws.ypart.size() < need_x) ws.ypart.resize(need_x, stream);
 }
 // the runtime knobs that change the launch sequence of an hgemv
 uint64_t knob_signature() {
-    uint64_t s = uint64_t(g_pdl & 0xff) | uint64_t(g_dense_overlap & 0xff) << 8;
+    uint64_t s = uint64_t(g_pdl & 0xff) | uint64_t(g_dense_overlap & 0xff) << 8 | uint64_t(g_dense_split & 0xff) << 48;
     for (int i = 0; i < 4; ++i) s |= uint64_t(g_tune[i] & 0xff) << (16 + 8 * i);
     return s;
 }
@@ -1573,6 +1614,7 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     k.xhat = ws.xhat.data();
     k.yhat = ws.yhat.data();
     k.scratch = ws.scratch.data();
+    k.ypart = ws.ypart.data();
     k.knobs = knob_signature();
     if (g.exec && g.key == k) {
         H2B_CUDA(cudaGraphLaunch(g.exec, stream));
@@ -1665,7 +1707,10 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                 EventTimer* timer, const HgemvPlan* dplan, int phases) {
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
     if (b < 1) throw std::invalid_argument("matvec: need at least one column");
-    if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
+    // phases & 8: sharded call on this rank's owned rows only (x / y point at a
+    // virtual n-row array whose owned range is the caller's buffer)
+    if (!(phases & 8) && (ldx < n || ldy < n)) throw std::invalid_argument("matvec: leading dimension smaller than n");
+    phases &= 7;
     std::shared_ptr<HgemvPlan> own_plan;
     if (!dplan) own_plan = select_plan(h, transpose, b);
     const HgemvPlan* plan = dplan ? dplan : own_plan.get();
@@ -1677,7 +1722,8 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     // both join back into the caller's stream before the dense slot sums / at the end
     HgemvGraph& sg = ws.graph;
     const cudaStream_t user_stream = stream;
-    const bool overlap = g_dense_overlap && plan->sym64 && phases == 3 && !timer && plan->num_leaves > 0;
+    const bool overlap = g_dense_overlap && (plan->sym64 || plan->split) && phases == 7 && !timer &&
+                         plan->num_leaves > 0;
     if (overlap) {
         ensure_side_streams(sg);
         H2B_CUDA(cudaEventRecord(sg.ev[0], user_stream));
@@ -1735,6 +1781,13 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         if (ld.zero_yhat && need_d) H2B_CUDA(cudaMemsetAsync(ws.yhat.data(), 0, need_d * sizeof(double), stream));
         const int ntasks = ld.task_end - ld.task_begin;
         if (ntasks == 0) continue;
+        // split stage 5: the near field (5d) on the least-priority side stream once x is
+        // gathered; the leaf expansion (5u) waits for it
+        const cudaStream_t ls = (overlap && ld.side) ? sg.lo : stream;
+        if (overlap && ld.yadd) {
+            H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
+            H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[2], 0));
+        }
         if (timer) {
             timer->mark(stream);
             timer->out->push_back({ld.stage, 0.f, ld.flops_per_col * double(b),
@@ -1746,7 +1799,8 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         a.src0 = ws.xint.data();
         a.src1 = ws.xhat.data();
         a.src2 = ws.yhat.data();
-        a.out = ld.out == 1 ? ws.xhat.data() : (ld.out == 2 ? ws.yhat.data() : y);
+        a.out = ld.out == 1 ? ws.xhat.data() : (ld.out == 2 ? ws.yhat.data() : (ld.out == 4 ? ws.ypart.data() : y));
+        a.yadd = ld.yadd ? ws.ypart.data() : nullptr;
         a.perm = perm;
         a.b = b;
         a.ldy = ldy;
@@ -1754,7 +1808,7 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         a.beta = beta;
         const bool vec = ld.vec && (ld.units_even || b % 2 == 0) &&
                          (reinterpret_cast<uintptr_t>(ws.xint.data()) % 16 == 0);
-        dispatch(a, ntasks, b, ld.mt, vec, ld.mode, stream);
+        dispatch(a, ntasks, b, ld.mt, vec, ld.mode, ls);
         if (timer) timer->mark(stream);
     }
     if (overlap) {   // join both side streams back into the caller's stream
@@ -1863,6 +1917,7 @@ struct DistPlan {
     std::vector<int64_t> send_rows, recv_rows;
     DeviceArray<XItem> send_items, recv_items;   // buffer offsets already global (peer blocks concatenated)
     int nsend = 0, nrecv = 0;
+    bool local_pending = false;   // begin() ran, the local near field (5d) not yet
     Workspace ws;
 };
 
@@ -1889,7 +1944,7 @@ std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nra
     p->h = &h;
     p->transpose = transpose;
     p->spec = make_dist_spec(h.tree(), nranks, rank);
-    p->plan = build_plan(h, transpose, &p->spec);
+    p->plan = build_plan(h, transpose, &p->spec, false, true);   // split: local near field while the exchange flies
     const std::vector<int64_t>& cu = p->plan->cu;
     p->send_rows.assign(size_t(nranks), 0);
     p->recv_rows.assign(size_t(nranks), 0);
@@ -1938,9 +1993,17 @@ int64_t dist_owned_rows(const DistPlan& p, int64_t* begin) {
     return ct.size(root);
 }
 
-void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, double* sendbuf, cudaStream_t s) {
+void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, double* sendbuf, cudaStream_t s,
+                      bool owned) {
     const int64_t n = p.h->tree().n;
-    hgemv_impl(*p.h, p.transpose, true, n, b, x, ldx, nullptr, n, 1.0, 0.0, s, p.ws, nullptr, p.plan.get(), 1);
+    int64_t ob = 0;
+    const int64_t orows = dist_owned_rows(p, &ob);
+    if (owned && ldx < orows) throw std::invalid_argument("dist hgemv: leading dimension smaller than the owned rows");
+    // owned: x holds this rank's rows in cluster order; address it as rows [ob, ob + orows) of an n-row array
+    const double* xb = owned ? x - ob : x;
+    hgemv_impl(*p.h, p.transpose, !owned, n, b, xb, ldx, nullptr, owned ? ldx : n, 1.0, 0.0, s, p.ws, nullptr,
+               p.plan.get(), 1 | (owned ? 8 : 0));
+    p.local_pending = true;
     if (p.nsend) {
         exchange_kernel<<<p.nsend, 256, 0, s>>>(p.send_items.data(), b, p.ws.xint.data(), p.ws.xhat.data(), sendbuf, 0);
         H2B_LAUNCH();
@@ -1948,14 +2011,28 @@ void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, doub
 }
 
 void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha, double beta,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool owned) {
     const int64_t n = p.h->tree().n;
     if (p.nrecv) {
         exchange_kernel<<<p.nrecv, 256, 0, s>>>(p.recv_items.data(), b, p.ws.xint.data(), p.ws.xhat.data(),
                                                 const_cast<double*>(recvbuf), 1);
         H2B_LAUNCH();
     }
-    hgemv_impl(*p.h, p.transpose, true, n, b, nullptr, n, y, ldy, alpha, beta, s, p.ws, nullptr, p.plan.get(), 2);
+    // phase 1 (after the exchange) plus the local near field if the caller did not run it
+    const int phases = 2 | (p.local_pending ? 4 : 0) | (owned ? 8 : 0);
+    p.local_pending = false;
+    int64_t ob = 0;
+    const int64_t orows = dist_owned_rows(p, &ob);
+    if (owned && ldy < orows) throw std::invalid_argument("dist hgemv: leading dimension smaller than the owned rows");
+    hgemv_impl(*p.h, p.transpose, !owned, n, b, nullptr, owned ? ldy : n, owned ? y - ob : y, ldy, alpha, beta, s,
+               p.ws, nullptr, p.plan.get(), phases);
+}
+
+void dist_hgemv_local(DistPlan& p, int64_t b, cudaStream_t s) {
+    if (!p.local_pending) throw std::logic_error("dist hgemv: local() needs a preceding begin()");
+    const int64_t n = p.h->tree().n;
+    hgemv_impl(*p.h, p.transpose, true, n, b, nullptr, n, nullptr, n, 1.0, 0.0, s, p.ws, nullptr, p.plan.get(), 4);
+    p.local_pending = false;
 }
 
 int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
@@ -1988,6 +2065,10 @@ extern "C" int h2b_tune(int which, int value) {
     }
     if (which == 8) {   // few-vector path: dense pass concurrent with the sweeps (1) / serial (0)
         h2b::g_dense_overlap = value;
+        return 0;
+    }
+    if (which == 9) {   // stage-5 split (near field beside the sweeps) on (1) / off (0); plans rebuild lazily
+        h2b::g_dense_split = value;
         return 0;
     }
     if (which < 0 || which > 3) return -1;

@@ -45,6 +45,7 @@ struct SegArgs {
     const double* src1;
     const double* src2;
     double* out;
+    const double* yadd;   // MODE_Y: blocked internal-order partial sums added before alpha (nullptr = none)
     const int* perm;      // MODE_Y: user row of internal row (nullptr = identity)
     int64_t b;
     int64_t ldy;

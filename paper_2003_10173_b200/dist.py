@@ -65,21 +65,34 @@ class DistPlan:
         check(lib.h2c_dist_plan_launches(self._h, C.byref(v)))
         return v.value
 
-    def begin(self, x, sendbuf, b, stream=None):
+    def begin(self, x, sendbuf, b, stream=None, owned=False):
+        """owned: x holds only this rank's owned_rows rows, in cluster order."""
         _, ldx = col_major_geom(x)
-        check(lib.h2c_dist_hgemv_begin(self._h, int(b), x.data_ptr(), ldx, sendbuf.data_ptr(), stream))
+        fn = lib.h2c_dist_hgemv_begin_owned if owned else lib.h2c_dist_hgemv_begin
+        check(fn(self._h, int(b), x.data_ptr(), ldx, sendbuf.data_ptr(), stream))
 
-    def end(self, recvbuf, y, b, alpha=1.0, beta=0.0, stream=None):
+    def local(self, b, stream=None):
+        """Near-field products with this rank's own source rows (overlaps the exchange)."""
+        check(lib.h2c_dist_hgemv_local(self._h, int(b), stream))
+
+    def end(self, recvbuf, y, b, alpha=1.0, beta=0.0, stream=None, owned=False):
         _, ldy = col_major_geom(y)
-        check(lib.h2c_dist_hgemv_end(self._h, int(b), recvbuf.data_ptr(), y.data_ptr(), ldy, float(alpha),
-                                     float(beta), stream))
+        fn = lib.h2c_dist_hgemv_end_owned if owned else lib.h2c_dist_hgemv_end
+        check(fn(self._h, int(b), recvbuf.data_ptr(), y.data_ptr(), ldy, float(alpha), float(beta), stream))
 
 
 class ShardedHgemv:
     """y = alpha H x + beta y for this rank's rows, exchange over torch.distributed.
 
     x, y: column-major (n x b, stride(0) == 1) float64 CUDA tensors holding the
-    full user-ordered vectors; only owned rows of x are read and of y written."""
+    full user-ordered vectors; only owned rows of x are read and of y written.
+
+    One hgemv: begin (gather, owned upsweep, pack) -> the all-to-all, issued
+    asynchronously -> local near field on the compute stream while it is in
+    flight -> wait -> end (unpack, couplings, downsweep, remaining near field,
+    leaf expansion). NCCL groups exchange device buffers (the collective runs
+    on NCCL's stream, concurrent with the local near field); other backends
+    (gloo) stage the buffers through host memory."""
 
     def __init__(self, m, group=None, transpose=False):
         import torch.distributed as dist
@@ -88,6 +101,7 @@ class ShardedHgemv:
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.plan = DistPlan(m, world, rank, transpose)
+        self.device_collective = dist.is_initialized() and dist.get_backend(group) == "nccl"
         self._bufs = {}
 
     def _buffers(self, b, device):
@@ -98,14 +112,27 @@ class ShardedHgemv:
                                torch.empty(max(1, int(self.plan.recv_rows.sum()) * b), dtype=torch.float64, device=device))
         return self._bufs[key]
 
-    def __call__(self, x, y, alpha=1.0, beta=0.0):
+    def __call__(self, x, y, alpha=1.0, beta=0.0, owned=False):
+        """owned=False: x, y are the full user-ordered vectors (n rows); owned=True:
+        only this rank's plan.owned_rows rows, in cluster order."""
         import torch
         b = x.shape[1] if x.dim() == 2 else 1
         send, recv = self._buffers(b, x.device)
         s = torch.cuda.current_stream(x.device).cuda_stream
-        self.plan.begin(x, send, b, s)
+        self.plan.begin(x, send, b, s, owned)
         if self.plan.nranks > 1:
-            self.dist.all_to_all_single(recv[:int(self.plan.recv_rows.sum()) * b], send[:int(self.plan.send_rows.sum()) * b],
-                                        output_split_sizes=[int(v) * b for v in self.plan.recv_rows],
-                                        input_split_sizes=[int(v) * b for v in self.plan.send_rows], group=self.group)
-        self.plan.end(recv, y, b, alpha, beta, s)
+            ns, nr = int(self.plan.send_rows.sum()) * b, int(self.plan.recv_rows.sum()) * b
+            osz = [int(v) * b for v in self.plan.recv_rows]
+            isz = [int(v) * b for v in self.plan.send_rows]
+            if self.device_collective:
+                work = self.dist.all_to_all_single(recv[:nr], send[:ns], output_split_sizes=osz,
+                                                   input_split_sizes=isz, group=self.group, async_op=True)
+                self.plan.local(b, s)   # on the compute stream, beside NCCL's
+                work.wait()             # the compute stream waits for the exchange
+            else:
+                self.plan.local(b, s)
+                hs = send[:ns].cpu()    # synchronises the compute stream
+                hr = torch.empty(nr, dtype=torch.float64)
+                self.dist.all_to_all_single(hr, hs, output_split_sizes=osz, input_split_sizes=isz, group=self.group)
+                recv[:nr].copy_(hr)
+        self.plan.end(recv, y, b, alpha, beta, s, owned)

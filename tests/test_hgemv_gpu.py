@@ -246,3 +246,31 @@ def test_knob_toggle_does_not_replay_stale_graph(cuda):
     for o in outs:
         assert rel(o, ora.matvec(x)) <= TOL
         assert np.array_equal(o, outs[0])
+
+
+_REF = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.dirname(
+    __import__("os").path.abspath(__file__))), "oracle", "_ref", "libh2ref.so")
+
+
+@pytest.mark.skipif(not __import__("os").path.exists(_REF), reason="oracle/_ref not built")
+@pytest.mark.parametrize("tree", ["1d-weak-96-8", "2d-12-16", "rand3d-300-12", "2d-64-64"])
+@pytest.mark.parametrize("sym", [True, False])
+def test_hgemv_matches_reference_build(cuda, tree, sym):
+    """The B200 hgemv against H2Matrix::matvec / matvec_transpose(_internal)
+    executed by the reference's OWN code (h2_matrix.hpp:108-124, 246-305 compiled
+    unchanged into oracle/_ref) on the reference's own fixture: the tree and the
+    random_h2 payloads are built by the reference and uploaded as they are."""
+    from oracle import pyref as R
+    pts, leaf, weak = TREES[tree]
+    rt = R.Tree(pts, leaf, 1.0, weak)
+    rh = R.H2.random(rt, sym, min(12, leaf), 77)
+    ct = build_cluster_tree(pts, leaf)
+    bt = build_block_tree(ct, ct, 1.0, Admissibility.weak if weak else Admissibility.strong)
+    rr, cr = rh.ranks()
+    m = H2Matrix.from_packed(bt, sym, rr, cr, rh.export())
+    n = pts.shape[0]
+    for b in (1, 2, 16, 32, 64):
+        x = O.gaussian(300 + b, n, b)
+        for transpose in (False, True):
+            for ordering in (0, 1):
+                assert rel(m._host(x, transpose, ordering), rh.matvec(x, transpose, ordering)) <= TOL
