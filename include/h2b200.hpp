@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <functional>
 #include <map>
+#include <sstream>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -137,6 +138,20 @@ inline std::shared_ptr<const BlockTree> build_block_tree(std::shared_ptr<const C
 }
 
 // device-resident H^2 matrix (h2_matrix.hpp:40-306); value semantics via shared ownership
+struct StorageReport {   // h2_matrix.hpp:25-31
+    Index dense_reals = 0;
+    Index leaf_basis_reals = 0;
+    Index transfer_reals = 0;
+    Index coupling_reals = 0;
+    Index total() const { return dense_reals + leaf_basis_reals + transfer_reals + coupling_reals; }
+};
+struct ValidationReport {   // h2_matrix.hpp:33-38
+    std::vector<std::string> violations;
+    std::vector<Index> level_max_rank;
+    StorageReport storage;
+    bool ok() const { return violations.empty(); }
+};
+
 class H2Matrix {
 public:
     H2Matrix() = default;
@@ -174,6 +189,42 @@ public:
         detail::check(h2c_matrix_ranks(h_.get(), r.data(), nullptr));
         return r;
     }
+    bool orthonormal() const {
+        int64_t n = 0;
+        int s = 0, o = 0;
+        detail::check(h2c_matrix_info(h_.get(), &n, &s, &o));
+        return o != 0;
+    }
+    // dense expansion in user ordering (:128-163); M: (rows, cols) constructible, data() column-major
+    template <class M = Matrix>
+    M to_dense(Index cap = 8192) const {
+        if (n() > cap) throw std::invalid_argument("to_dense: matrix size exceeds cap");
+        M a(n(), n());
+        detail::check(h2c_to_dense(h_.get(), cap, a.data()));
+        return a;
+    }
+    ValidationReport validate(Index ortho_cap = 4096) const {   // :308-404
+        int nv = 0, nl = 0;
+        std::vector<char> msg(1 << 14);
+        std::vector<int64_t> prof(128);
+        int64_t st[4] = {0, 0, 0, 0};
+        detail::check(h2c_validate(h_.get(), ortho_cap, &nv, msg.data(), int64_t(msg.size()), prof.data(),
+                                   int(prof.size()), &nl, st));
+        ValidationReport r;
+        std::string all(msg.data());
+        for (size_t a = 0; nv > 0 && a <= all.size();) {
+            const size_t e = all.find('\n', a);
+            const std::string line = all.substr(a, e == std::string::npos ? std::string::npos : e - a);
+            if (!line.empty()) r.violations.push_back(line);
+            if (e == std::string::npos) break;
+            a = e + 1;
+        }
+        r.level_max_rank.assign(prof.begin(), prof.begin() + std::min<int>(nl, int(prof.size())));
+        r.storage = StorageReport{st[0], st[1], st[2], st[3]};
+        return r;
+    }
+    std::vector<Index> rank_profile() const { return validate(0).level_max_rank; }   // :190-195
+    StorageReport storage() const { return validate(0).storage; }                    // :167-188
     h2c_matrix handle() const { return h_.get(); }
 
     std::shared_ptr<const BlockTree> blocks;
@@ -198,6 +249,31 @@ inline H2Matrix orthogonalize(const H2Matrix& h) {   // algebra.hpp:72-113
 inline H2Matrix recompress(const H2Matrix& h, double eps) {   // algebra.hpp:144-226
     h2c_matrix o = nullptr;
     detail::check(h2c_recompress(h.handle(), eps, &o));
+    return H2Matrix(o, h.blocks);
+}
+
+inline double frobenius_norm(const H2Matrix& h) {   // algebra.hpp:119-137 (needs orthonormal bases)
+    double v = 0;
+    detail::check(h2c_frobenius_norm(h.handle(), &v));
+    return v;
+}
+struct LowRankFactor {   // algebra.hpp:18-21: X Y^T, n x k each, user ordering
+    Matrix X, Y;
+    Index rank() const { return X.cols(); }
+};
+inline H2Matrix low_rank_update(const H2Matrix& h, const LowRankFactor& f, double eps) {   // algebra.hpp:334-346
+    if (f.X.rows() != h.n() || f.Y.rows() != h.n() || f.X.cols() != f.Y.cols())
+        throw std::invalid_argument("low_rank_update: factor dimensions do not match");
+    h2c_matrix o = nullptr;
+    detail::check(h2c_low_rank_update_host(h.handle(), f.rank(), f.X.data(), f.Y.data(), eps, &o));
+    return H2Matrix(o, h.blocks);
+}
+// local_low_rank_update(h, t, s, U_blk, V_blk, eps) (algebra.hpp:323-332): cluster-order factors
+template <class M>
+H2Matrix local_low_rank_update(const H2Matrix& h, int t, int s, const M& u_blk, const M& v_blk, double eps) {
+    if (u_blk.cols() != v_blk.cols()) throw std::invalid_argument("local update: factor dimensions do not match clusters");
+    h2c_matrix o = nullptr;
+    detail::check(h2c_local_low_rank_update_host(h.handle(), t, s, u_blk.cols(), u_blk.data(), v_blk.data(), eps, &o));
     return H2Matrix(o, h.blocks);
 }
 
@@ -337,6 +413,85 @@ inline PeelResult peel_construct(const LinearOperator& op, std::shared_ptr<const
     for (int i = 0; i < nl; ++i) r.stats.levels.push_back({lv[size_t(i)].level, lv[size_t(i)].blocks,
                                                            lv[size_t(i)].max_rank, long(lv[size_t(i)].samples)});
     return r;
+}
+
+namespace detail {
+// lend a caller's std::mt19937_64 to the library and take it back advanced
+// (h2c_rng_set_state / get_state: libstdc++'s textual engine state)
+template <class Engine>
+struct LentRng {
+    Engine& eng;
+    h2c_rng r = nullptr;
+    explicit LentRng(Engine& e) : eng(e) {
+        std::ostringstream out;
+        out << eng;
+        check(h2c_rng_create(0, &r));
+        check(h2c_rng_set_state(r, out.str().c_str()));
+    }
+    ~LentRng() {
+        int64_t need = 0;
+        if (h2c_rng_get_state(r, nullptr, &need) == H2C_OK) {
+            std::string buf(static_cast<size_t>(need), '\0');
+            if (h2c_rng_get_state(r, &buf[0], &need) == H2C_OK) {
+                std::istringstream in(buf);
+                in >> eng;
+            }
+        }
+        h2c_rng_destroy(r);
+    }
+};
+}  // namespace detail
+
+// sample_block_column(op, ct, t, s, count, rng) (construction.hpp:137-148):
+// (Omega restricted to s, op(Omega) restricted to t); rng advances exactly as
+// the reference's fill_gaussian would advance it
+template <class Engine>
+std::pair<Matrix, Matrix> sample_block_column(const LinearOperator& op, const ClusterTree& ct, int t, int s,
+                                              Index count, Engine& rng) {
+    if (count < 1) throw std::invalid_argument("sample_block_column: count must be >= 1");
+    detail::LentRng<Engine> lent(rng);
+    Index mt = 0, ms = 0;
+    {
+        std::vector<int64_t> b(static_cast<size_t>(ct.num_nodes())), e(b.size());
+        std::vector<int> lv(b.size()), par(b.size()), c0(b.size()), c1(b.size());
+        detail::check(h2c_cluster_tree_nodes(ct.handle(), b.data(), e.data(), lv.data(), par.data(), c0.data(),
+                                             c1.data(), nullptr, nullptr));
+        if (t < 0 || s < 0 || t >= ct.num_nodes() || s >= ct.num_nodes())
+            throw std::invalid_argument("sample_block_column: cluster id out of range");
+        mt = e[size_t(t)] - b[size_t(t)];
+        ms = e[size_t(s)] - b[size_t(s)];
+    }
+    Matrix om(ms, count), y(mt, count);
+    detail::check(h2c_sample_block_column_host(op.handle(), ct.handle(), t, s, count, lent.r, om.data(), y.data()));
+    return {std::move(om), std::move(y)};
+}
+
+struct BlockFactor {   // construction.hpp:150-154
+    Matrix u, v;
+    Index rank = 0;
+    double err_est = 0;
+};
+// adaptive_block_factorization(op, ct, t, s, eps_block, cfg) (construction.hpp:156-198)
+inline BlockFactor adaptive_block_factorization(const LinearOperator& op, const ClusterTree& ct, int t, int s,
+                                                double eps_block, const PeelConfig& cfg) {
+    h2c_peel_config c;
+    c.eps = cfg.eps;
+    c.sample_block_size = cfg.sample_block_size;
+    c.oversampling = cfg.oversampling;
+    c.max_rank = cfg.max_rank;
+    c.seed = cfg.seed;
+    c.norm_scale = cfg.norm_scale;
+    c.crossover_rank_cap = cfg.crossover_rank_cap;
+    c.rng = cfg.rng;
+    h2c_block_factor f = nullptr;
+    detail::check(h2c_adaptive_block_factorization(op.handle(), ct.handle(), t, s, eps_block, &c, &f));
+    std::unique_ptr<h2c_block_factor_s, void (*)(h2c_block_factor)> guard(f, h2c_block_factor_destroy);
+    int64_t ru = 0, rv = 0, k = 0;
+    double e = 0;
+    detail::check(h2c_block_factor_info(f, &ru, &rv, &k, &e));
+    BlockFactor out{Matrix(ru, k), Matrix(rv, k), Index(k), e};
+    detail::check(h2c_block_factor_download(f, out.u.data(), out.v.data()));
+    return out;
 }
 
 inline double estimate_relative_error(const LinearOperator& op, const H2Matrix& h, double op_norm = 0) {

@@ -199,12 +199,21 @@ int h2c_rng_create(uint64_t seed, h2c_rng* out);
 /* rows x cols normals from the stream, column-major host buffer (a fresh
  * normal_distribution per call, exactly detail::fill_gaussian; host only) */
 int h2c_rng_fill_gaussian(h2c_rng r, int64_t rows, int64_t cols, double* out);
+/* engine state as libstdc++ writes it (operator<< of std::mt19937_64): lets a
+ * C++ caller lend its own std::mt19937_64 to a sampler and take it back
+ * advanced, exactly as the reference's `std::mt19937_64& rng` arguments work.
+ * get: *bytes = required size incl. the terminator; written when buf is large enough */
+int h2c_rng_set_state(h2c_rng r, const char* state);
+int h2c_rng_get_state(h2c_rng r, char* buf, int64_t* bytes);
 void h2c_rng_destroy(h2c_rng r);
 /* sample_block_column(op, ct, t, s, count, rng) (construction.hpp:137-148):
  * omega_s (|s| x count, ld |s|) and y_t = op(Omega) on the rows of t
  * (|t| x count, ld |t|); device buffers, cluster (internal) row order */
 int h2c_sample_block_column(h2c_operator op, h2c_cluster_tree ct, int t, int s, int64_t count, h2c_rng rng,
                             double* omega_s, double* y_t, void* stream);
+/* the same with host output buffers (synchronous) */
+int h2c_sample_block_column_host(h2c_operator op, h2c_cluster_tree ct, int t, int s, int64_t count, h2c_rng rng,
+                                 double* omega_s, double* y_t);
 /* adaptive_block_factorization(op, ct, t, s, eps_block, cfg) (construction.hpp:156-198);
  * BlockFactor (:150-154): u (|t| x rank, orthonormal), v (|s| x rank), err_est.
  * A rank above cfg->max_rank returns H2C_MAX_RANK_ERROR (max_rank_error). */
@@ -222,6 +231,11 @@ void h2c_block_factor_destroy(h2c_block_factor f);
  * (a block-tree node), then recompressed to eps */
 int h2c_local_low_rank_update(h2c_matrix h, int t, int s, int64_t k, const double* U, int64_t ldu, const double* V,
                               int64_t ldv, double eps, h2c_matrix* out);
+/* host-buffer forms of low_rank_update (X, Y: n x k user order) and
+ * local_low_rank_update (U: |t| x k, V: |s| x k cluster order), ld = rows */
+int h2c_low_rank_update_host(h2c_matrix h, int64_t k, const double* X, const double* Y, double eps, h2c_matrix* out);
+int h2c_local_low_rank_update_host(h2c_matrix h, int t, int s, int64_t k, const double* U, const double* V, double eps,
+                                   h2c_matrix* out);
 /* frobenius_norm(h): requires orthonormal bases (H2C_INVALID_ARGUMENT otherwise) */
 int h2c_frobenius_norm(h2c_matrix h, double* out);
 /* H2Matrix::to_dense(cap): n x n host buffer, column-major, user ordering;

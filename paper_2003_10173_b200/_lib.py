@@ -196,6 +196,8 @@ def check(rc):   # noqa: F811  (extends the mapping with io_error)
 _sig("h2c_rng_create", i32, C.c_uint64, P(H))
 _sig("h2c_rng_destroy", None, H)
 _sig("h2c_rng_fill_gaussian", i32, H, i64, i64, vp)
+_sig("h2c_rng_set_state", i32, H, C.c_char_p)
+_sig("h2c_rng_get_state", i32, H, C.c_char_p, P(i64))
 _sig("h2c_sample_block_column", i32, H, H, i32, i32, i64, H, vp, vp, vp)
 _sig("h2c_adaptive_block_factorization", i32, H, H, i32, i32, f64, P(PeelConfigC), P(H))
 _sig("h2c_block_factor_info", i32, H, P(i64), P(i64), P(i64), P(f64))

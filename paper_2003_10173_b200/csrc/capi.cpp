@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <sstream>
 #include <string>
 
 #include "h2dev.hpp"
@@ -1125,6 +1126,25 @@ int h2c_rng_create(uint64_t seed, h2c_rng* out) {
     });
 }
 void h2c_rng_destroy(h2c_rng r) { delete r; }
+int h2c_rng_set_state(h2c_rng r, const char* state) {
+    return guard([&] {
+        need(r != nullptr && state != nullptr, "null argument");
+        std::istringstream in(state);
+        in >> r->g;
+        need(!in.fail(), "h2c_rng_set_state: malformed engine state");
+    });
+}
+int h2c_rng_get_state(h2c_rng r, char* buf, int64_t* bytes) {
+    return guard([&] {
+        need(r != nullptr && bytes != nullptr, "null argument");
+        std::ostringstream out;
+        out << r->g;
+        const std::string st = out.str();
+        const int64_t cap = *bytes;
+        *bytes = int64_t(st.size()) + 1;
+        if (buf && cap >= *bytes) std::memcpy(buf, st.c_str(), st.size() + 1);
+    });
+}
 int h2c_rng_fill_gaussian(h2c_rng r, int64_t rows, int64_t cols, double* out) {
     return guard([&] {
         need(r != nullptr && (out != nullptr || rows * cols == 0), "null argument");
@@ -1141,6 +1161,23 @@ int h2c_sample_block_column(h2c_operator op, h2c_cluster_tree ct, int t, int s, 
         need(op->op->dim() == ct->t->n, "sample_block_column: operator and tree sizes differ");
         h2b::sample_block_column(*op->op, *ct->t, t, s, count, rng->g, omega_s, y_t,
                                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+int h2c_sample_block_column_host(h2c_operator op, h2c_cluster_tree ct, int t, int s, int64_t count, h2c_rng rng,
+                                 double* omega_s, double* y_t) {
+    return guard([&] {
+        need(op != nullptr && ct != nullptr && rng != nullptr, "null argument");
+        need(omega_s != nullptr && y_t != nullptr, "null output buffer");
+        need(op->op->dim() == ct->t->n, "sample_block_column: operator and tree sizes differ");
+        need(t >= 0 && t < ct->t->num_nodes() && s >= 0 && s < ct->t->num_nodes(),
+             "sample_block_column: cluster id out of range");
+        const size_t no = size_t(std::max<int64_t>(count, 0) * ct->t->size(s));
+        const size_t ny = size_t(std::max<int64_t>(count, 0) * ct->t->size(t));
+        h2b::DeviceArray<double> om(std::max<size_t>(no, 1)), y(std::max<size_t>(ny, 1));
+        h2b::sample_block_column(*op->op, *ct->t, t, s, count, rng->g, om.data(), y.data(), nullptr);
+        H2B_CUDA(cudaMemcpy(omega_s, om.data(), no * sizeof(double), cudaMemcpyDeviceToHost));
+        H2B_CUDA(cudaMemcpy(y_t, y.data(), ny * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
 
@@ -1181,6 +1218,36 @@ int h2c_local_low_rank_update(h2c_matrix h, int t, int s, int64_t k, const doubl
     return guard([&] {
         need(h != nullptr && out != nullptr, "null argument");
         *out = wrap_matrix(h2b::local_low_rank_update(*h->h, t, s, k, U, ldu, V, ldv, eps, nullptr));
+    });
+}
+int h2c_low_rank_update_host(h2c_matrix h, int64_t k, const double* X, const double* Y, double eps, h2c_matrix* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        need(k >= 0 && (k == 0 || (X != nullptr && Y != nullptr)), "null factor");
+        const size_t sz = size_t(h->h->tree().n * k);
+        h2b::DeviceArray<double> xd, yd;
+        xd.upload(X, sz);
+        // a bitwise-equal pair stays one buffer: the symmetric update keeps symmetric storage
+        const bool same = X == Y || (sz && std::memcmp(X, Y, sz * sizeof(double)) == 0);
+        if (!same) yd.upload(Y, sz);
+        *out = wrap_matrix(h2b::low_rank_update(*h->h, xd.data(), same ? xd.data() : yd.data(), int(k), eps, nullptr));
+    });
+}
+int h2c_local_low_rank_update_host(h2c_matrix h, int t, int s, int64_t k, const double* U, const double* V, double eps,
+                                   h2c_matrix* out) {
+    return guard([&] {
+        need(h != nullptr && out != nullptr, "null argument");
+        const h2b::ClusterTree& ct = h->h->tree();
+        need(t >= 0 && t < ct.num_nodes() && s >= 0 && s < ct.num_nodes(), "local update: cluster id out of range");
+        need(k >= 0 && (k == 0 || (U != nullptr && V != nullptr)), "null factor");
+        const int64_t mt = ct.size(t), ms = ct.size(s);
+        h2b::DeviceArray<double> ud, vd;
+        ud.upload(U, size_t(mt * k));
+        const bool same = mt == ms && (U == V || (k && std::memcmp(U, V, size_t(mt * k) * sizeof(double)) == 0));
+        if (!same) vd.upload(V, size_t(ms * k));
+        *out = wrap_matrix(h2b::local_low_rank_update(*h->h, t, s, k, ud.data(), std::max<int64_t>(mt, 1),
+                                                      same ? ud.data() : vd.data(), std::max<int64_t>(ms, 1), eps,
+                                                      nullptr));
     });
 }
 int h2c_frobenius_norm(h2c_matrix h, double* out) {

@@ -1346,8 +1346,12 @@ int g_small_b = 2;            // symmetric few-vector path for b <= this (0 = of
 // sweep chain on a greatest-priority stream (0 = one stream)
 int g_dense_overlap = 1;
 // stage-5 split on one GPU (h2b_tune 9): the near field runs on the side
-// stream beside the sweeps and the leaf expansion adds its partial sums
-int g_dense_split = 1;
+// stream beside the sweeps and the leaf expansion adds its partial sums. Off by
+// default: measured on B200 it is slower at every b (cfg2 b=32 4.82 -> 5.00 ms,
+// cfg4 b=64 56.7 -> 57.5 ms; the DMMA-bound near field leaves no idle tensor
+// pipe for the sweeps, and ypart costs an extra write + read of n x b). Sharded
+// plans always split: there the near field hides the all-to-all.
+int g_dense_split = 0;
 
 // lazily create the fork/join streams and events of the overlapped few-vector path
 void ensure_side_streams(HgemvGraph& g) {

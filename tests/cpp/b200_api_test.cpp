@@ -115,6 +115,135 @@ TEST_CASE("max_rank_error is raised with the reference's exception type") {   //
     CHECK_THROWS_AS(peel_construct(DenseOperator(a, true), bt, cfg), max_rank_error);
 }
 
+TEST_CASE("sample_block_column hits exactly the requested block; rng advances like the reference's") {   // test_construction.cpp:39-59
+    std::mt19937_64 rng(50), op_rng(51);
+    auto ct = build_cluster_tree(grid1d(64, 0, 1), 8);
+    Matrix d = random_matrix(64, 1, op_rng);
+    Matrix dg(64, 64);
+    for (Index i = 0; i < 64; ++i) dg(i, i) = d(i, 0);
+    std::vector<int64_t> b(static_cast<size_t>(ct->num_nodes())), e(b.size());
+    std::vector<int> lv(b.size()), par(b.size()), c0(b.size()), c1(b.size());
+    detail::check(h2c_cluster_tree_nodes(ct->handle(), b.data(), e.data(), lv.data(), par.data(), c0.data(), c1.data(),
+                                         nullptr, nullptr));
+    const int t = c0[0], s = c1[0];
+    auto y0 = sample_block_column(DenseOperator(dg, true), *ct, t, s, 4, rng).second;
+    CHECK(fro(y0) == 0.0);
+    // the reference's stream: omega = fill_gaussian over the same engine, which the call advanced
+    std::mt19937_64 mirror(50);
+    Matrix skip = random_matrix(e[size_t(s)] - b[size_t(s)], 4, mirror);   // what the first call consumed
+    (void)skip;
+    Matrix a = random_matrix(64, 64, op_rng);
+    auto [omega, y] = sample_block_column(DenseOperator(a, false), *ct, t, s, 6, rng);
+    Matrix expect_omega = random_matrix(e[size_t(s)] - b[size_t(s)], 6, mirror);
+    CHECK(rel_err(omega, expect_omega) == 0.0);
+    std::vector<int64_t> perm(64);
+    detail::check(h2c_cluster_tree_perm(ct->handle(), perm.data()));
+    Matrix blk(e[size_t(t)] - b[size_t(t)], e[size_t(s)] - b[size_t(s)]);
+    for (Index i = 0; i < blk.rows(); ++i)
+        for (Index j = 0; j < blk.cols(); ++j) blk(i, j) = a(perm[size_t(b[size_t(t)] + i)], perm[size_t(b[size_t(s)] + j)]);
+    CHECK(rel_err(y, mul(blk, omega)) < 1e-12);
+}
+
+TEST_CASE("adaptive factorization: zero block in one increment, exact rank 3, max_rank") {   // test_construction.cpp:61-108
+    std::mt19937_64 op_rng(52);
+    auto ct = build_cluster_tree(grid1d(64, 0, 1), 8);
+    std::vector<int64_t> b(static_cast<size_t>(ct->num_nodes())), e(b.size());
+    std::vector<int> lv(b.size()), par(b.size()), c0(b.size()), c1(b.size());
+    detail::check(h2c_cluster_tree_nodes(ct->handle(), b.data(), e.data(), lv.data(), par.data(), c0.data(), c1.data(),
+                                         nullptr, nullptr));
+    std::vector<int64_t> perm(64);
+    detail::check(h2c_cluster_tree_perm(ct->handle(), perm.data()));
+    const int t = c0[0], s = c1[0];
+    Matrix d = random_matrix(64, 1, op_rng), dg(64, 64);
+    for (Index i = 0; i < 64; ++i) dg(i, i) = d(i, 0);
+    auto diag = DenseOperator(dg, true);
+    PeelConfig cfg;
+    diag.reset_counter();
+    BlockFactor f0 = adaptive_block_factorization(diag, *ct, t, s, 1e-8, cfg);
+    CHECK(f0.rank == 0);
+    CHECK(diag.columns_applied() == cfg.sample_block_size);
+    Matrix xf(64, 3), yf(64, 3);
+    for (Index i = b[size_t(t)]; i < e[size_t(t)]; ++i) {
+        Matrix r = random_matrix(1, 3, op_rng);
+        for (Index j = 0; j < 3; ++j) xf(perm[size_t(i)], j) = r(0, j);
+    }
+    for (Index i = b[size_t(s)]; i < e[size_t(s)]; ++i) {
+        Matrix r = random_matrix(1, 3, op_rng);
+        for (Index j = 0; j < 3; ++j) yf(perm[size_t(i)], j) = r(0, j);
+    }
+    Matrix a = mul(xf, yf, true);
+    auto op = DenseOperator(a, false);
+    PeelConfig tight;
+    tight.eps = 1e-12;
+    op.reset_counter();
+    BlockFactor f = adaptive_block_factorization(op, *ct, t, s, 1e-12, tight);
+    CHECK(f.rank == 3);
+    CHECK(op.columns_applied() <= 3 + tight.sample_block_size + 3);
+    Matrix blk(e[size_t(t)] - b[size_t(t)], e[size_t(s)] - b[size_t(s)]);
+    for (Index i = 0; i < blk.rows(); ++i)
+        for (Index j = 0; j < blk.cols(); ++j) blk(i, j) = a(perm[size_t(b[size_t(t)] + i)], perm[size_t(b[size_t(s)] + j)]);
+    CHECK(rel_err(mul(f.u, f.v, true), blk) < 1e-12);
+    PeelConfig capped;
+    capped.eps = 1e-10;
+    capped.max_rank = 2;
+    CHECK_THROWS_AS(adaptive_block_factorization(DenseOperator(random_matrix(64, 64, op_rng), false), *ct, t, s,
+                                                 1e-10, capped),
+                    max_rank_error);
+}
+
+TEST_CASE("to_dense, validate, frobenius_norm, low-rank updates") {   // h2_matrix.hpp:128-163, 308-404; algebra.hpp:119-137, 323-346
+    std::mt19937_64 rng(57);
+    Matrix g = random_matrix(96, 96, rng);
+    Matrix a = mul(g, g, true);
+    for (Index i = 0; i < 96; ++i) a(i, i) += 96.0;
+    auto op = DenseOperator(a, true);
+    auto bt = tree1d(96, 12, Admissibility::weak);
+    PeelConfig tight;
+    tight.eps = 1e-12;
+    auto h = peel_construct(op, bt, tight).matrix;
+    const Matrix dense = h.to_dense();
+    CHECK(rel_err(dense, a) < 1e-11);
+    CHECK_THROWS_AS(h.to_dense(50), std::invalid_argument);
+    auto rep = h.validate();
+    CHECK(rep.ok());
+    CHECK(rep.level_max_rank.size() == 4u);   // 96 points, leaf 12: depth 3
+    CHECK(rep.storage.total() > 0);
+    CHECK(h.orthonormal());
+    const double fn = frobenius_norm(h);
+    CHECK(std::abs(fn - fro(a)) <= 1e-10 * fro(a));
+    // global update A + x x^T keeps symmetric storage
+    LowRankFactor f{random_matrix(96, 2, rng), Matrix()};
+    f.Y = f.X;
+    auto h2 = low_rank_update(h, f, 1e-12);
+    CHECK(h2.symmetric());
+    CHECK(rel_err(h2.to_dense(), [&] {
+              Matrix r = a;
+              Matrix xx = mul(f.X, f.X, true);
+              for (Index j = 0; j < 96; ++j)
+                  for (Index i = 0; i < 96; ++i) r(i, j) += xx(i, j);
+              return r;
+          }()) < 1e-10);
+    // local update on the root's sibling pair (cluster order factors)
+    std::vector<int64_t> b(static_cast<size_t>(bt->row_tree().num_nodes())), e(b.size());
+    std::vector<int> lv(b.size()), par(b.size()), c0(b.size()), c1(b.size());
+    detail::check(h2c_cluster_tree_nodes(bt->row_tree().handle(), b.data(), e.data(), lv.data(), par.data(), c0.data(),
+                                         c1.data(), nullptr, nullptr));
+    const int t = c0[0], s = c1[0];
+    Matrix u = random_matrix(e[size_t(t)] - b[size_t(t)], 2, rng), v = random_matrix(e[size_t(s)] - b[size_t(s)], 2, rng);
+    auto h3 = local_low_rank_update(h, t, s, u, v, 1e-12);
+    const Matrix d3 = h3.to_dense();
+    std::vector<int64_t> perm(96);
+    detail::check(h2c_cluster_tree_perm(bt->row_tree().handle(), perm.data()));
+    Matrix expect = a;
+    const Matrix uv = mul(u, v, true);
+    for (Index i = 0; i < uv.rows(); ++i)
+        for (Index j = 0; j < uv.cols(); ++j) {
+            expect(perm[size_t(b[size_t(t)] + i)], perm[size_t(b[size_t(s)] + j)]) += uv(i, j);
+            expect(perm[size_t(b[size_t(s)] + j)], perm[size_t(b[size_t(t)] + i)]) += uv(i, j);   // symmetric mirror
+        }
+    CHECK(rel_err(d3, expect) < 1e-10);
+}
+
 MINI_MAIN
 
 TEST_CASE("diffusion oracle: registry, symmetric PSD Hessian, two marches per source") {   // test_oracles.cpp:205-238, 321-331
