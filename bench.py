@@ -35,6 +35,12 @@ CONFIGS = {
     # BASELINE.json configs[0] structure (hgemv part)
     "cfg1": dict(workload="2D exponential-kernel H2 hgemv N=16384 (128^2), leaf 64, rank 32, 1 vector",
                  grid=(128, 128), kind="exponential", ell=0.2, rank=32, b=1, leaf=64),
+    # BASELINE.json configs[0]'s build: peel_construct over DenseOperator of the 128^2 exponential kernel
+    # (eps 1e-4, max_rank 0), the matrix resident in HBM as the black box
+    "cfg1build": dict(workload="HARA peel_construct(DenseOperator(K)) of the 2D exponential kernel K=exp(-|x-y|/0.2) "
+                               "on the 128^2 grid (N=16384, dense 2.1 GB), strong admissibility eta=1, leaf 64, eps 1e-4, "
+                               "max_rank 0, PeelConfig defaults (b=16, p=10, seed 42)",
+                      grid=(128, 128), kind="exponential", ell=0.2, leaf=64, eps=1e-4, hara=True, dense=True),
     # BASELINE.json configs[2]: HARA from a black-box matvec of a diffusion Hessian: the reference's own
     # "diff1d-262144" oracle (registry.hpp:104-124; misfit + TV Hessian at the target density, two
     # Crank-Nicolson marches per source per application) with steps=64 as SURVEY §9.3 recommends,
@@ -546,9 +552,27 @@ def hara_problem(cfg, n):
     return pts, ct, bt, src
 
 
+def dense_kernel(cfg):
+    """(points, dense kernel matrix as a column-major host array) of a dense-black-box config."""
+    import torch
+    pts = grid_points(cfg["grid"])
+    p = torch.from_numpy(pts)
+    if torch.cuda.is_available():
+        p = p.cuda()
+    r = torch.cdist(p, p)
+    k = torch.exp(-r / cfg["ell"]) if cfg["kind"] == "exponential" else torch.exp(-(r / cfg["ell"]) ** 2)
+    return pts, np.asfortranarray(k.cpu().numpy())   # symmetric: C and F order hold the same numbers
+
+
 def hara_operator(cfg, n):
     """(black-box operator, block tree, keep-alive) of a HARA config."""
-    from paper_2003_10173_b200 import H2Operator, make_oracle
+    from paper_2003_10173_b200 import (Admissibility, DenseOperator, H2Operator, build_block_tree, build_cluster_tree,
+                                       make_oracle)
+    if cfg.get("dense"):
+        pts, a = dense_kernel(cfg)
+        ct = build_cluster_tree(pts, cfg["leaf"])
+        bt = build_block_tree(ct, ct, 1.0, Admissibility.strong)
+        return DenseOperator(a, True), bt, (pts, a)
     if cfg.get("pde"):
         o = make_oracle(f"diff1d-{n}", {"steps": str(cfg["steps"]), "leaf": str(cfg["leaf"])})
         return o.op, o.default_block_tree(), o
@@ -561,7 +585,7 @@ def run_hara(args, cfg, world, rank, local, dist):
     import torch
     from paper_2003_10173_b200 import PeelConfig, estimate_relative_error, peel_construct
     torch.cuda.set_device(local)
-    n = cfg["grid"][0]
+    n = int(np.prod(cfg["grid"]))
     op, bt, keep = hara_operator(cfg, n)
     rngs = {"device": 1, "reference": 0}
     pc = PeelConfig(eps=cfg["eps"], rng=rngs[args.hara_rng])
@@ -625,7 +649,7 @@ def run_hara(args, cfg, world, rank, local, dist):
     prof = [int(v) for v in res.matrix.rank_profile()]
     data = ("synthetic: the reference's diff1d oracle (target density, Ricker sources) marched on the device"
             if cfg.get("pde") else "synthetic (device-generated kernel H^2 black box)")
-    out = {"metric": "HARA build time (N=2^18, tol 1e-6)", "value": t, "unit": "s", "n_gpus": world,
+    out = {"metric": hara_metric(cfg), "value": t, "unit": "s", "n_gpus": world,
            "steps": steps, "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": data,
            "config": {"workload": cfg["workload"], "n": n, "eps": cfg["eps"], "rng": args.hara_rng,
@@ -636,7 +660,14 @@ def run_hara(args, cfg, world, rank, local, dist):
            "clocks": clk.summary()}
     if cfg.get("pde"):
         out["hara"]["pde_solves"] = keep.diffusion.pde_solves()
+    if cfg.get("dense"):
+        out["data"] = "synthetic: the dense kernel matrix generated on the device, applied as the black box from HBM"
     return out
+
+
+def hara_metric(cfg):
+    n = int(np.prod(cfg["grid"]))
+    return f"HARA build time (N={n}, tol {cfg['eps']:g})"
 
 
 def run_inversion(args, cfg, world, rank, local, dist):
@@ -697,23 +728,45 @@ def run_inversion(args, cfg, world, rank, local, dist):
             "clocks": clk.summary()}
 
 
+def ref_module():
+    """The reference's own compiled code (oracle/_ref) when present, else the restatement."""
+    try:
+        from oracle import pyref as M
+        return M, "reference"
+    except Exception:
+        from oracle import pyoracle as M
+        return M, "port"
+
+
 def cpu_hara_build(cfg, n, threads):
-    """One peel_construct on the CPU restatement (oracle) of the same problem:
-    (seconds, samples, operator seconds)."""
+    """One peel_construct on the CPU of the same problem: (seconds, samples,
+    operator seconds[, extra]). Dense configs run the reference's own compiled
+    construction (oracle/_ref) around a threaded dense black box."""
     from oracle import pyoracle as O
+    if cfg.get("dense"):
+        M, kind = ref_module()
+        pts, a = dense_kernel(cfg)
+        ref = M.Tree(pts, cfg["leaf"], 1.0, False)
+        t0 = time.perf_counter()
+        h, st, ops = M.peel_dense_threads(ref, a, True, eps=cfg["eps"], threads=threads)
+        t = time.perf_counter() - t0
+        prof = np.zeros(ref.depth + 1, np.int64)
+        np.maximum.at(prof, ref.level, h.ranks()[0])
+        return t, st["total"], ops, {"kind": kind, "level_samples": st["level_samples"],
+                                     "rank_profile": prof.tolist()}
     if cfg.get("pde"):
         d = O.Diff1D(n=n, steps=cfg["steps"])
         ref = O.Tree(d.points(), cfg["leaf"], 1.0, True)
         t0 = time.perf_counter()
         _, tot, ops = d.peel(ref, eps=cfg["eps"], threads=threads)
-        return time.perf_counter() - t0, tot, ops
+        return time.perf_counter() - t0, tot, ops, {"kind": "port"}
     pts, ct, bt, src = hara_problem(cfg, n)
     ref = O.Tree(pts, cfg["leaf"], 1.0, True)
     rr, _ = src.ranks()
     osrc = O.H2.from_packed(ref, True, rr, None, src.download())
     t0 = time.perf_counter()
     _, tot = O.peel_h2(ref, osrc, eps=cfg["eps"])
-    return time.perf_counter() - t0, tot, None
+    return time.perf_counter() - t0, tot, None, {"kind": "port"}
 
 
 def cpu_baseline_hara(args, cfg):
@@ -721,9 +774,18 @@ def cpu_baseline_hara(args, cfg):
     at N = sample_n, next to the B200 on the same sample."""
     import torch
     from paper_2003_10173_b200 import PeelConfig, peel_construct
+    if cfg.get("dense"):   # the full build (about a minute on the host cores): no smaller sample of this config
+        threads = os.cpu_count()
+        n = int(np.prod(cfg["grid"]))
+        tc, tot, ops, ex = cpu_hara_build(cfg, n, threads)
+        return {"value": tc, "unit": "s", "cores": threads, "kind": ex["kind"],
+                "sample": f"the full N={n} build, 1 step ({'the reference construction compiled from its headers' if ex['kind'] == 'reference' else 'oracle restatement'}, "
+                          f"single-threaded as written, around a dense black box applied on {threads} threads): "
+                          f"{tot} samples, operator applies {ops:.1f} s",
+                "level_samples": ex["level_samples"], "rank_profile": ex["rank_profile"]}
     n = cfg["sample_n"]
     threads = os.cpu_count() if cfg.get("pde") else 1
-    tc, tot, ops = cpu_hara_build(cfg, n, threads)
+    tc, tot, ops, _ = cpu_hara_build(cfg, n, threads)
     op, bt, keep = hara_operator(cfg, n)
     peel_construct(op, bt, PeelConfig(eps=cfg["eps"], rng=0))
     torch.cuda.synchronize()
@@ -746,13 +808,13 @@ def reference_hara(args, cfg, world):
     if cfg.get("pde"):
         n = cfg["grid"][0]
         threads = os.cpu_count()
-        t, tot, ops = cpu_hara_build(cfg, n, threads)
+        t, tot, ops, _ = cpu_hara_build(cfg, n, threads)
         cb = {"value": t, "unit": "s", "cores": threads, "kind": "port",
               "sample": f"the full N={n} build, 1 step: {tot} samples, operator applies {ops:.1f} s on {threads} "
                         f"threads, construction {t - ops:.1f} s on 1 thread (oracle restatement; Eigen absent)"}
     else:
         cb = cpu_baseline_hara(args, cfg)
-    return {"impl": "reference", "metric": "HARA build time (N=2^18, tol 1e-6)", "value": cb["value"], "unit": "s",
+    return {"impl": "reference", "metric": hara_metric(cfg), "value": cb["value"], "unit": "s",
             "n_gpus": world, "steps": 1, "warmup": 0, "higher_is_better": False,
             "config": {"workload": cfg["workload"]}, "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -806,6 +868,11 @@ def main():
         if rank == 0 and not args.no_cpu_baseline:
             try:
                 out["cpu_baseline"] = cpu_baseline_hara(args, cfg)
+                cb = out["cpu_baseline"]
+                if "level_samples" in cb and args.hara_rng == "reference":
+                    out["hara"]["same_samples_and_ranks_as_cpu"] = (
+                        cb["level_samples"] == out["hara"]["level_samples"] and
+                        cb["rank_profile"] == out["hara"]["rank_profile"])
             except Exception as e:
                 out["cpu_baseline"] = {"value": None, "error": repr(e)}
         if rank == 0:

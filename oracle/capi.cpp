@@ -368,6 +368,72 @@ int ora_peel_dense(ora_tree* t, const double* a, int symmetric, double eps, int6
     });
 }
 
+// peel_construct over a dense black box applied by `nthreads` host threads
+// (y = A x rows split across threads, A^T x output rows = columns of A): the
+// reference's construction code, single-threaded as it is, around a threaded
+// user operator. *op_seconds = wall time inside the operator.
+int ora_peel_dense_threads(ora_tree* t, const double* a, int symmetric, double eps, uint64_t seed, double norm_scale,
+                           int nthreads, ora_h2** o, int64_t* total_samples, int64_t* level_samples,
+                           int64_t* level_max_rank, int* nlevels, double* op_seconds) {
+    return guard([&] {
+        const Index n = t->ct->n();
+        const int nt = std::max(1, nthreads);
+        double op_s = 0;
+        auto apply = [&](const Matrix& x, bool trans) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const Index b = x.cols();
+            Matrix y(n, b);
+            const double* xp = x.data();
+            double* yp = y.data();
+            std::vector<std::thread> th;
+            for (int w = 0; w < nt; ++w)
+                th.emplace_back([&, w] {
+                    const Index r0 = n * w / nt, r1 = n * (w + 1) / nt;
+                    if (!trans) {   // y[r0:r1, :] = A[r0:r1, :] x  (A column-major: stream each column's slice)
+                        for (Index j = 0; j < b; ++j)
+                            for (Index i = r0; i < r1; ++i) yp[i + j * n] = 0.0;
+                        for (Index k = 0; k < n; ++k) {
+                            const double* ac = a + k * n;
+                            for (Index j = 0; j < b; ++j) {
+                                const double xk = xp[k + j * n];
+                                double* yc = yp + j * n;
+                                for (Index i = r0; i < r1; ++i) yc[i] += ac[i] * xk;
+                            }
+                        }
+                    } else {        // y[i, :] = A[:, i]^T x for i in [r0, r1)
+                        for (Index i = r0; i < r1; ++i) {
+                            const double* ac = a + i * n;
+                            for (Index j = 0; j < b; ++j) {
+                                const double* xc = xp + j * n;
+                                double acc = 0;
+                                for (Index k = 0; k < n; ++k) acc += ac[k] * xc[k];
+                                yp[i + j * n] = acc;
+                            }
+                        }
+                    }
+                });
+            for (auto& x2 : th) x2.join();
+            op_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return y;
+        };
+        auto op = make_operator(n, symmetric != 0, [&](const Matrix& x) { return apply(x, false); },
+                                [&](const Matrix& x) { return apply(x, true); });
+        PeelConfig cfg;
+        cfg.eps = eps;
+        cfg.seed = seed;
+        cfg.norm_scale = norm_scale;
+        PeelResult r = peel_construct(*op, t->bt, cfg);
+        *total_samples = r.stats.total;
+        *nlevels = int(r.stats.levels.size());
+        for (size_t i = 0; i < r.stats.levels.size(); ++i) {
+            level_samples[i] = r.stats.levels[i].samples;
+            level_max_rank[i] = r.stats.levels[i].max_rank;
+        }
+        *op_seconds = op_s;
+        *o = new ora_h2{std::move(r.matrix)};
+    });
+}
+
 // peel_construct over an H2Operator of another oracle matrix
 int ora_peel_h2(ora_tree* t, ora_h2* src, double eps, uint64_t seed, double norm_scale, ora_h2** o,
                 int64_t* total_samples) {

@@ -68,6 +68,7 @@ _sig("ora_low_rank_update", vp, i64, vp, vp, f64, P(vp))
 _sig("ora_frobenius_norm", vp, P(f64))
 _sig("ora_peel_dense", vp, vp, i32, f64, i64, i64, i64, u64, f64, P(vp), P(i64), vp, vp, P(i32))
 _sig("ora_peel_h2", vp, vp, f64, u64, f64, P(vp), P(i64))
+_sig("ora_peel_dense_threads", vp, vp, i32, f64, u64, f64, i32, P(vp), P(i64), vp, vp, P(i32), P(f64))
 _sig("ora_pnorm2_dense", vp, i64, i32, P(f64), P(i32))
 _sig("ora_sample_block_column", vp, vp, i32, i32, i32, i64, u64, vp, vp)
 _sig("ora_adaptive_block_factorization", vp, vp, i32, i32, i32, f64, i64, i64, i64, u64, vp, vp, P(i64), P(f64),
@@ -285,6 +286,23 @@ def peel_dense(tree, a, symmetric, eps=1e-4, b=16, p=10, max_rank=0, seed=42, no
                                float(norm_scale), C.byref(h), C.byref(tot), _p(ls), _p(lr), C.byref(nl)))
     return H2(h, tree), {"total": tot.value, "level_samples": ls[:nl.value].tolist(),
                          "level_max_rank": lr[:nl.value].tolist()}
+
+
+def peel_dense_threads(tree, a, symmetric, eps=1e-4, seed=42, norm_scale=0.0, threads=1):
+    """peel_construct over a dense black box applied on `threads` host threads ->
+    (H2, stats, operator seconds)."""
+    a = np.asfortranarray(a, np.float64)
+    h = vp()
+    tot = i64()
+    ls = np.zeros(64, np.int64)
+    lr = np.zeros(64, np.int64)
+    nl = i32()
+    ops = f64()
+    _check(_lib.ora_peel_dense_threads(tree._h, _p(a), int(symmetric), float(eps), int(seed), float(norm_scale),
+                                       int(threads), C.byref(h), C.byref(tot), _p(ls), _p(lr), C.byref(nl),
+                                       C.byref(ops)))
+    return H2(h, tree), {"total": tot.value, "level_samples": ls[:nl.value].tolist(),
+                         "level_max_rank": lr[:nl.value].tolist()}, ops.value
 
 
 def peel_h2(tree, src, eps=1e-4, seed=42, norm_scale=0.0):
