@@ -11,7 +11,7 @@ BIN = os.path.join(ROOT, "tests", "cpp", "build", "b200_api_test")
 
 def build():
     os.makedirs(os.path.dirname(BIN), exist_ok=True)
-    subprocess.run(["g++", "-std=c++17", "-O2", "-march=x86-64-v3", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
+    subprocess.run(["g++", "-std=c++17", "-O3", "-march=x86-64-v3", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
                     "-I/usr/local/cuda/include", os.path.join(ROOT, "tests", "cpp", "b200_api_test.cpp"),
                     "-L" + os.path.join(ROOT, "paper_2003_10173_b200", "lib"), "-lh2b200",
                     "-Wl,-rpath," + os.path.join(ROOT, "paper_2003_10173_b200", "lib"), "-o", BIN], check=True)
