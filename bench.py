@@ -71,8 +71,32 @@ CONFIGS = {
 }
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_PEAK_TFLOPS = 37.1   # DMMA m8n8k4 f64 measured on this pool's B200 (profiles/fp64_peak.txt)
-FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA m8n8k4 f64 on B200 (profiles/fp64_peak.txt)"
+def _fp64_peak():
+    """FP64 tensor-path roofline denominator: profiles/fp64_peak.json (tools/measure_fp64_peak.py,
+    DMMA m8n8k4 measured on this pool's B200 with SM clocks recorded), else the round-1 figure."""
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        clk = d.get("clocks", {})
+        return d["dmma_tflops"], (f"measured: tools/fp64_peak.cu DMMA m8n8k4 f64 on B200 at SM "
+                                  f"{clk.get('sm_mhz')} MHz (max {clk.get('sm_max_mhz')}), profiles/fp64_peak.json")
+    except (OSError, KeyError, ValueError):
+        return 37.1, "measured round 1: tools/fp64_peak.cu DMMA m8n8k4 f64 (profiles/r01/fp64_peak.txt, no clock record)"
+
+
+FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = _fp64_peak()
+
+
+def ncu_traffic(config):
+    """DRAM bytes per launch of the config's dominant kernel from its committed
+    `ncu --set full` capture (tools/ncu_traffic.py -> profiles/ncu_traffic_<config>.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")) as f:
+            d = json.load(f)
+        return d["traffic_bytes_per_launch"], f"profiles/ncu_traffic_{config}.json ({d['kernel'][:60]}, {d['when']})"
+    except (OSError, KeyError, ValueError):
+        return None, None
 
 
 def grid_points(shape):
@@ -264,8 +288,9 @@ def stage5_roofline(args, m, n, b, F5, stages):
              "sym_pass64_kernel (dense near-field, each canonical block streamed once) + seg_gemm leaf expansion "
              "+ csr_sum")
     roof.update({"kernel": kname, "share_of_step": dom["ms"] / sum(s["ms"] for s in stages.values()),
-                 "traffic": args.traffic, "algorithmic_gflop": dom["gflop"], "algorithmic_gbytes": dom["gbytes"],
-                 "ms": dom["ms"]})
+                 "traffic": args.traffic, "traffic_source": args.traffic_source,
+                 "traffic_over_algorithmic": (args.traffic / (dom["gbytes"] * 1e9)) if args.traffic else None,
+                 "algorithmic_gflop": dom["gflop"], "algorithmic_gbytes": dom["gbytes"], "ms": dom["ms"]})
     return roof
 
 
@@ -449,13 +474,8 @@ def run_b200(args, cfg, world, rank, local, dist):
         "value": value, "unit": "GFLOP/s", "gbytes_per_s": gbs, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-generated kernel matrix)",
-        "config": {"workload": cfg["workload"], "n": n, "vectors": b, "rank": cfg["rank"], "leaf": cfg["leaf"],
-                   "kernel": f"{cfg['kind']} ell={cfg['ell']}", "admissible_leaves": int(len(bt.admissible_leaves)),
-                   "dense_leaves": int(len(bt.dense_leaves)),
-                   "parallelism": (f"row-subtree sharded x{world} (one NCCL all-to-all of x-hat / x halos per "
-                                   f"hgemv, {int(sharded.plan.recv_rows.sum()) * b * 8} B received by rank 0)")
-                   if sharded is not None else "single GPU",
-                   "l2": "inputs larger than L2 (8.6 GB matrix, no flush needed)"},
+        "config": hgemv_config(cfg, args, n, b, len(bt.admissible_leaves), len(bt.dense_leaves), world,
+                               int(sharded.plan.recv_rows.sum()) * b * 8 if sharded is not None else None),
         "algorithmic": {"gflop_per_step": F / 1e9, "gbytes_per_step": Bbytes / 1e9},
         "stages": {str(k): v for k, v in sorted(stages.items())},
         "roofline": roof,
@@ -491,11 +511,21 @@ def cpu_baseline_sample(args, ctx):
             "seconds": t, "load_s": t_load, "parity_rel_err_full_size": relerr}
 
 
+def hgemv_config(cfg, args, n, b, tree_adm, tree_dense, world, recv_bytes=None):
+    """The `config` dict of an hgemv line (identical on the B200 and reference arms)."""
+    return {"workload": cfg["workload"], "n": n, "vectors": b, "rank": cfg["rank"], "leaf": cfg["leaf"],
+            "kernel": f"{cfg['kind']} ell={cfg['ell']}", "admissible_leaves": int(tree_adm),
+            "dense_leaves": int(tree_dense),
+            "parallelism": (f"row-subtree sharded x{world} (one NCCL all-to-all of x-hat / x halos per hgemv, "
+                            f"{recv_bytes} B received by rank 0)") if recv_bytes is not None else "single GPU",
+            "l2": "inputs larger than L2 (8.6 GB matrix, no flush needed)"}
+
+
 def run_reference(args, cfg, world, rank):
-    """--impl reference: the CPU port of the reference (oracle) on the host
-    cores, same config/metric; one step = one oracle hgemv over a bounded
-    sample of the vectors: up to two vectors per host thread, all host threads;
-    the step count is bounded so the arm finishes within a few minutes)."""
+    """--impl reference: the CPU restatement of the reference (oracle) on the host
+    cores, same config/metric/payload; one step = one oracle hgemv over a
+    bounded sample of the vectors: up to two vectors per host thread, all host
+    threads; the step count is bounded so the arm finishes within a few minutes."""
     from oracle import pyoracle as O
     if rank != 0:
         return None
@@ -506,7 +536,8 @@ def run_reference(args, cfg, world, rank):
     n = pts.shape[0]
     t0 = time.perf_counter()
     tree = O.Tree(pts, cfg["leaf"], 1.0, False)
-    h = O.H2.fixed_rank(tree, cfg["rank"], 42, threads)
+    # the same kernel H^2 as the B200 arm (host restatement of its generator, to rounding)
+    h = O.H2.kernel(tree, cfg["kind"], cfg["ell"], cfg["rank"], threads)
     setup = time.perf_counter() - t0
     x = np.asfortranarray(np.random.default_rng(42).standard_normal((n, bs)))
     # algorithmic flops for bs vectors (SURVEY §8d formula)
@@ -520,8 +551,11 @@ def run_reference(args, cfg, world, rank):
     Fcol += 2 * float(np.sum(sz[tree.brow[dense]].astype(np.float64) * sz[tree.bcol[dense]]))
     nth = min(threads, bs)
     t0 = time.perf_counter()
-    h.matvec(x, threads=nth)   # warm-up (also sizes the step budget)
+    h.matvec(x, threads=nth)   # first warm-up step (also sizes the step budget)
     t1 = time.perf_counter() - t0
+    warm = max(1, min(args.warmup, int(30.0 / max(t1, 1e-3))))
+    for _ in range(warm - 1):
+        h.matvec(x, threads=nth)
     steps = max(2, min(args.steps, int(150.0 / max(t1, 1e-3))))
     ts = []
     for _ in range(steps):
@@ -532,13 +566,15 @@ def run_reference(args, cfg, world, rank):
     v = Fcol * bs / t / 1e9
     return {"impl": "reference", "metric": "hgemv GFLOP/s (N=2^20, 32 vectors, fp64)" if args.config == "cfg2"
             else f"hgemv GFLOP/s ({args.config})", "value": v, "unit": "GFLOP/s", "n_gpus": world,
-            "steps": steps, "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (fixed-rank content)",
-            "config": {"workload": cfg["workload"], "n": n, "vectors": b, "rank": cfg["rank"]},
+            "steps": steps, "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (the B200 arm's kernel H^2: host restatement of its generator)",
+            "config": hgemv_config(cfg, args, n, b, len(tree.adm), len(tree.dense), 1),
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": nth, "kind": "port",
                              "sample": f"{bs} of {b} vectors per step ({bs // nth} per host thread, {nth} threads), "
-                                       f"oracle restatement of the reference (Eigen absent; SURVEY 8c); "
-                                       f"{steps} steps (bounded to ~150 s)"},
+                                       f"oracle restatement of the reference's matvec (h2_matrix.hpp:246-305; its "
+                                       f"GEMM beats the Eigen-shim build of the reference's own headers by ~25%, so "
+                                       f"the faster CPU arm is reported); {steps} steps (bounded to ~150 s)"},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "setup_s": setup}
 
@@ -833,8 +869,8 @@ def main():
     ap.add_argument("--hara-rng", default="device", choices=["device", "reference"],
                     help="cfg3 Gaussian panels: device Philox (perf) or the reference host stream")
     ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes/launch of the dominant kernel from an ncu --set full capture "
-                         "(default for cfg2: the committed capture, profiles/ncu_full_cfg2_r01_v6.txt)")
+                    help="dram bytes/launch of the dominant kernel (default: the committed ncu --set full capture "
+                         "profiles/ncu_traffic_<config>.json written by tools/ncu_traffic.py)")
     args = ap.parse_args()
     # NCCL communicator setup (ranks, rings / NVLS) on stderr; stdout carries only the JSON line
     os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -844,10 +880,9 @@ def main():
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     cfg = CONFIGS[args.config]
-    if args.traffic is None and args.config == "cfg2":
-        # ncu --set full of the stage-5 kernel (dram__bytes_read.sum + dram__bytes_write.sum):
-        # 8.242 GB + 0.267 GB per launch, profiles/ncu_full_cfg2_r01_v6.txt
-        args.traffic = 8.241948e9 + 0.266976e9
+    args.traffic_source = "command line" if args.traffic is not None else None
+    if args.traffic is None:
+        args.traffic, args.traffic_source = ncu_traffic(args.config)
     world, rank, local, dist = dist_setup(args)
     if cfg.get("inversion"):
         if args.impl == "reference":

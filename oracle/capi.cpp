@@ -183,6 +183,179 @@ int ora_fixed_rank_h2(ora_tree* t, int64_t k, uint64_t seed, int nthreads, ora_h
     });
 }
 
+// kernel-matrix H^2 content on the host: a CPU restatement of the product's
+// benchmark generator (paper_2003_10173_b200/csrc/matrix.cu make_kernel_h2,
+// SURVEY §8d option (ii)) so the reference arm multiplies the same payload as
+// the B200 arm (to rounding: exp/cos on the host vs the device). Symmetric,
+// rank min(k, |v|) per node: Chebyshev tensor grids, Lagrange leaf bases and
+// transfers, S = K(grid_t, grid_s), D = K(x_t, x_s). kind 0 exponential,
+// 1 Gaussian, 2 Matern-3/2.
+}  // extern "C"
+namespace {
+struct KGrid {
+    double lo[3], hi[3];
+    int p[3];
+};
+double kval(int kind, double ell, double r2) {
+    if (kind == 1) return std::exp(-r2 / (ell * ell));
+    const double r = std::sqrt(r2);
+    if (kind == 0) return std::exp(-r / ell);
+    const double a = 1.7320508075688772 * r / ell;
+    return (1.0 + a) * std::exp(-a);
+}
+double knode(const KGrid& g, int ax, int i) {
+    const int p = g.p[ax];
+    const double c = 0.5 * (g.lo[ax] + g.hi[ax]), h = 0.5 * (g.hi[ax] - g.lo[ax]);
+    if (p == 1) return c;
+    return c + h * std::cos(3.14159265358979323846 * (2 * i + 1) / (2.0 * p));
+}
+double klagrange(const KGrid& g, int dim, int a, const double* x) {
+    double v = 1.0;
+    for (int d = 0; d < dim; ++d) {
+        const int ia = a % g.p[d];
+        a /= g.p[d];
+        const double xa = knode(g, d, ia);
+        for (int j = 0; j < g.p[d]; ++j)
+            if (j != ia) {
+                const double xj = knode(g, d, j);
+                v *= (x[d] - xj) / (xa - xj);
+            }
+    }
+    return v;
+}
+void kgrid_point(const KGrid& g, int dim, int a, double* x) {
+    for (int d = 0; d < dim; ++d) {
+        x[d] = knode(g, d, a % g.p[d]);
+        a /= g.p[d];
+    }
+}
+void kaxis_counts(int dim, int k, const double* ext, int* p) {
+    int order[3] = {0, 1, 2};
+    for (int i = 1; i < dim && i < 3; ++i)
+        for (int j = i; j > 0 && ext[order[j]] > ext[order[j - 1]]; --j) std::swap(order[j], order[j - 1]);
+    for (int d = 0; d < 3; ++d) p[d] = 1;
+    int rem = k;
+    std::vector<int> f(size_t(dim), 1);
+    for (int d = dim - 1; d >= 0; --d) {
+        int best = 1;
+        const double target = std::pow(double(rem), 1.0 / double(d + 1));
+        for (int q = 1; q <= rem; ++q)
+            if (rem % q == 0 && std::abs(q - target) < std::abs(best - target)) best = q;
+        f[size_t(d)] = best;
+        rem /= best;
+    }
+    std::sort(f.begin(), f.end(), std::greater<int>());
+    f[0] *= rem;
+    for (int d = 0; d < dim; ++d) p[order[d]] = f[size_t(d)];
+}
+template <class F>
+void parallel_for(int64_t n, int nthreads, F&& f) {
+    const int nt = std::max(1, nthreads);
+    std::vector<std::thread> th;
+    for (int w = 0; w < nt; ++w)
+        th.emplace_back([&, w] {
+            for (int64_t i = w; i < n; i += nt) f(i);
+        });
+    for (auto& t : th) t.join();
+}
+}  // namespace
+extern "C" {
+
+int ora_kernel_h2(ora_tree* t, const double* coords, int kind, double ell, int64_t rank, int nthreads, ora_h2** o) {
+    return guard([&] {
+        const ClusterTree& ct = *t->ct;
+        const int nn = ct.num_nodes(), dim = ct.dim();
+        const Index n = ct.n();
+        H2Matrix h = H2Matrix::zero(t->bt, true);
+        std::vector<KGrid> grids(static_cast<size_t>(nn));
+        for (int v = 0; v < nn; ++v) {
+            const auto& nd = ct.node(v);
+            h.row_basis.set_rank(v, std::min<Index>(rank, nd.size()));
+            KGrid& g = grids[size_t(v)];
+            double ext[3] = {0, 0, 0}, diam = 0;
+            for (int d = 0; d < 3; ++d) {
+                g.lo[d] = d < dim ? nd.box.lo[size_t(d)] : 0.0;
+                g.hi[d] = d < dim ? nd.box.hi[size_t(d)] : 0.0;
+                ext[d] = d < dim ? g.hi[d] - g.lo[d] : 0;
+                diam += ext[d] * ext[d];
+            }
+            diam = std::sqrt(diam);
+            for (int d = 0; d < dim; ++d)
+                if (ext[d] < 1e-9 * std::max(diam, 1e-300)) {
+                    const double w = std::max(1e-3 * diam, 1e-12);
+                    g.lo[d] -= w;
+                    g.hi[d] += w;
+                    ext[d] = g.hi[d] - g.lo[d];
+                }
+            kaxis_counts(dim, int(h.row_basis.rank(v)), ext, g.p);
+        }
+        auto pt = [&](Index user, double* x) {
+            for (int d = 0; d < dim; ++d) x[d] = coords[user + d * n];
+        };
+        for (int v : ct.leaves()) {
+            const auto& nd = ct.node(v);
+            const Index m = nd.size(), k = h.row_basis.rank(v);
+            Matrix u(m, k);
+            for (Index a = 0; a < k; ++a)
+                for (Index i = 0; i < m; ++i) {
+                    double x[3];
+                    pt(ct.perm()[size_t(nd.begin + i)], x);
+                    u(i, a) = klagrange(grids[size_t(v)], dim, int(a), x);
+                }
+            h.row_basis.leaf_basis(v) = std::move(u);
+        }
+        for (int v = 0; v < nn; ++v) {
+            const int par = ct.node(v).parent;
+            if (par < 0) continue;
+            const Index kc = h.row_basis.rank(v), kp = h.row_basis.rank(par);
+            Matrix e(kc, kp);
+            for (Index ap = 0; ap < kp; ++ap)
+                for (Index ac = 0; ac < kc; ++ac) {
+                    double x[3];
+                    kgrid_point(grids[size_t(v)], dim, int(ac), x);
+                    e(ac, ap) = klagrange(grids[size_t(par)], dim, int(ap), x);
+                }
+            h.row_basis.transfer(v) = std::move(e);
+        }
+        const auto& adm = t->bt->admissible_leaves();
+        parallel_for(int64_t(adm.size()), nthreads, [&](int64_t i) {
+            const int b = adm[size_t(i)];
+            if (!h.stores(b)) return;
+            const auto& bn = t->bt->node(b);
+            const Index kr = h.row_basis.rank(bn.row), kc = h.row_basis.rank(bn.col);
+            Matrix sm(kr, kc);
+            for (Index c = 0; c < kc; ++c)
+                for (Index a = 0; a < kr; ++a) {
+                    double x[3], y[3], r2 = 0;
+                    kgrid_point(grids[size_t(bn.row)], dim, int(a), x);
+                    kgrid_point(grids[size_t(bn.col)], dim, int(c), y);
+                    for (int d = 0; d < dim; ++d) r2 += (x[d] - y[d]) * (x[d] - y[d]);
+                    sm(a, c) = kval(kind, ell, r2);
+                }
+            h.coupling[size_t(i)] = std::move(sm);
+        });
+        const auto& den = t->bt->dense_leaves();
+        parallel_for(int64_t(den.size()), nthreads, [&](int64_t i) {
+            const int b = den[size_t(i)];
+            if (!h.stores(b)) return;
+            const auto& bn = t->bt->node(b);
+            const auto &tr = ct.node(bn.row), &tc = ct.node(bn.col);
+            Matrix dm(tr.size(), tc.size());
+            for (Index j = 0; j < tc.size(); ++j)
+                for (Index r = 0; r < tr.size(); ++r) {
+                    double x[3], y[3], r2 = 0;
+                    pt(ct.perm()[size_t(tr.begin + r)], x);
+                    pt(ct.perm()[size_t(tc.begin + j)], y);
+                    for (int d = 0; d < dim; ++d) r2 += (x[d] - y[d]) * (x[d] - y[d]);
+                    dm(r, j) = kval(kind, ell, r2);
+                }
+            h.dense[size_t(i)] = std::move(dm);
+        });
+        h.orthonormal = false;
+        *o = new ora_h2{std::move(h)};
+    });
+}
+
 // H2Matrix::zero (h2_matrix.hpp:53-75)
 int ora_zero(ora_tree* t, int symmetric, ora_h2** o) {
     return guard([&] { *o = new ora_h2{H2Matrix::zero(t->bt, symmetric != 0)}; });

@@ -53,6 +53,7 @@ _sig("ora_tree_arrays", vp, *([vp] * 12))
 _sig("ora_tree_boxes", vp, vp, vp)
 _sig("ora_random_h2", vp, i32, i64, u64, P(vp))
 _sig("ora_zero", vp, i32, P(vp))
+_sig("ora_kernel_h2", vp, vp, i32, f64, i64, i32, P(vp))
 _sig("ora_fixed_rank_h2", vp, i64, u64, i32, P(vp))
 _lib.ora_h2_destroy.argtypes = [vp]
 _lib.ora_h2_destroy.restype = None
@@ -183,6 +184,16 @@ class H2:
         """Symmetric fixed-rank content (CPU-only benchmark inputs)."""
         h = vp()
         _check(_lib.ora_fixed_rank_h2(tree._h, int(k), int(seed), int(threads), C.byref(h)))
+        return H2(h, tree)
+
+    @staticmethod
+    def kernel(tree, kind="gaussian", ell=0.1, rank=32, threads=1):
+        """Kernel-matrix H^2 (host restatement of the product's benchmark generator,
+        csrc/matrix.cu make_kernel_h2): symmetric, Chebyshev interpolation."""
+        kinds = {"exponential": 0, "gaussian": 1, "matern32": 2}
+        h = vp()
+        _check(_lib.ora_kernel_h2(tree._h, _p(tree.points), kinds[kind], float(ell), int(rank), int(threads),
+                                  C.byref(h)))
         return H2(h, tree)
 
     @staticmethod

@@ -106,3 +106,21 @@ def test_full_size_cfg2_properties(cuda):
     yu = torch.empty_like(yi)
     yu[perm] = yi
     assert float(torch.linalg.norm(yu - hx) / torch.linalg.norm(hx)) < 1e-15
+
+
+@pytest.mark.parametrize("kind,grid,rank", [("gaussian", (40, 40), 32), ("exponential", (32, 32), 16),
+                                            ("matern32", (12, 12, 12), 32)])
+def test_kernel_generator_matches_host_restatement(cuda, kind, grid, rank):
+    """The benchmark payload (device generator, csrc/matrix.cu) equals its host
+    restatement (oracle ora_kernel_h2) that the reference arm multiplies."""
+    from paper_2003_10173_b200 import H2Matrix, build_block_tree, build_cluster_tree
+    pts = O.grid2d(*grid) if len(grid) == 2 else O.grid3d(*grid)
+    ct = build_cluster_tree(pts, 32)
+    bt = build_block_tree(ct, ct, 1.0)
+    m = H2Matrix.kernel(bt, pts, kind, 0.1, rank)
+    h = O.H2.kernel(O.Tree(pts, 32), kind, 0.1, rank, threads=4)
+    assert np.array_equal(m.ranks()[0], h.ranks()[0])
+    dm, dh = m.download(), h.export()
+    for k in ("U", "E", "S", "D"):
+        assert dm[k].shape == dh[k].shape
+        assert np.abs(dm[k] - dh[k]).max() <= 1e-12 * max(1.0, np.abs(dh[k]).max()), k
