@@ -11,6 +11,7 @@
 #include <numeric>
 
 #include "la.hpp"
+#include "dmma_tile.cuh"
 
 namespace h2b {
 namespace la {
@@ -44,62 +45,105 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ---------------------------------------------------------------------------
-// batched GEMM: one 32x32 output tile per CTA (256 threads, 2x2 per thread)
+// batched GEMM on the FP64 tensor path: one 32x32 output tile per CTA, four
+// warps of 16x16 DMMA (mma.sync m8n8k4 f64) fragments, K in 32-wide chunks
+// double-buffered through shared memory with cp.async (dmma_tile.cuh formats)
 // ---------------------------------------------------------------------------
 struct GemmTile {
     int desc, m0, n0, kbeg, kend;
     double* part;   // split-K partial (m x n, ld m) or null: write C with alpha/beta
 };
 
-__global__ void __launch_bounds__(256) bgemm_kernel(const GemmDesc* __restrict__ descs,
-                                                    const GemmTile* __restrict__ tiles) {
-    __shared__ double As[32][33];
-    __shared__ double Bs[32][33];
+// stage a KC x C tile whose C index is contiguous in global (element (k, c) at
+// base[c + k * ld], i.e. op(B) = B^T) into the "kc" layout
+template <int C, int KC, int NT>
+__device__ __forceinline__ void load_kc_rows(double* tile, const double* base, int64_t ld, int kv, int cv, int tid) {
+    constexpr int KP = KC + 4, NE = C * KC;
+#pragma unroll
+    for (int p0 = 0; p0 < NE; p0 += NT) {
+        const int p = p0 + tid;
+        if (NE % NT == 0 || p < NE) {
+            const int c = p % C, k = p / C;
+            const bool ok = k < kv && c < cv;
+            tile::cp_async8(tile + c * KP + k, ok ? base + c + k * ld : base, ok ? 8 : 0);
+        }
+    }
+}
+
+constexpr int kGemmMT = 32, kGemmNB = 32, kGemmKC = 32, kGemmThreads = 128;
+
+__global__ void __launch_bounds__(kGemmThreads) bgemm_kernel(const GemmDesc* __restrict__ descs,
+                                                             const GemmTile* __restrict__ tiles) {
+    constexpr int MT = kGemmMT, NB = kGemmNB, KC = kGemmKC, KP = KC + 4, NT = kGemmThreads;
+    constexpr int WM = 2, WN = 2, TM = MT / (WM * 8), TN = NB / (WN * 8);
+    constexpr int A_SZ = MT * KP, B_SZ = NB * KP, ST_SZ = A_SZ + B_SZ;
+    __shared__ __align__(16) double smem[2 * ST_SZ];
     const GemmTile t = tiles[blockIdx.x];
     const GemmDesc d = descs[t.desc];
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    double acc[2][2] = {{0, 0}, {0, 0}};
-    for (int k0 = t.kbeg; k0 < t.kend; k0 += 32) {
-        for (int e = tid; e < 1024; e += 256) {
-            int i, kk;
-            if (!d.ta) { i = e & 31; kk = e >> 5; } else { kk = e & 31; i = e >> 5; }
-            const int gi = t.m0 + i, gk = k0 + kk;
-            double v = 0;
-            if (gi < d.m && gk < t.kend) v = d.ta ? d.A[gk + int64_t(gi) * d.lda] : d.A[gi + int64_t(gk) * d.lda];
-            As[kk][i] = v;
-            int j;
-            if (!d.tb) { kk = e & 31; j = e >> 5; } else { j = e & 31; kk = e >> 5; }
-            const int gj = t.n0 + j, gk2 = k0 + kk;
-            double w = 0;
-            if (gj < d.n && gk2 < t.kend) w = d.tb ? d.B[gj + int64_t(gk2) * d.ldb] : d.B[gk2 + int64_t(gj) * d.ldb];
-            Bs[kk][j] = w;
-        }
-        __syncthreads();
-        const int kend = min(32, t.kend - k0);
-        for (int kk = 0; kk < kend; ++kk) {
-            const double a0 = As[kk][tx], a1 = As[kk][tx + 16];
-            const double b0 = Bs[kk][ty], b1 = Bs[kk][ty + 16];
-            acc[0][0] = fma(a0, b0, acc[0][0]);
-            acc[0][1] = fma(a0, b1, acc[0][1]);
-            acc[1][0] = fma(a1, b0, acc[1][0]);
-            acc[1][1] = fma(a1, b1, acc[1][1]);
-        }
-        __syncthreads();
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int wm = warp % WM, wn = warp / WM, g = lane >> 2, t4 = lane & 3;
+    const int rv = min(MT, d.m - t.m0), cv = min(NB, d.n - t.n0);
+    int offa[TM], offb[TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int m = (wm * TM + i) * 8 + g;
+        offa[i] = d.ta ? m * KP + t4 : t4 * MT + (m ^ (t4 << 2));
     }
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int j = 0; j < TN; ++j) offb[j] = ((wn * TN + j) * 8 + g) * KP + t4;
+    double acc[TM][TN][2];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const int i = t.m0 + tx + 16 * a, j = t.n0 + ty + 16 * b;
-            if (i < d.m && j < d.n) {
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    auto issue = [&](int stage, int k0) {
+        double* at = smem + stage * ST_SZ;
+        double* bt = at + A_SZ;
+        const int kv = min(KC, t.kend - k0);
+        if (!d.ta) tile::load_mc<MT, KC, NT, false>(at, d.A + t.m0 + int64_t(k0) * d.lda, d.lda, rv, kv, tid);
+        else tile::load_kc<MT, KC, NT, false>(at, d.A + k0 + int64_t(t.m0) * d.lda, d.lda, kv, rv, tid);
+        if (!d.tb) tile::load_kc<NB, KC, NT, false>(bt, d.B + k0 + int64_t(t.n0) * d.ldb, d.ldb, kv, cv, tid);
+        else load_kc_rows<NB, KC, NT>(bt, d.B + t.n0 + int64_t(k0) * d.ldb, d.ldb, kv, cv, tid);
+        tile::cp_async_commit();
+    };
+    const int nchunks = t.kend > t.kbeg ? (t.kend - t.kbeg + KC - 1) / KC : 0;
+    if (nchunks > 0) issue(0, t.kbeg);
+    for (int c = 0; c < nchunks; ++c) {
+        const int k0 = t.kbeg + c * KC;
+        if (c + 1 < nchunks) {
+            issue((c + 1) & 1, k0 + KC);
+            tile::cp_async_wait<1>();
+        } else {
+            tile::cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* at = smem + (c & 1) * ST_SZ;
+        const double* bt = at + A_SZ;
+        const int ksteps = (min(KC, t.kend - k0) + 3) >> 2;
+        if (d.ta) tile::chunk_mma<MT, KC, TM, TN, true>(at, bt, acc, offa, offb, ksteps);
+        else tile::chunk_mma<MT, KC, TM, TN, false>(at, bt, acc, offa, offb, ksteps);
+        __syncthreads();   // the next issue overwrites this stage
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int m = (wm * TM + i) * 8 + g;
+        if (m >= rv) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int nn = (wn * TN + j) * 8 + 2 * t4 + h;
+                if (nn >= cv) continue;
+                const int gi = t.m0 + m, gj = t.n0 + nn;
+                const double v = acc[i][j][h];
                 if (t.part) {
-                    t.part[i + int64_t(j) * d.m] = acc[a][b];
+                    t.part[gi + int64_t(gj) * d.m] = v;
                 } else {
-                    double* c = d.C + i + int64_t(j) * d.ldc;
-                    *c = d.beta == 0.0 ? d.alpha * acc[a][b] : d.alpha * acc[a][b] + d.beta * *c;
+                    double* cp = d.C + gi + int64_t(gj) * d.ldc;
+                    *cp = d.beta == 0.0 ? d.alpha * v : d.alpha * v + d.beta * *cp;
                 }
             }
-        }
+    }
 }
 
 // split-K reduction in a fixed order: C = alpha sum_p part[p] + beta C
@@ -426,7 +470,7 @@ void bgemm(const std::vector<GemmDesc>& d, cudaStream_t s) {
     if (tiles.empty()) return;
     DevVec<GemmDesc> dd(d, s);
     DevVec<GemmTile> dt(tiles, s);
-    bgemm_kernel<<<unsigned(tiles.size()), 256, 0, s>>>(dd.p, dt.p);
+    bgemm_kernel<<<unsigned(tiles.size()), kGemmThreads, 0, s>>>(dd.p, dt.p);
     H2B_LAUNCH();
     if (!splits.empty()) {
         DevVec<SplitDesc> ds(splits, s);

@@ -11,8 +11,9 @@ import bench
 from paper_2003_10173_b200 import PeelConfig, peel_construct
 
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg3k"]
-op, bt, keep = bench.hara_operator(cfg, cfg["grid"][0])
-pc = PeelConfig(eps=cfg["eps"], rng=1)
+import numpy as np
+op, bt, keep = bench.hara_operator(cfg, int(np.prod(cfg["grid"])))
+pc = PeelConfig(eps=cfg["eps"], rng=int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 peel_construct(op, bt, pc)
 torch.cuda.synchronize()
 t = time.perf_counter()

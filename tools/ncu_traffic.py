@@ -15,32 +15,40 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # dominant kernel per config (name regex for ncu) and how many matching launches to skip
 # (past the warm-up and the stage-timed calls, into the steady state)
+# (demangled-name regex, launches to skip, description)
 TARGETS = {
-    "cfg2": ("regex:seg_gemm_kernel", "mode 2 (kModeY leaf expansion + dense near field)"),
-    "cfg4": ("regex:seg_gemm_kernel", "mode 2 (kModeY leaf expansion + dense near field)"),
-    "cfg2b1": ("regex:sym_pass64_kernel", "symmetric few-vector dense block pass"),
-    "cfg1": ("regex:sym_pass64_kernel", "symmetric few-vector dense block pass"),
+    "cfg2": (r"regex:seg_gemm_kernel<64, 32, 4, 1, 2, 32", 4,
+             "seg_gemm kModeY (leaf expansion + dense near field): the longest captured launch"),
+    "cfg4": (r"regex:seg_gemm_kernel<64, 32, 4, 1, 2, 32", 4,
+             "seg_gemm kModeY (leaf expansion + dense near field): the longest captured launch"),
+    "cfg2b1": (r"regex:sym_pass64_kernel", 5, "symmetric few-vector dense block pass"),
+    "cfg1": (r"regex:sym_pass64_kernel", 5, "symmetric few-vector dense block pass"),
 }
 
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-    name, what = TARGETS[cfg]
+    name, skip, what = TARGETS[cfg]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     rep = os.path.join(ROOT, "gpurun_out", f"ncu_traffic_{cfg}")
-    cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "--kernel-name", name,
-           "--launch-skip", "40", "--launch-count", "4", "-f", "-o", rep,
+    cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "--kernel-name-base", "demangled",
+           "--kernel-name", name, "--launch-skip", str(skip), "--launch-count", "6", "-f", "-o", rep,
            sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "3", "--warmup", "3",
            "--no-cpu-baseline"]
     subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL)
     out = subprocess.run(["ncu", "-i", rep + ".ncu-rep", "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "%": 1.0, "": 1.0}
     launches = []
     for row in rows[2:]:
         d = dict(zip(hdr, row))
-        num = lambda k: float(d.get(k, "nan").replace(",", "") or "nan")
+
+        def num(k, d=d):   # to bytes / nanoseconds, whatever unit ncu chose for this column
+            v = d.get(k, "")
+            return float(v.replace(",", "")) * scale.get(units.get(k, ""), 1.0) if v else float("nan")
         launches.append({"kernel": d.get("Kernel Name", ""), "duration_ns": num("gpu__time_duration.sum"),
                          "dram_read_bytes": num("dram__bytes_read.sum"), "dram_write_bytes": num("dram__bytes_write.sum"),
                          "l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
