@@ -788,5 +788,53 @@ int ora_peel_diff1d(ora_tree* t, ora_diff1d* d, int include_tv, double eps, uint
 
 #endif  // ORA_REFERENCE_HEADERS
 
+#ifdef ORA_REFERENCE_HEADERS
+// The reference's own hierarchical inversion drivers (inversion.hpp:137-311),
+// oracle/_ref only: h_newton_schulz (method 0) / h_hyperpower (1, arg = order)
+// from X0 = scaled_identity_start(A) (:124-130) with a fixed (dynamic = 0) or
+// dynamic threshold schedule. rows: (iter, residual, eps_k, samples, seconds)
+// per rebuild, up to max_rows. Returns the divergence status in *converged
+// (1 converged, 0 divergence_error) instead of throwing, keeping the trace.
+int ora_h_inverse(ora_h2* a, int method, int arg, int dynamic, double eps_initial, double eps, uint64_t seed,
+                  int max_iter, ora_h2** x_out, double* rows, int max_rows, int* num_rows, double* final_residual,
+                  int* converged) {
+    return guard([&] {
+        H2Matrix x0 = scaled_identity_start(a->h);
+        ThresholdSchedule sched;
+        sched.mode = dynamic ? ThresholdSchedule::Mode::dynamic : ThresholdSchedule::Mode::fixed;
+        sched.eps_initial = eps_initial;
+        PeelConfig cfg;
+        cfg.eps = eps;
+        cfg.seed = seed;
+        ConvergenceTrace tr;
+        H2Matrix x;
+        try {
+            HInverseResult r = method == 0 ? h_newton_schulz(a->h, x0, sched, eps, cfg, max_iter)
+                                           : h_hyperpower(a->h, x0, arg, sched, eps, cfg, max_iter);
+            tr = std::move(r.trace);
+            x = std::move(r.X);
+            *converged = tr.converged ? 1 : 0;
+        } catch (const divergence_error& e) {
+            tr = e.trace;
+            x = x0;
+            *converged = 0;
+        }
+        *num_rows = int(tr.rows.size());
+        for (int i = 0; i < *num_rows && i < max_rows; ++i) {
+            rows[5 * i + 0] = tr.rows[size_t(i)].iter;
+            rows[5 * i + 1] = tr.rows[size_t(i)].residual;
+            rows[5 * i + 2] = tr.rows[size_t(i)].eps_k;
+            rows[5 * i + 3] = double(tr.rows[size_t(i)].samples);
+            rows[5 * i + 4] = tr.rows[size_t(i)].wall_seconds;
+        }
+        *final_residual = tr.final_residual;
+        *x_out = new ora_h2{std::move(x)};
+    });
+}
+int ora_residual_norm(ora_h2* a, ora_h2* x, double* out) {   // inversion.hpp:222-225
+    return guard([&] { *out = residual_norm(a->h, x->h); });
+}
+#endif
+
 }  // extern "C"
 

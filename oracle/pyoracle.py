@@ -51,6 +51,8 @@ _lib.ora_tree_destroy.restype = None
 _sig("ora_tree_info", vp, P(i64), P(i32), P(i32), P(i32), P(i32), P(i32))
 _sig("ora_tree_arrays", vp, *([vp] * 12))
 _sig("ora_tree_boxes", vp, vp, vp)
+_sig("ora_h_inverse", vp, i32, i32, i32, f64, f64, u64, i32, P(vp), vp, i32, P(i32), P(f64), P(i32))
+_sig("ora_residual_norm", vp, vp, P(f64))
 _sig("ora_random_h2", vp, i32, i64, u64, P(vp))
 _sig("ora_zero", vp, i32, P(vp))
 _sig("ora_kernel_h2", vp, vp, i32, f64, i64, i32, P(vp))
@@ -278,6 +280,22 @@ class H2:
         st = np.zeros(4, np.int64)
         _check(_lib.ora_validate(self._h, int(ortho_cap), C.byref(nv), _p(prof), _p(st)))
         return nv.value, prof.tolist(), st.tolist()
+
+    def h_inverse(self, eps, method=0, order=2, dynamic=True, eps_initial=1e-2, seed=42, max_iter=64):
+        """oracle/_ref only: the reference's h_newton_schulz / h_hyperpower from
+        scaled_identity_start -> (X, trace rows, final residual, converged)."""
+        rows = np.zeros((512, 5))
+        nr, fr, cv = i32(), f64(), i32()
+        h = vp()
+        _check(_lib.ora_h_inverse(self._h, int(method), int(order), int(dynamic), float(eps_initial), float(eps),
+                                  int(seed), int(max_iter), C.byref(h), _p(rows), 512, C.byref(nr), C.byref(fr),
+                                  C.byref(cv)))
+        return H2(h, self.tree), rows[:min(nr.value, 512)], fr.value, bool(cv.value)
+
+    def residual_norm(self, x):
+        v = f64()
+        _check(_lib.ora_residual_norm(self._h, x._h, C.byref(v)))
+        return v.value
 
     def frobenius_norm(self):
         v = f64()
