@@ -36,9 +36,14 @@ vp, i32, i64, u64, f64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double
 P = C.POINTER
 
 
+# entries only one of the two builds exports: the diffusion oracle (restatement
+# only) and the reference's own inversion drivers (oracle/_ref only)
+_OPTIONAL = {"ora_h_inverse", "ora_residual_norm"}
+
+
 def _sig(name, *args):
-    if _REF_BUILD and not hasattr(_lib, name):
-        return   # restatement-only entry (e.g. the diffusion oracle)
+    if (_REF_BUILD or name in _OPTIONAL) and not hasattr(_lib, name):
+        return
     f = getattr(_lib, name)
     f.restype = i32
     f.argtypes = list(args)

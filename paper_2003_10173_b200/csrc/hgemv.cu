@@ -601,6 +601,129 @@ __global__ void __launch_bounds__(256) sym_pass64_kernel(const SymBlock* __restr
     }
 }
 
+// ---------------------------------------------------------------------------
+// sym_pass64 with bulk-async (TMA engine) staging: a persistent CTA per SM, one
+// producer warp streams whole canonical blocks (each stored contiguously,
+// R*C*8 bytes) into an NSTAGE-deep shared-memory ring with
+// cp.async.bulk + mbarrier transaction counts, and consumer warp w works on
+// stage w. Up to NSTAGE*32 KB per SM stay in flight without any register or
+// scoreboard cost on the consumers, which read the block from shared memory.
+// Same arithmetic and output slots as sym_pass64_kernel (bitwise equal).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int B, int NSTAGE>
+__global__ void __launch_bounds__((NSTAGE + 1) * 32, 1) sym_tma64_kernel(const SymBlock* __restrict__ blocks,
+                                                                         int nblocks, const double* __restrict__ src,
+                                                                         double* __restrict__ scratch, int64_t b) {
+    extern __shared__ __align__(128) double ring[];   // NSTAGE x 64 x 64
+    __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == NSTAGE) {   // producer
+        if (lane == 0) {
+            int g = 0;
+            for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x, ++g) {
+                const int st = g % NSTAGE;
+                if (g >= NSTAGE) mbar_wait(&empty[st], ((g / NSTAGE) - 1) & 1);
+                const SymBlock d = blocks[blk];
+                const unsigned bytes = unsigned(d.R) * unsigned(d.C) * 8u;
+                mbar_expect_tx(&full[st], bytes);
+                bulk_g2s(ring + st * 4096, d.A, bytes, &full[st]);
+            }
+        }
+        return;
+    }
+    int g = warp;
+    for (int blk = blockIdx.x + warp * gridDim.x; blk < nblocks; blk += NSTAGE * gridDim.x, g += NSTAGE) {
+        const int st = warp;   // == g % NSTAGE
+        const SymBlock d = blocks[blk];
+        const int R = d.R, C = d.C;
+        const double* xs = src + d.xs_unit * b;
+        const double* xt = src + d.xt_unit * b;
+        const int rr = lane * 2;
+        const bool vr = rr < R;
+        double xa[B], xb[B], ua[B], ub[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            xa[q] = vr ? xt[rr + q * R] : 0.0;
+            xb[q] = vr ? xt[rr + 1 + q * R] : 0.0;
+            ua[q] = ub[q] = 0.0;
+        }
+        const bool want_w = d.w_off >= 0;
+        double* w = want_w ? scratch + d.w_off * b : nullptr;
+        const double* A = ring + st * 4096;
+        mbar_wait(&full[st], (g / NSTAGE) & 1);
+#pragma unroll 2
+        for (int j0 = 0; j0 < C; j0 += 8) {
+            double p[8][B];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = j0 + jj;
+                const bool vj = j < C;
+                double2 a = make_double2(0.0, 0.0);
+                if (vr && vj) a = *reinterpret_cast<const double2*>(A + j * R + rr);
+#pragma unroll
+                for (int q = 0; q < B; ++q) {
+                    const double xj = vj ? __ldg(xs + j + q * C) : 0.0;
+                    ua[q] = fma(a.x, xj, ua[q]);
+                    ub[q] = fma(a.y, xj, ub[q]);
+                    p[jj][q] = fma(a.x, xa[q], a.y * xb[q]);
+                }
+            }
+            if (want_w) {
+#pragma unroll
+                for (int sft = 4; sft >= 1; sft >>= 1) {
+                    const bool up = lane & sft;
+#pragma unroll
+                    for (int k = 0; k < sft; ++k)
+#pragma unroll
+                        for (int q = 0; q < B; ++q) {
+                            const double send = up ? p[k][q] : p[k + sft][q];
+                            const double keep = up ? p[k + sft][q] : p[k][q];
+                            p[k][q] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+                        }
+                }
+#pragma unroll
+                for (int q = 0; q < B; ++q) {
+                    p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 8);
+                    p[0][q] += __shfl_xor_sync(0xffffffffu, p[0][q], 16);
+                }
+                const int j = j0 + lane;
+                if (lane < 8 && j < C)
+#pragma unroll
+                    for (int q = 0; q < B; ++q) w[j + q * C] = p[0][q];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);   // the stage may be refilled
+        if (vr) {
+            double* u = scratch + d.u_off * b;
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                u[rr + q * R] = ua[q];
+                u[rr + 1 + q * R] = ub[q];
+            }
+        }
+    }
+}
+
 // per output unit, the fixed-order sum of its slots: mode 0 sets y-hat, mode 1
 // adds alpha * sum into the rows of y (user order through perm)
 __global__ void __launch_bounds__(256) csr_sum_kernel(const CsrUnit* __restrict__ units, int nunits,
@@ -1211,6 +1334,23 @@ int g_small_b = 2;            // symmetric few-vector path for b <= this (0 = of
 // gathered x) on a least-priority stream concurrently with the latency-bound
 // sweep chain on a greatest-priority stream (0 = one stream)
 int g_dense_overlap = 1;
+// few-vector dense block pass staged by bulk-async copies (h2b_tune 10): 1 on, 0 the register-streaming kernel
+int g_sym_tma = 1;
+constexpr int kSymStages = 6;
+constexpr int kSymSmem = kSymStages * 4096 * 8;
+int num_sms() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        H2B_CUDA(cudaGetDevice(&dev));
+        H2B_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        H2B_CUDA(cudaFuncSetAttribute(sym_tma64_kernel<1, kSymStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSymSmem));
+        H2B_CUDA(cudaFuncSetAttribute(sym_tma64_kernel<2, kSymStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSymSmem));
+        return v;
+    }();
+    return n;
+}
 // stage-5 split on one GPU (h2b_tune 9): the near field runs on the side
 // stream beside the sweeps and the leaf expansion adds its partial sums. Off by
 // default: measured on B200 it is slower at every b (cfg2 b=32 4.82 -> 5.00 ms,
@@ -1425,6 +1565,8 @@ void set_node_priorities(cudaGraph_t graph) {
     H2B_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
     const void* lo1 = reinterpret_cast<const void*>(sym_pass64_kernel<1>);
     const void* lo2 = reinterpret_cast<const void*>(sym_pass64_kernel<2>);
+    const void* lo3 = reinterpret_cast<const void*>(sym_tma64_kernel<1, kSymStages>);
+    const void* lo4 = reinterpret_cast<const void*>(sym_tma64_kernel<2, kSymStages>);
     for (cudaGraphNode_t nd : nodes) {
         cudaGraphNodeType ty;
         H2B_CUDA(cudaGraphNodeGetType(nd, &ty));
@@ -1432,7 +1574,7 @@ void set_node_priorities(cudaGraph_t graph) {
         cudaKernelNodeParams kp{};
         H2B_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
         cudaLaunchAttributeValue v{};
-        v.priority = (kp.func == lo1 || kp.func == lo2) ? least : greatest;
+        v.priority = (kp.func == lo1 || kp.func == lo2 || kp.func == lo3 || kp.func == lo4) ? least : greatest;
         H2B_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
     }
 }
@@ -1452,7 +1594,8 @@ void reserve_workspace(const HgemvPlan& plan, int64_t n, int64_t b, cudaStream_t
 }
 // the runtime knobs that change the launch sequence of an hgemv
 uint64_t knob_signature() {
-    uint64_t s = uint64_t(g_pdl & 0xff) | uint64_t(g_dense_overlap & 0xff) << 8 | uint64_t(g_dense_split & 0xff) << 48;
+    uint64_t s = uint64_t(g_pdl & 0xff) | uint64_t(g_dense_overlap & 0xff) << 8 | uint64_t(g_dense_split & 0xff) << 48 |
+                 uint64_t(g_sym_tma & 0xff) << 56;
     for (int i = 0; i < 4; ++i) s |= uint64_t(g_tune[i] & 0xff) << (16 + 8 * i);
     return s;
 }
@@ -1629,8 +1772,15 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                 else sym_pass32_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
             } else if (ld.kind == 3 && plan->sym64) {
                 const cudaStream_t ds = overlap ? sg.lo : stream;
-                if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, ds>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
-                else sym_pass64_kernel<2><<<grid, 256, 0, ds>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xint.data(), ws.scratch.data(), b);
+                const SymBlock* sb = plan->sym_blocks.data() + ld.item_begin;
+                // bulk-async staged variant (one persistent CTA per SM) when there are enough blocks to
+                // keep every SM's ring full (measured: cfg2 b=1 1.90 -> 1.84 ms; slower on cfg1's 2.5k blocks)
+                if (g_sym_tma > 0 && nitems >= 32 * num_sms()) {
+                    const unsigned tg = unsigned(std::min(nitems, num_sms()));
+                    if (b == 1) sym_tma64_kernel<1, kSymStages><<<tg, (kSymStages + 1) * 32, kSymSmem, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
+                    else sym_tma64_kernel<2, kSymStages><<<tg, (kSymStages + 1) * 32, kSymSmem, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
+                } else if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
+                else sym_pass64_kernel<2><<<grid, 256, 0, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
             } else if (ld.kind == 1 || ld.kind == 3) {
                 const double* src = ld.kind == 1 ? ws.xhat.data() : ws.xint.data();
                 if (b == 1) sym_pass_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
@@ -1935,6 +2085,10 @@ extern "C" int h2b_tune(int which, int value) {
     }
     if (which == 8) {   // few-vector path: dense pass concurrent with the sweeps (1) / serial (0)
         h2b::g_dense_overlap = value;
+        return 0;
+    }
+    if (which == 10) {   // few-vector dense block pass: bulk-async ring (1) / register streaming (0)
+        h2b::g_sym_tma = value;
         return 0;
     }
     if (which == 9) {   // stage-5 split (near field beside the sweeps) on (1) / off (0); plans rebuild lazily
