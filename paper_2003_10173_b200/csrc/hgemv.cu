@@ -840,6 +840,16 @@ struct HgemvPlan {
     // U_t E_t per leaf (m_t x k_parent): the finest downsweep step folded into
     // the leaf expansion, y_t += (U_t E_t) yhat_parent
     DeviceArray<double> ue;
+    // recorded on the legacy stream after the plan's uploads / U E products; an
+    // hgemv on any stream waits for it on the device (no host synchronisation,
+    // so a plan builds on the host while earlier device work still runs)
+    cudaEvent_t ready = nullptr;
+    HgemvPlan() = default;
+    HgemvPlan(const HgemvPlan&) = delete;
+    HgemvPlan& operator=(const HgemvPlan&) = delete;
+    ~HgemvPlan() {
+        if (ready) cudaEventDestroy(ready);
+    }
 };
 
 namespace {
@@ -1323,7 +1333,8 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     plan->leaf_m.upload(lm);
     lap(2);
     const auto ts = std::chrono::steady_clock::now();
-    H2B_CUDA(cudaDeviceSynchronize());
+    H2B_CUDA(cudaEventCreateWithFlags(&plan->ready, cudaEventDisableTiming));
+    H2B_CUDA(cudaEventRecord(plan->ready, nullptr));   // uploads and U E products were enqueued there
     g_plan_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count();
     return plan;
 }
@@ -1728,6 +1739,11 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     if (!dplan) own_plan = select_plan(h, transpose, b);
     const HgemvPlan* plan = dplan ? dplan : own_plan.get();
     reserve_workspace(*plan, n, b, stream, ws);
+    if (plan->ready) {   // the plan's device arrays were filled on the legacy stream
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        H2B_CUDA(cudaStreamIsCapturing(stream, &cs));
+        if (cs == cudaStreamCaptureStatusNone) H2B_CUDA(cudaStreamWaitEvent(stream, plan->ready, 0));
+    }
     const size_t need_d = size_t(plan->coef_down * b);
     const int* perm = user_order ? plan->perm->data() : nullptr;
     // few-vector path, unsharded, untimed: fork the sweep chain onto the greatest-priority
