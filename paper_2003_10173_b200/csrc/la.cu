@@ -415,96 +415,6 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const SvdJob* __restrict__ 
         }
 }
 
-// ---------------------------------------------------------------------------
-// one-sided Jacobi for problems with rows <= 32 and cols <= 32: one WARP per
-// problem, lane j holds column j of M and of V in registers. The same
-// tournament schedule and rotation rule as jacobi_kernel (cols/2 disjoint
-// pairs per round; rotate when |gamma| > 1e-15 sqrt(alpha beta)), but a round
-// is a register exchange with the partner lane instead of a CTA barrier, so
-// the recompression's many small SVDs (k <= 32 per node) cost microseconds.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) jacobi_warp_kernel(const SvdJob* __restrict__ jobs, int njobs) {
-    __shared__ int partner_s[8][32];
-    const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int w = blockIdx.x * 8 + wl;
-    if (w >= njobs) return;
-    const SvdJob jb = jobs[w];
-    const int r = jb.rows, c = jb.cols, ce = c + (c & 1);
-    int* partner = partner_s[wl];
-    double m[32], v[32], o[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        double x = 0.0;
-        if (lane < c && i < r) x = jb.trans ? jb.A[lane + int64_t(i) * jb.lda] : jb.A[i + int64_t(lane) * jb.lda];
-        m[i] = x;
-        v[i] = i == lane ? 1.0 : 0.0;
-    }
-    for (int sweep = 0; sweep < 60 && ce >= 2; ++sweep) {
-        bool rotated = false;
-        for (int round = 0; round < ce - 1; ++round) {
-            if (lane < ce / 2) {   // tournament pairing (fixed element 0, others rotate)
-                const int p = lane;
-                int a = p == 0 ? 0 : 1 + (p - 1 + round) % (ce - 1);
-                int b = 1 + (ce - 2 - p + round) % (ce - 1);
-                partner[a] = b;
-                partner[b] = a;
-            }
-            __syncwarp();
-            const int q = lane < ce ? partner[lane] : lane;
-            __syncwarp();
-            const bool is_a = lane < q;
-            double al = 0, be = 0, ga = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                o[i] = __shfl_sync(0xffffffffu, m[i], q);
-                if (i < r) {
-                    const double xa = is_a ? m[i] : o[i], xb = is_a ? o[i] : m[i];
-                    al += xa * xa;
-                    be += xb * xb;
-                    ga += xa * xb;
-                }
-            }
-            const bool rot = lane < ce && !(ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be));
-            rotated |= rot;
-            double cs = 1.0, sn = 0.0;
-            if (rot) {
-                const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                cs = 1.0 / sqrt(1.0 + t * t);
-                sn = cs * t;
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const double ov = __shfl_sync(0xffffffffu, v[i], q);
-                if (rot) {
-                    // a: x' = cs x - sn y ; b: y' = sn x + cs y  (x = column a, y = column b)
-                    m[i] = is_a ? cs * m[i] - sn * o[i] : sn * o[i] + cs * m[i];
-                    v[i] = is_a ? cs * v[i] - sn * ov : sn * ov + cs * v[i];
-                }
-            }
-        }
-        if (!__any_sync(0xffffffffu, rotated)) break;
-    }
-    double nrm = 0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-        if (i < r) nrm += m[i] * m[i];
-    nrm = sqrt(nrm);
-    // stable descending order: rank = #{j : nrm_j > nrm_lane, or equal with j < lane}
-    int rank = 0;
-    for (int j = 0; j < c; ++j) {
-        const double nj = __shfl_sync(0xffffffffu, nrm, j);
-        rank += (nj > nrm || (nj == nrm && j < lane)) ? 1 : 0;
-    }
-    if (lane < c) {
-        jb.sigma[rank] = nrm;
-        if (jb.V)
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (i < c) jb.V[i + int64_t(rank) * jb.ldv] = v[i];
-    }
-}
-
 constexpr size_t kSmemCap = 200 * 1024;   // bytes of dynamic shared memory per CTA
 
 __global__ void permute_rows_kernel(const double* __restrict__ in, int64_t ldi, double* __restrict__ out,
@@ -709,8 +619,6 @@ void bqr(const std::vector<QrDesc>& d, cudaStream_t s) {
     bgemm(g, s);
 }
 
-int g_jacobi_warp = 1;   // warp-per-problem Jacobi for <= 32 x 32 (h2b_la_tune 0)
-
 void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     std::vector<SvdJob> sj, gj;
     size_t smax = 0, gtot = 0;
@@ -718,14 +626,9 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
         const size_t ce = size_t(c + (c & 1));
         return size_t(r) * ce + ce * ce + ce + ce / 2;
     };
-    std::vector<SvdJob> wj;
     for (const SvdDesc& q : d) {
         if (q.rows <= 0 || q.cols <= 0) continue;
         SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr};
-        if (g_jacobi_warp && q.rows <= 32 && q.cols <= 32) {
-            wj.push_back(j);
-            continue;
-        }
         const size_t nd = need(q.rows, q.cols);
         if (nd * sizeof(double) <= kSmemCap) {
             sj.push_back(j);
@@ -734,11 +637,6 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
             gj.push_back(j);
             gtot += nd;
         }
-    }
-    if (!wj.empty()) {
-        DevVec<SvdJob> dj(wj, s);
-        jacobi_warp_kernel<<<unsigned((wj.size() + 7) / 8), 256, 0, s>>>(dj.p, int(wj.size()));
-        H2B_LAUNCH();
     }
     if (!sj.empty()) {
         DevVec<SvdJob> dj(sj, s);
@@ -873,12 +771,3 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
 
 }  // namespace la
 }  // namespace h2b
-
-// tuning hook (not part of the public ABI)
-extern "C" int h2b_la_tune(int which, int value) {
-    if (which == 0) {
-        h2b::la::g_jacobi_warp = value;
-        return 0;
-    }
-    return -1;
-}
