@@ -659,6 +659,7 @@ def run_hara(args, cfg, world, rank, local, dist):
     # one more build with the phase timers draining the stream at each phase end
     # (device-accurate phase split; not part of the timed steps)
     _l.h2b_hara_phase_sync(1)
+    _l.h2b_hara_phase_reset()
     _l.h2b_plan_build_ms(1)
     _l.h2b_plan_sync_ms(1)
     _l.h2b_plan_parts_ms((C.c_double * 4)(), 1)

@@ -896,7 +896,6 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
 PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, const PeelConfig& cfg,
                           cudaStream_t s) {
     const auto t_start = Clock::now();
-    std::fill(g_phase_ms, g_phase_ms + 16, 0.0);
     const ClusterTree& ct = *bt->tree;
     if (ct.n != op.dim()) throw std::invalid_argument("peel_construct: dimension mismatch");
     std::mt19937_64 rng(cfg.seed);
@@ -1019,6 +1018,11 @@ double estimate_relative_error(DevOperator& op, const H2Dev& h, double op_norm, 
 // device-accurate (slower builds); 0 (default) = no timing synchronisation
 extern "C" int h2b_hara_phase_sync(int on) {
     h2b::g_phase_sync = on;
+    return 0;
+}
+// the phase timers accumulate across builds until reset (an inversion runs many)
+extern "C" int h2b_hara_phase_reset() {
+    std::fill(h2b::g_phase_ms, h2b::g_phase_ms + 16, 0.0);
     return 0;
 }
 extern "C" int h2b_hara_phase_ms(double* out, int n) {

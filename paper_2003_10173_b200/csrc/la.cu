@@ -225,7 +225,7 @@ __device__ double block_sum(double v, double* red) {
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(256) qr_kernel(const QrJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(1024) qr_kernel(const QrJob* __restrict__ jobs) {
     extern __shared__ double sm[];
     __shared__ double red[33];
     const QrJob jb = jobs[blockIdx.x];
@@ -324,7 +324,7 @@ struct SvdJob {
 };
 
 template <bool SMEM>
-__global__ void __launch_bounds__(256) jacobi_kernel(const SvdJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__ jobs) {
     extern __shared__ double sm[];
     __shared__ int rotated;
     const SvdJob jb = jobs[blockIdx.x];
@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(256) jacobi_kernel(const SvdJob* __restrict__ 
 }
 
 constexpr size_t kSmemCap = 200 * 1024;   // bytes of dynamic shared memory per CTA
+constexpr int kWideCols = 40;              // QR / Jacobi problems with this many columns run on 1024 threads
 
 __global__ void permute_rows_kernel(const double* __restrict__ in, int64_t ldi, double* __restrict__ out,
                                     int64_t ldo, const int* __restrict__ perm, int64_t n, int64_t c, int scatter) {
@@ -515,15 +516,26 @@ void qr_direct(const std::vector<QrDesc>& d, cudaStream_t s) {
         }
     }
     if (!sj.empty()) {
-        DevVec<QrJob> dj(sj, s);
-        const size_t bytes = smax * sizeof(double);
         static const bool qr_attr = [] {   // once per process: the attribute call is a driver round trip
             H2B_CUDA(cudaFuncSetAttribute(qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
             return true;
         }();
         (void)qr_attr;
-        qr_kernel<true><<<unsigned(sj.size()), 256, bytes, s>>>(dj.p);
-        H2B_LAUNCH();
+        // wide problems get 32 warps (one per trailing column in the reflector update),
+        // narrow ones 8: two launches, each sized for its class
+        std::vector<QrJob> cls[2];
+        size_t cmax[2] = {0, 0};
+        for (const QrJob& j : sj) {
+            const int c = j.n >= kWideCols ? 1 : 0;
+            cls[c].push_back(j);
+            cmax[c] = std::max(cmax[c], qr_doubles(j.m, j.n, j.Q != nullptr));
+        }
+        for (int c = 0; c < 2; ++c) {
+            if (cls[c].empty()) continue;
+            DevVec<QrJob> dj(cls[c], s);
+            qr_kernel<true><<<unsigned(cls[c].size()), c ? 1024 : 256, cmax[c] * sizeof(double), s>>>(dj.p);
+            H2B_LAUNCH();
+        }
     }
     if (!gj.empty()) {
         DBuf work(gtot, s);
@@ -639,14 +651,25 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
         }
     }
     if (!sj.empty()) {
-        DevVec<SvdJob> dj(sj, s);
         static const bool jacobi_attr = [] {
             H2B_CUDA(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
             return true;
         }();
         (void)jacobi_attr;
-        jacobi_kernel<true><<<unsigned(sj.size()), 256, smax * sizeof(double), s>>>(dj.p);
-        H2B_LAUNCH();
+        // one warp per column pair: wide problems (>= kWideCols columns) get 32 warps
+        std::vector<SvdJob> cls[2];
+        size_t cmax[2] = {0, 0};
+        for (const SvdJob& j : sj) {
+            const int c = j.cols >= kWideCols ? 1 : 0;
+            cls[c].push_back(j);
+            cmax[c] = std::max(cmax[c], need(j.rows, j.cols));
+        }
+        for (int c = 0; c < 2; ++c) {
+            if (cls[c].empty()) continue;
+            DevVec<SvdJob> dj(cls[c], s);
+            jacobi_kernel<true><<<unsigned(cls[c].size()), c ? 1024 : 256, cmax[c] * sizeof(double), s>>>(dj.p);
+            H2B_LAUNCH();
+        }
     }
     if (!gj.empty()) {
         DBuf work(gtot, s);
