@@ -409,9 +409,20 @@ Truncation truncation_bases(const H2Dev& g, bool row_side, double eps, double le
             sv.push_back(LeftSvdDesc{Gv, k, c, k, U.at(size_t(v)), k, sg.at(size_t(v)),
                                      c > k ? P.at(size_t(v)) : nullptr, k});
         }
+        const auto tl = Clock::now();
         bcopy(cp, s);
         bgemm(gm, s);
         bleft_svd(sv, s);
+        if (g_trace_recompress && !sv.empty()) {   // diagnostics: per-level SVD batch shape and time
+            H2B_CUDA(cudaStreamSynchronize(s));
+            int km = 0, cm = 0;
+            for (const auto& q : sv) {
+                km = std::max(km, q.m);
+                cm = std::max(cm, q.c);
+            }
+            std::fprintf(stderr, "trunc_level side=%d l=%d problems=%zu kmax=%d cmax=%d ms=%.3f\n", int(row_side), l,
+                         sv.size(), km, cm, ms_since(tl));
+        }
     }
     std::vector<double> sh(sg.total);
     if (sg.total)

@@ -321,6 +321,8 @@ struct SvdJob {
     double* V;
     int ldv;
     double* work;
+    double* U;
+    int ldu;
 };
 
 template <bool SMEM>
@@ -372,12 +374,14 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
                     ma[i] = cs * x - sn * y;
                     mb[i] = sn * x + cs * y;
                 }
-                double* va = V + int64_t(a) * ce;
-                double* vb = V + int64_t(b) * ce;
-                for (int i = lane; i < ce; i += 32) {
-                    const double x = va[i], y = vb[i];
-                    va[i] = cs * x - sn * y;
-                    vb[i] = sn * x + cs * y;
+                if (jb.V) {   // right vectors only when asked for
+                    double* va = V + int64_t(a) * ce;
+                    double* vb = V + int64_t(b) * ce;
+                    for (int i = lane; i < ce; i += 32) {
+                        const double x = va[i], y = vb[i];
+                        va[i] = cs * x - sn * y;
+                        vb[i] = sn * x + cs * y;
+                    }
                 }
             }
             __syncthreads();
@@ -408,6 +412,12 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
     }
     __syncthreads();
     for (int j = tid; j < c; j += blockDim.x) jb.sigma[j] = nrm[order[j]];
+    if (jb.U)   // left vectors: the rotated columns, normalised, in the sorted order
+        for (int64_t e = tid; e < int64_t(r) * c; e += blockDim.x) {
+            const int i = int(e % r), j = int(e / r);
+            const double nj = nrm[order[j]];
+            jb.U[i + int64_t(j) * jb.ldu] = nj > 0.0 ? M[i + int64_t(order[j]) * r] / nj : 0.0;
+        }
     if (jb.V)
         for (int64_t e = tid; e < int64_t(c) * c; e += blockDim.x) {
             const int i = int(e % c), j = int(e / c);
@@ -640,7 +650,7 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     };
     for (const SvdDesc& q : d) {
         if (q.rows <= 0 || q.cols <= 0) continue;
-        SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr};
+        SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr, q.U, q.ldu};
         const size_t nd = need(q.rows, q.cols);
         if (nd * sizeof(double) <= kSmemCap) {
             sj.push_back(j);
@@ -757,7 +767,9 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
             to += size_t(q.c) * q.m;
             cp.push_back(CopyDesc{q.A, At, q.c, q.m, q.lda, q.c, 1});
             qrs.push_back(QrDesc{At, q.c, q.m, q.c, R, p, nullptr, 0});
-            svs.push_back(SvdDesc{R, p, p, p, 0, q.sigma, q.U, q.ldu});
+            // one-sided Jacobi on R^T (converges in far fewer sweeps than on R); its
+            // normalised rotated columns are the right singular vectors of R = left of A
+            svs.push_back(SvdDesc{R, p, p, p, 1, q.sigma, nullptr, 0, q.U, q.ldu});
             if (q.P && q.c > q.m) cp.push_back(CopyDesc{R, q.P, p, p, p, q.ldp, 1});
         } else {
             double* Q = qb.data() + qo;

@@ -104,8 +104,10 @@ struct SvdDesc {
     int rows, cols, lda;
     int trans;
     double* sigma;
-    double* V;
+    double* V;      // optional: right singular vectors (cols x cols)
     int ldv;
+    double* U = nullptr;   // optional: left singular vectors, the normalised rotated columns (rows x cols)
+    int ldu = 0;
 };
 void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s);
 
