@@ -1,6 +1,7 @@
 #pragma once
 // Error handling and device memory ownership shared by the B200 H^2 library.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -8,6 +9,16 @@
 #include <vector>
 
 namespace h2b {
+
+// NVTX range for the duration of a scope (visible in Nsight Systems / ncu
+// --nvtx; a few nanoseconds when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 // status codes mirror the reference's exception kinds (include/h2c.h)
 struct cuda_error : std::runtime_error {

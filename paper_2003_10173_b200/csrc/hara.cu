@@ -269,6 +269,7 @@ std::vector<int> ortho_ranks(const ClusterTree& ct, const BasisDev& b) {
 }  // namespace
 
 std::unique_ptr<H2Dev> orthogonalize(const H2Dev& h, cudaStream_t s) {
+    NvtxRange nvtx("orthogonalize");
     Phase ph(8, s);
     const ClusterTree& ct = h.tree();
     const BlockTree& bt = *h.bt;
@@ -321,6 +322,7 @@ struct Truncation {
 Truncation truncation_bases(const H2Dev& g, bool row_side, double eps, double level_corr,
                             const std::vector<std::vector<size_t>>& by_row,
                             const std::vector<std::vector<size_t>>& by_col, cudaStream_t s) {
+    NvtxRange nvtx("recompress truncation bases");
     const ClusterTree& ct = g.tree();
     const BlockTree& bt = *g.bt;
     const int nn = ct.num_nodes();
@@ -481,6 +483,7 @@ void project_basis(const ClusterTree& ct, const BasisDev& in, BasisDev& out, con
 }  // namespace
 
 std::unique_ptr<H2Dev> recompress(const H2Dev& hin, double eps, cudaStream_t s) {
+    NvtxRange nvtx("recompress");
     if (eps < 0) throw std::invalid_argument("recompress: eps must be >= 0");
     std::unique_ptr<H2Dev> own;
     const H2Dev* gp = &hin;
@@ -737,6 +740,7 @@ struct Range {
 std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
                                       const std::vector<std::pair<int, int>>& pairs, double tol_abs,
                                       const PeelConfig& cfg, std::mt19937_64& rng, DBuf& Qlev, int& cap, DBuf& Wi) {
+    NvtxRange nvtx("sample_level_group");
     const int64_t n = ct.n;
     cudaStream_t s = ctx.s;
     std::vector<Range> ranges(pairs.size());
@@ -906,6 +910,7 @@ std::vector<Range> sample_level_group(PeelContext& ctx, const ClusterTree& ct,
 
 PeelResult peel_construct(DevOperator& op, std::shared_ptr<const BlockTree> bt, const PeelConfig& cfg,
                           cudaStream_t s) {
+    NvtxRange nvtx("peel_construct");
     const auto t_start = Clock::now();
     const ClusterTree& ct = *bt->tree;
     if (ct.n != op.dim()) throw std::invalid_argument("peel_construct: dimension mismatch");

@@ -1614,6 +1614,7 @@ uint64_t knob_signature() {
 
 void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b, const double* x, int64_t ldx,
            double* y, int64_t ldy, double alpha, double beta, cudaStream_t stream, Workspace& ws) {
+    NvtxRange nvtx("hgemv");
     if (n != h.tree().n) throw std::invalid_argument("matvec: dimension mismatch");
     if (b < 1) throw std::invalid_argument("matvec: need at least one column");
     if (ldx < n || ldy < n) throw std::invalid_argument("matvec: leading dimension smaller than n");
@@ -1844,6 +1845,9 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         a.beta = beta;
         const bool vec = ld.vec && (ld.units_even || b % 2 == 0) &&
                          (reinterpret_cast<uintptr_t>(ws.xint.data()) % 16 == 0);
+        static const char* kStageName[6] = {"hgemv gather", "hgemv leaf upsweep", "hgemv transfer upsweep",
+                                            "hgemv coupling", "hgemv downsweep", "hgemv leaf + near field"};
+        NvtxRange nvs(kStageName[ld.stage >= 0 && ld.stage < 6 ? ld.stage : 0]);
         dispatch(a, ntasks, b, ld.mt, vec, ld.mode, ls);
         if (timer) timer->mark(stream);
     }
