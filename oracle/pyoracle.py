@@ -162,7 +162,7 @@ class Tree:
         return lo, hi
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:   # (module globals may be gone at exit)
             _lib.ora_tree_destroy(self._h)
             self._h = None
 
@@ -175,7 +175,7 @@ class H2:
         self.tree = tree
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.ora_h2_destroy(self._h)
             self._h = None
 
@@ -441,7 +441,7 @@ class Diff1D:
         self.n = int(c["n"])
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.ora_diff1d_destroy(self._h)
             self._h = None
 
