@@ -854,8 +854,12 @@ def cpu_hara_build(cfg, n, threads):
         d = O.Diff1D(n=n, steps=cfg["steps"])
         ref = O.Tree(d.points(), cfg["leaf"], 1.0, True)
         t0 = time.perf_counter()
-        _, tot, ops = d.peel(ref, eps=cfg["eps"], threads=threads)
-        return time.perf_counter() - t0, tot, ops, {"kind": "port"}
+        h, tot, ops = d.peel(ref, eps=cfg["eps"], threads=threads)
+        t = time.perf_counter() - t0
+        prof = np.zeros(ref.depth + 1, np.int64)
+        np.maximum.at(prof, ref.level, h.ranks()[0])
+        return t, tot, ops, {"kind": "port", "level_samples": d.last_stats["level_samples"],
+                             "rank_profile": prof.tolist()}
     pts, ct, bt, src = hara_problem(cfg, n)
     ref = O.Tree(pts, cfg["leaf"], 1.0, True)
     rr, _ = src.ranks()
@@ -904,10 +908,12 @@ def reference_hara(args, cfg, world):
     if cfg.get("pde"):
         n = cfg["grid"][0]
         threads = os.cpu_count()
-        t, tot, ops, _ = cpu_hara_build(cfg, n, threads)
+        t, tot, ops, ex = cpu_hara_build(cfg, n, threads)
         cb = {"value": t, "unit": "s", "cores": threads, "kind": "port",
               "sample": f"the full N={n} build, 1 step: {tot} samples, operator applies {ops:.1f} s on {threads} "
-                        f"threads, construction {t - ops:.1f} s on 1 thread (oracle restatement; Eigen absent)"}
+                        f"threads, construction {t - ops:.1f} s on 1 thread (oracle restatement of the construction "
+                        f"and of the diffusion black box)",
+              "level_samples": ex["level_samples"], "rank_profile": ex["rank_profile"]}
     else:
         cb = cpu_baseline_hara(args, cfg)
     return {"impl": "reference", "metric": hara_metric(cfg), "value": cb["value"], "unit": "s",

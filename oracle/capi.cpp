@@ -765,7 +765,8 @@ int ora_diff1d_state(ora_diff1d* d, int source, double* u) {
 // with hessian_operator(include_tv), diffusion1d.hpp:177-181); the operator
 // applies run on `nthreads` host threads (columns are independent)
 int ora_peel_diff1d(ora_tree* t, ora_diff1d* d, int include_tv, double eps, uint64_t seed, int nthreads, ora_h2** o,
-                    int64_t* total_samples, double* op_seconds) {
+                    int64_t* total_samples, double* op_seconds, int64_t* level_samples, int64_t* level_max_rank,
+                    int* nlevels) {
     return guard([&] {
         const Index n = d->d.n();
         double op_s = 0;
@@ -782,6 +783,11 @@ int ora_peel_diff1d(ora_tree* t, ora_diff1d* d, int include_tv, double eps, uint
         PeelResult r = peel_construct(*op, t->bt, cfg);
         *total_samples = r.stats.total;
         *op_seconds = op_s;
+        *nlevels = int(r.stats.levels.size());
+        for (size_t i = 0; i < r.stats.levels.size(); ++i) {
+            level_samples[i] = r.stats.levels[i].samples;
+            level_max_rank[i] = r.stats.levels[i].max_rank;
+        }
         *o = new ora_h2{std::move(r.matrix)};
     });
 }

@@ -92,7 +92,7 @@ if hasattr(_lib, "ora_diff1d_destroy"):
 _sig("ora_diff1d_info", vp, P(i64), P(i64), P(f64), P(f64), P(i64))
 _sig("ora_diff1d_hessvec", vp, i64, vp, vp, i32, i32)
 _sig("ora_diff1d_state", vp, i32, vp)
-_sig("ora_peel_diff1d", vp, vp, i32, f64, u64, i32, P(vp), P(i64), P(f64))
+_sig("ora_peel_diff1d", vp, vp, i32, f64, u64, i32, P(vp), P(i64), P(f64), vp, vp, P(i32))
 
 
 class OracleError(RuntimeError):
@@ -468,8 +468,13 @@ class Diff1D:
         """peel_construct(hessian_operator(include_tv), bt, {eps, seed}) on the CPU:
         returns (H2, total samples, seconds spent in operator applies)."""
         h, tot, ops = vp(), i64(), f64()
+        ls = np.zeros(64, np.int64)
+        lr = np.zeros(64, np.int64)
+        nl = i32()
         _check(_lib.ora_peel_diff1d(tree._h, self._h, int(include_tv), float(eps), int(seed), int(threads),
-                                    C.byref(h), C.byref(tot), C.byref(ops)))
+                                    C.byref(h), C.byref(tot), C.byref(ops), _p(ls), _p(lr), C.byref(nl)))
+        self.last_stats = {"total": tot.value, "level_samples": ls[:nl.value].tolist(),
+                           "level_max_rank": lr[:nl.value].tolist()}
         return H2(h, tree), tot.value, ops.value
 
     def points(self):

@@ -17,22 +17,20 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # (past the warm-up and the stage-timed calls, into the steady state)
 # (demangled-name regex, launches to skip, description)
 TARGETS = {
-    "cfg2": (r"regex:seg_gemm_kernel<64, 32, 4, 1, 2, 32", 4,
-             "seg_gemm kModeY (leaf expansion + dense near field): the longest captured launch"),
-    "cfg4": (r"regex:seg_gemm_kernel<64, 32, 4, 1, 2, 32", 4,
-             "seg_gemm kModeY (leaf expansion + dense near field): the longest captured launch"),
-    "cfg2b1": (r"regex:sym_pass64_kernel", 5, "symmetric few-vector dense block pass"),
-    "cfg1": (r"regex:sym_pass64_kernel", 5, "symmetric few-vector dense block pass"),
+    "cfg2": ("regex:seg_gemm_kernel", 30, 30, "seg_gemm kModeY (leaf expansion + dense near field): the longest captured launch"),
+    "cfg4": ("regex:seg_gemm_kernel", 30, 30, "seg_gemm kModeY (leaf expansion + dense near field): the longest captured launch"),
+    "cfg2b1": ("regex:sym_tma64_kernel|sym_pass64_kernel", 4, 2, "symmetric few-vector dense block pass"),
+    "cfg1": ("regex:sym_tma64_kernel|sym_pass64_kernel", 4, 2, "symmetric few-vector dense block pass"),
 }
 
 
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-    name, skip, what = TARGETS[cfg]
+    name, skip, count, what = TARGETS[cfg]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     rep = os.path.join(ROOT, "gpurun_out", f"ncu_traffic_{cfg}")
-    cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "--kernel-name-base", "demangled",
-           "--kernel-name", name, "--launch-skip", str(skip), "--launch-count", "6", "-f", "-o", rep,
+    cmd = ["ncu", "--set", "full", "--clock-control", "none", "--import-source", "on", "--kernel-name-base", "function",
+           "--kernel-name", name, "--launch-skip", str(skip), "--launch-count", str(count), "-f", "-o", rep,
            sys.executable, os.path.join(ROOT, "bench.py"), "--config", cfg, "--steps", "3", "--warmup", "3",
            "--no-cpu-baseline"]
     subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL)
