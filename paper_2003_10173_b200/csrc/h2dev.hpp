@@ -85,6 +85,8 @@ struct HgemvGraph {
     // few-vector path: the dense near-field block pass runs on `lo` (least
     // priority) beside the sweep chain on `hi` (greatest priority)
     cudaStream_t hi = nullptr, lo = nullptr;
+    int greatest = 0;     // numeric value of the greatest stream priority
+    int prio_mode = 0;    // last hgemv_impl: 1 few-vector overlap, 2 top chain (graph node priorities)
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ~HgemvGraph() {
         if (exec) cudaGraphExecDestroy(exec);

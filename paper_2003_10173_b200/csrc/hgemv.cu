@@ -798,6 +798,8 @@ struct LaunchDesc {
     int stage = 0;            // 1 leaf up, 2 transfer up, 3 coupling, 4 downsweep, 5 leaf+dense
     int phase = 0;            // sharded hgemv: 0 before the exchange, 1 after, 2 local-source near field
     bool side = false;        // split near field (5d): may run on the side stream beside the sweeps
+    bool chain = false;       // top-of-tree chain (upsweep / coupling / downsweep above split_level): runs on
+                              // the greatest-priority side stream beside the deep coupling
     bool yadd = false;        // leaf expansion (5u): adds the split near-field partial sums
     // 0 segmented GEMM; symmetric few-vector path: 1 block pass over couplings,
     // 2 slot sums into y-hat, 3 block pass over dense blocks, 4 slot sums into y
@@ -828,6 +830,8 @@ struct HgemvPlan {
     // stage 5 split: the near field (5d) writes blocked partial sums to the
     // workspace's ypart, the leaf expansion (5u) adds them in its epilogue
     bool split = false;
+    int chain_level = 0;      // > 0: levels above it form the top chain (LaunchDesc::chain)
+    int chain_nodes = 0;      // g_chain_nodes the plan was built with
     std::once_flag accounted;
     DeviceArray<SegTask> tasks;
     DeviceArray<SegEntry> entries;
@@ -854,6 +858,14 @@ struct HgemvPlan {
 
 namespace {
 
+// general plans on one GPU: the tree levels with fewer than this many nodes
+// (the latency-bound top of both sweeps) run with the top couplings as one chain
+// on the greatest-priority side stream while the deep coupling (the bulk of
+// stage 3) runs on the caller's stream (h2b_tune 12; 0 = off; plans rebuild lazily)
+int g_chain_nodes = 4096;
+// priority attribute of the segmented-GEMM launches issued by this thread (0 = the stream's)
+thread_local int t_launch_priority = 0;
+
 struct PlanBuilder {
     std::vector<SegTask> tasks;
     std::vector<SegEntry> entries;
@@ -868,10 +880,12 @@ struct PlanBuilder {
     };
 
     int phase = 0;
+    bool chain = false;
     void emit(const std::vector<Pending>& outs, const std::vector<SegEntry>& pool, int mode, int out, int stage,
               bool zero_yhat = false) {
         LaunchDesc ld;
         ld.phase = phase;
+        ld.chain = chain;
         ld.stage = stage;
         ld.mode = mode;
         ld.out = out;
@@ -1026,6 +1040,17 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         tpart = t;
     };
     g_plan_part_ms[3] += 1;
+    // top chain (see g_chain_nodes): needs every coupling to pair nodes of one level
+    int chain_level = 0;
+    if (!small && !ds && g_chain_nodes > 0) {
+        int l = 0;
+        while (l <= ct.depth && int(ct.levels[size_t(l)].size()) < g_chain_nodes) ++l;
+        bool same = true;
+        for (int b : bt.adm) same = same && ct.level[size_t(bt.row[size_t(b)])] == ct.level[size_t(bt.col[size_t(b)])];
+        if (same && l >= 2 && l < ct.depth) chain_level = l;
+    }
+    plan->chain_level = chain_level;
+    plan->chain_nodes = g_chain_nodes;
     std::vector<P> outs;
     std::vector<SegEntry> pool;
     // stage 1a: leaves  xhat_t = U_t^T X_t
@@ -1046,6 +1071,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         outs.clear();
         pool.clear();
         pb.phase = (ds && l < ds->lp) ? 1 : 0;
+        pb.chain = l < chain_level;
         for (int v : ct.levels[size_t(l)]) {
             if (ct.is_leaf(v) || !local(v)) continue;
             const int kv = up.rank[size_t(v)];
@@ -1058,6 +1084,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         }
         pb.emit(outs, pool, kModeSet, 1, 2);
     }
+    pb.chain = false;
     // symmetric few-vector path: block passes (kinds 1, 3) + slot sums (kinds 2, 4)
     std::vector<SymBlock> sblocks;
     std::vector<CsrUnit> sunits;
@@ -1164,21 +1191,29 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         }
         for (int v = 0; v < nn; ++v)
             order_entries(by_target.pool, by_target.start[size_t(v)], by_target.start[size_t(v) + 1], 1, cu[size_t(v)]);
-        outs.clear();
         pb.phase = 1;
-        for (int v = 0; v < nn; ++v) {
-            // every local node with a rank gets a task (nodes without couplings write
-            // zeros), so y-hat needs no memset before the downsweep accumulates
-            if (!local(v) || down.rank[size_t(v)] == 0) continue;
-            const int k = down.rank[size_t(v)];
-            outs.push_back(P{k, k, cd[size_t(v)], by_target.start[size_t(v)], by_target.start[size_t(v) + 1]});
+        // with a top chain: first the deep targets (caller's stream), then the top ones (chain)
+        for (int pass = 0; pass < (chain_level > 0 ? 2 : 1); ++pass) {
+            outs.clear();
+            for (int v = 0; v < nn; ++v) {
+                // every local node with a rank gets a task (nodes without couplings write
+                // zeros), so y-hat needs no memset before the downsweep accumulates
+                if (!local(v) || down.rank[size_t(v)] == 0) continue;
+                if (chain_level > 0 && (ct.level[size_t(v)] < chain_level) != (pass == 1)) continue;
+                const int k = down.rank[size_t(v)];
+                outs.push_back(P{k, k, cd[size_t(v)], by_target.start[size_t(v)], by_target.start[size_t(v) + 1]});
+            }
+            pb.chain = pass == 1;
+            pb.emit(outs, by_target.pool, kModeSet, 2, 3);
         }
-        pb.emit(outs, by_target.pool, kModeSet, 2, 3);
+        pb.chain = false;
     }
-    // stage 3: downsweep top-down  yhat_c += E_c yhat_v
+    // stage 3: downsweep top-down  yhat_c += E_c yhat_v (the chain ends with the level
+    // writing chain_level - 1; the level writing chain_level waits for the deep coupling)
     for (int l = 0; l < ct.depth; ++l) {
         outs.clear();
         pool.clear();
+        pb.chain = l + 1 < chain_level;
         for (int v : ct.levels[size_t(l)]) {
             if (ct.is_leaf(v)) continue;
             const int kv = down.rank[size_t(v)];
@@ -1192,6 +1227,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         }
         pb.emit(outs, pool, kModeAdd, 2, 4);
     }
+    pb.chain = false;
     lap(0);
     // U_t E_t for every owned non-root leaf (one batched GEMM at plan time)
     std::vector<int64_t> ue_off(static_cast<size_t>(nn), -1);
@@ -1375,6 +1411,7 @@ void ensure_side_streams(HgemvGraph& g) {
     if (g.hi) return;
     int least = 0, greatest = 0;
     H2B_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    g.greatest = greatest;
     H2B_CUDA(cudaStreamCreateWithPriority(&g.hi, cudaStreamNonBlocking, greatest));
     H2B_CUDA(cudaStreamCreateWithPriority(&g.lo, cudaStreamNonBlocking, least));
     for (cudaEvent_t& e : g.ev) H2B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1385,7 +1422,7 @@ std::shared_ptr<HgemvPlan> get_plan(const H2Dev& h, bool transpose) {
     if (h.symmetric) transpose = false;   // op(H) = H: one plan serves both
     auto& p = h.plan[transpose ? 1 : 0];
     const bool split = g_dense_split != 0;
-    if (!p || p->split != split) {
+    if (!p || p->split != split || p->chain_nodes != g_chain_nodes) {
         const auto t0 = std::chrono::steady_clock::now();
         p = build_plan(h, transpose, nullptr, false, split);
         g_plan_build_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1424,17 +1461,24 @@ void launch_one(const SegArgs& a, int ntasks, int64_t b, cudaStream_t s) {
     }();
     (void)attr;
     dim3 grid(unsigned(ntasks), unsigned((b + NB - 1) / NB));
-    if (g_pdl) {   // overlap this launch's prologue with the previous kernel's tail
+    if (g_pdl || t_launch_priority) {   // PDL: overlap this launch's prologue with the previous kernel's tail
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(WM * WN * 32);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchAttribute at[2];
+        int na = 0;
+        if (g_pdl) {
+            at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[na++].val.programmaticStreamSerializationAllowed = 1;
+        }
+        if (t_launch_priority) {   // carried into a captured graph's kernel node
+            at[na].id = cudaLaunchAttributePriority;
+            at[na++].val.priority = t_launch_priority;
+        }
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = unsigned(na);
         H2B_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     } else {
         kern<<<grid, WM * WN * 32, smem, s>>>(a);
@@ -1667,8 +1711,10 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     }
     H2B_CUDA(cudaStreamEndCapture(g.cap, &graph));
     unsigned long long iflags = 0;
-    if (g.hi) {   // keep the overlapped few-vector path's priorities inside the graph
+    if (g.prio_mode == 1) {   // keep the overlapped few-vector path's priorities inside the graph
         set_node_priorities(graph);
+        iflags = cudaGraphInstantiateFlagUseNodePriority;
+    } else if (g.prio_mode == 2) {   // top chain: its launches carry their priority attribute
         iflags = cudaGraphInstantiateFlagUseNodePriority;
     }
     H2B_CUDA(cudaGraphInstantiateWithFlags(&g.exec, graph, iflags));
@@ -1754,6 +1800,7 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
     const cudaStream_t user_stream = stream;
     const bool overlap = g_dense_overlap && (plan->sym64 || plan->split) && phases == 7 && !timer &&
                          plan->num_leaves > 0;
+    sg.prio_mode = overlap ? 1 : 0;
     if (overlap) {
         ensure_side_streams(sg);
         H2B_CUDA(cudaEventRecord(sg.ev[0], user_stream));
@@ -1774,8 +1821,23 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         H2B_CUDA(cudaEventRecord(sg.ev[1], stream));
         H2B_CUDA(cudaStreamWaitEvent(sg.lo, sg.ev[1], 0));
     }
+    // general plan with a top chain: fork it onto the greatest-priority stream at its
+    // first launch, join before the first launch that needs it (downsweep below it / stage 5)
+    const bool chain_ok = plan->chain_level > 0 && phases == 7 && !timer && !overlap;
+    bool forked = false;
     for (const LaunchDesc& ld : plan->launches) {
         if (!(phases & (1 << ld.phase))) continue;
+        if (chain_ok && ld.chain && !forked) {
+            ensure_side_streams(sg);
+            sg.prio_mode = 2;
+            H2B_CUDA(cudaEventRecord(sg.ev[0], stream));
+            H2B_CUDA(cudaStreamWaitEvent(sg.hi, sg.ev[0], 0));
+            forked = true;
+        } else if (forked && !ld.chain && ld.stage >= 4) {
+            H2B_CUDA(cudaEventRecord(sg.ev[1], sg.hi));
+            H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[1], 0));
+            forked = false;
+        }
         if (ld.kind != 0) {
             const int nitems = ld.item_end - ld.item_begin;
             if (nitems == 0) continue;
@@ -1820,7 +1882,11 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         if (ntasks == 0) continue;
         // split stage 5: the near field (5d) on the least-priority side stream once x is
         // gathered; the leaf expansion (5u) waits for it
-        const cudaStream_t ls = (overlap && ld.side) ? sg.lo : stream;
+        const cudaStream_t ls = (overlap && ld.side) ? sg.lo : ((forked && ld.chain) ? sg.hi : stream);
+        struct PrioScope {   // chain launches carry the greatest priority (also inside a captured graph)
+            explicit PrioScope(int p) { t_launch_priority = p; }
+            ~PrioScope() { t_launch_priority = 0; }
+        } prio(forked && ld.chain ? sg.greatest : 0);
         if (overlap && ld.yadd) {
             H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
             H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[2], 0));
@@ -1850,6 +1916,10 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
         NvtxRange nvs(kStageName[ld.stage >= 0 && ld.stage < 6 ? ld.stage : 0]);
         dispatch(a, ntasks, b, ld.mt, vec, ld.mode, ls);
         if (timer) timer->mark(stream);
+    }
+    if (forked) {
+        H2B_CUDA(cudaEventRecord(sg.ev[1], sg.hi));
+        H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[1], 0));
     }
     if (overlap) {   // join both side streams back into the caller's stream
         H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
@@ -2109,6 +2179,10 @@ extern "C" int h2b_tune(int which, int value) {
     }
     if (which == 10) {   // few-vector dense block pass: bulk-async ring (1) / register streaming (0)
         h2b::g_sym_tma = value;
+        return 0;
+    }
+    if (which == 12) {   // general plans: top-chain node threshold (0 = off); plans rebuild lazily
+        h2b::g_chain_nodes = value;
         return 0;
     }
     if (which == 9) {   // stage-5 split (near field beside the sweeps) on (1) / off (0); plans rebuild lazily

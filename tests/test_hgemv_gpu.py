@@ -330,3 +330,31 @@ def test_split_near_field_matches(cuda, b):
     for o in outs:
         assert rel(o, expect) <= TOL
     assert np.array_equal(outs[1], outs[2])   # deterministic with the side stream
+
+
+@pytest.mark.parametrize("sym,b,transpose", [(True, 3, False), (True, 32, False), (False, 32, True), (False, 1, False)])
+def test_top_chain_matches(cuda, sym, b, transpose):
+    """General plans with a top chain (h2b_tune 12: the levels with fewer nodes than the
+    threshold run with their couplings on a side stream beside the deep coupling) are
+    bitwise the single-stream plan, eagerly and through the captured graph."""
+    import torch
+    from paper_2003_10173_b200._lib import lib
+    pts = O.grid2d(64, 64)
+    ora, m, _ = pair(pts, 32, False, sym, 12, seed=21)
+    n = pts.shape[0]
+    x = O.gaussian(97, n, b)
+    xt = torch.from_numpy(x.T.copy()).to(cuda).t()
+    outs = []
+    try:
+        for knob in (0, 8, 8, 8, 8):   # eager, eager, captured, replayed
+            lib.h2b_tune(12, knob)
+            yt = torch.zeros(b, n, dtype=torch.float64, device=cuda).t()
+            m.hgemv(xt, yt, transpose=transpose)
+            torch.cuda.synchronize()
+            outs.append(yt.cpu().numpy().copy())
+    finally:
+        lib.h2b_tune(12, 4096)
+    expect = ora.matvec(x, transpose=transpose)
+    assert rel(outs[0], expect) <= TOL
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
