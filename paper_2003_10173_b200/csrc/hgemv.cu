@@ -9,6 +9,7 @@
 #include <map>
 #include <mutex>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_set>
 
@@ -1381,22 +1382,48 @@ int g_small_b = 2;            // symmetric few-vector path for b <= this (0 = of
 // gathered x) on a least-priority stream concurrently with the latency-bound
 // sweep chain on a greatest-priority stream (0 = one stream)
 int g_dense_overlap = 1;
-// few-vector dense block pass staged by bulk-async copies (h2b_tune 10): 1 on, 0 the register-streaming kernel
+// few-vector dense block pass staged by bulk-async copies (h2b_tune 10): the ring depth
+// in 32 KB stages (1 = the default kSymStages), 0 the register-streaming kernel
 int g_sym_tma = 1;
 constexpr int kSymStages = 6;
-constexpr int kSymSmem = kSymStages * 4096 * 8;
 int num_sms() {
     static const int n = [] {
         int dev = 0, v = 0;
         H2B_CUDA(cudaGetDevice(&dev));
         H2B_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-        H2B_CUDA(cudaFuncSetAttribute(sym_tma64_kernel<1, kSymStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSymSmem));
-        H2B_CUDA(cudaFuncSetAttribute(sym_tma64_kernel<2, kSymStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSymSmem));
         return v;
     }();
     return n;
+}
+template <int B, int NSTAGE>
+void launch_sym_tma(const SymBlock* sb, int nitems, const double* src, double* scratch, int64_t b, cudaStream_t s) {
+    constexpr int smem = NSTAGE * 4096 * 8;
+    static const bool attr = [] {
+        H2B_CUDA(cudaFuncSetAttribute(sym_tma64_kernel<B, NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        return true;
+    }();
+    (void)attr;
+    const unsigned tg = unsigned(std::min(nitems, num_sms()));
+    sym_tma64_kernel<B, NSTAGE><<<tg, (NSTAGE + 1) * 32, smem, s>>>(sb, nitems, src, scratch, b);
+}
+template <int B>
+void launch_sym_tma_depth(int depth, const SymBlock* sb, int nitems, const double* src, double* scratch, int64_t b,
+                          cudaStream_t s) {
+    switch (depth) {
+        case 2: launch_sym_tma<B, 2>(sb, nitems, src, scratch, b, s); break;
+        case 3: launch_sym_tma<B, 3>(sb, nitems, src, scratch, b, s); break;
+        case 4: launch_sym_tma<B, 4>(sb, nitems, src, scratch, b, s); break;
+        default: launch_sym_tma<B, kSymStages>(sb, nitems, src, scratch, b, s); break;
+    }
+}
+bool is_sym_tma(const void* f) {
+    for (const void* k : {reinterpret_cast<const void*>(sym_tma64_kernel<1, 2>), reinterpret_cast<const void*>(sym_tma64_kernel<2, 2>),
+                          reinterpret_cast<const void*>(sym_tma64_kernel<1, 3>), reinterpret_cast<const void*>(sym_tma64_kernel<2, 3>),
+                          reinterpret_cast<const void*>(sym_tma64_kernel<1, 4>), reinterpret_cast<const void*>(sym_tma64_kernel<2, 4>),
+                          reinterpret_cast<const void*>(sym_tma64_kernel<1, kSymStages>),
+                          reinterpret_cast<const void*>(sym_tma64_kernel<2, kSymStages>)})
+        if (f == k) return true;
+    return false;
 }
 // stage-5 split on one GPU (h2b_tune 9): the near field runs on the side
 // stream beside the sweeps and the leaf expansion adds its partial sums. Off by
@@ -1620,8 +1647,7 @@ void set_node_priorities(cudaGraph_t graph) {
     H2B_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
     const void* lo1 = reinterpret_cast<const void*>(sym_pass64_kernel<1>);
     const void* lo2 = reinterpret_cast<const void*>(sym_pass64_kernel<2>);
-    const void* lo3 = reinterpret_cast<const void*>(sym_tma64_kernel<1, kSymStages>);
-    const void* lo4 = reinterpret_cast<const void*>(sym_tma64_kernel<2, kSymStages>);
+
     for (cudaGraphNode_t nd : nodes) {
         cudaGraphNodeType ty;
         H2B_CUDA(cudaGraphNodeGetType(nd, &ty));
@@ -1629,7 +1655,7 @@ void set_node_priorities(cudaGraph_t graph) {
         cudaKernelNodeParams kp{};
         H2B_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
         cudaLaunchAttributeValue v{};
-        v.priority = (kp.func == lo1 || kp.func == lo2 || kp.func == lo3 || kp.func == lo4) ? least : greatest;
+        v.priority = (kp.func == lo1 || kp.func == lo2 || is_sym_tma(kp.func)) ? least : greatest;
         H2B_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
     }
 }
@@ -1855,9 +1881,8 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                 // bulk-async staged variant (one persistent CTA per SM) when there are enough blocks to
                 // keep every SM's ring full (measured: cfg2 b=1 1.90 -> 1.84 ms; slower on cfg1's 2.5k blocks)
                 if (g_sym_tma > 0 && nitems >= 32 * num_sms()) {
-                    const unsigned tg = unsigned(std::min(nitems, num_sms()));
-                    if (b == 1) sym_tma64_kernel<1, kSymStages><<<tg, (kSymStages + 1) * 32, kSymSmem, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
-                    else sym_tma64_kernel<2, kSymStages><<<tg, (kSymStages + 1) * 32, kSymSmem, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
+                    if (b == 1) launch_sym_tma_depth<1>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ds);
+                    else launch_sym_tma_depth<2>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ds);
                 } else if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
                 else sym_pass64_kernel<2><<<grid, 256, 0, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
             } else if (ld.kind == 1 || ld.kind == 3) {

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--lib", default="libh2b200")
     ap.add_argument("--local", default=os.path.join(ROOT, "paper_2003_10173_b200", "lib", "libh2b200.so"))
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--callers", default=None, help="also list the nearest --lib callers of frames matching this")
     a = ap.parse_args()
     samples = [line.split() for line in open(a.file) if line.strip()]
     offs = set()
@@ -60,6 +61,18 @@ def main():
     print("== inclusive")
     for k, v in incl.most_common(a.top):
         print(f"{v:7d} {100.0 * v / n:5.1f}%  {k}")
+    if a.callers:
+        cal = collections.Counter()
+        for s in samples:
+            labs = [label(fr) for fr in s]
+            hit = [i for i, lab in enumerate(labs) if a.callers in lab]
+            if not hit:
+                continue
+            chain = [lab for lab in labs[hit[0] + 1:] if not lab.startswith("[") and "libcudart" not in lab][:3]
+            cal[" <- ".join(c[:60] for c in chain)] += 1
+        print(f"== callers of {a.callers}")
+        for k, v in cal.most_common(a.top):
+            print(f"{v:7d}  {k}")
 
 
 if __name__ == "__main__":
