@@ -20,8 +20,12 @@ python bench.py --config cfg1build --steps 3 --warmup 1 --hara-rng reference > $
 python bench.py --config cfg3 --steps 3 --warmup 1 > $O/bench_cfg3.json 2> $O/bench_cfg3.err
 python bench.py --config cfg3 --steps 1 --warmup 1 --hara-rng reference --no-cpu-baseline > $O/bench_cfg3_refrng.json 2> $O/bench_cfg3_refrng.err
 python bench.py --config cfg5 --steps 2 --warmup 1 > $O/bench_cfg5.json 2> $O/bench_cfg5.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg2.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# launch list of one replayed cfg2 hgemv (the 5th call: calls 1-2 eager, 3 captured, 4-5 replayed);
+# only the hgemv kernels match the filter, so the setup (tree, matrix generation) is skipped
+NL=$(python tools/run_hgemv.py cfg2 32 1 2>/dev/null | sed -n 's/launches per hgemv: //p')
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base function \
+  --kernel-name regex:"seg_gemm|gather_blocked|sym_|csr_sum" --launch-skip $((4 * NL)) --launch-count $NL \
+  --csv --log-file $O/launches_cfg2.csv python tools/run_hgemv.py cfg2 32 5 > /dev/null 2>&1
 for k in qr_kernel jacobi_kernel bgemm_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base function --kernel-name regex:$k \
     --launch-skip 200 --launch-count 1 -f -o $O/hara_$k python tools/hara_launches.py cfg1build 1 > /dev/null 2>&1
