@@ -7,13 +7,11 @@ from paper_2003_10173_b200._lib import lib, check
 import bench
 cfg = bench.CONFIGS[sys.argv[1]]
 b = int(sys.argv[2])
-fuse = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 pts = bench.grid_points(cfg["grid"]); n = pts.shape[0]
 ct = build_cluster_tree(pts, cfg["leaf"], device=True); bt = build_block_tree(ct, ct, 1.0)
 m = H2Matrix.kernel(bt, pts, cfg["kind"], cfg["ell"], cfg["rank"])
 X = torch.randn(b, n, dtype=torch.float64, device="cuda"); Y = torch.empty_like(X)
 s = torch.cuda.current_stream().cuda_stream
-lib.h2b_tune(11, fuse)
 cnt = C.c_int(); st = np.zeros(512, np.int32); ms = np.zeros(512); fl = np.zeros(512); by = np.zeros(512)
 best = None
 for rep in range(6):
@@ -21,6 +19,6 @@ for rep in range(6):
           st.ctypes.data_as(C.c_void_p), ms.ctypes.data_as(C.c_void_p), fl.ctypes.data_as(C.c_void_p), by.ctypes.data_as(C.c_void_p)))
     cur = ms[:cnt.value].copy()
     best = cur if best is None else np.minimum(best, cur)
-print(f"{sys.argv[1]} b={b} fuse={fuse}: {cnt.value} launches, sum {best.sum():.4f} ms")
+print(f"{sys.argv[1]} b={b}: {cnt.value} launches, sum {best.sum():.4f} ms")
 for i in range(cnt.value):
     print(f"  {i:3d} stage {st[i]}  {best[i]*1e3:8.1f} us  {fl[i]*b/1e6:9.2f} MF  {by[i]/1e6:8.2f} MB")
