@@ -103,6 +103,7 @@ struct Workspace {
     DeviceArray<double> scratch;   // per-block products of the symmetric few-vector path
     DeviceArray<double> ypart;     // split stage 5: near-field partial sums (internal blocked order)
     DeviceArray<double> hx, hy;   // staging of the host-buffer entry point
+    DeviceArray<unsigned> work;    // work counter of the persistent few-vector dense pass
     HgemvGraph graph;
 };
 

@@ -364,6 +364,7 @@ template <int B>
 __global__ void __launch_bounds__(256) sym_pass_kernel(const SymBlock* __restrict__ blocks, int nblocks,
                                                        const double* __restrict__ src, double* __restrict__ scratch,
                                                        int64_t b) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // PDL: inputs come from the previous launch
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (wid >= nblocks) return;
     const SymBlock d = blocks[wid];
@@ -443,6 +444,7 @@ template <int B>
 __global__ void __launch_bounds__(256) sym_pass32_kernel(const SymBlock* __restrict__ blocks, int nblocks,
                                                          const double* __restrict__ src,
                                                          double* __restrict__ scratch, int64_t b) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // PDL: inputs come from the previous launch
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (wid >= nblocks) return;
     const SymBlock d = blocks[wid];
@@ -534,6 +536,7 @@ template <int B>
 __global__ void __launch_bounds__(256) sym_pass64_kernel(const SymBlock* __restrict__ blocks, int nblocks,
                                                          const double* __restrict__ src,
                                                          double* __restrict__ scratch, int64_t b) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // PDL: inputs come from the previous launch
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (wid >= nblocks) return;
     const SymBlock d = blocks[wid];
@@ -622,42 +625,92 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  : "memory");
 }
 
+template <int B>
+struct SymTmaStage {   // doubles per ring stage: the block (64 x 64) + x_t and x_s (64 x B each)
+    static constexpr int kDoubles = 4096 + 2 * 64 * B;
+};
+
 template <int B, int NSTAGE>
 __global__ void __launch_bounds__((NSTAGE + 1) * 32, 1) sym_tma64_kernel(const SymBlock* __restrict__ blocks,
                                                                          int nblocks, const double* __restrict__ src,
-                                                                         double* __restrict__ scratch, int64_t b) {
-    extern __shared__ __align__(128) double ring[];   // NSTAGE x 64 x 64
+                                                                         double* __restrict__ scratch, int64_t b,
+                                                                         unsigned* __restrict__ work) {
+    constexpr int SD = SymTmaStage<B>::kDoubles;
+    extern __shared__ __align__(128) double ring[];   // NSTAGE x SD
     __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+    __shared__ SymBlock meta[NSTAGE];   // the block in each stage (A == nullptr: no more work)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; ++i) {
-            mbar_init(&full[i], 1);
+            mbar_init(&full[i], 33);   // 32 lanes' cp.async (x_t, x_s) + the bulk-copy arrive
             mbar_init(&empty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    if (warp == NSTAGE) {   // producer
-        if (lane == 0) {
-            int g = 0;
-            for (int blk = blockIdx.x; blk < nblocks; blk += gridDim.x, ++g) {
+    if (warp == NSTAGE) {
+        // producer warp: blocks are taken from a global counter kGrab at a time (so CTAs
+        // that start late, their SMs still busy with the sweep chain, simply take fewer);
+        // the next grab and its descriptors are in flight while the current one is issued.
+        // Per block: one bulk copy of the block (mbarrier transaction count) and the
+        // block's x_t / x_s rows by cp.async from all lanes (noinc arrivals), so the
+        // consumers never wait on global memory
+        constexpr int kGrab = 8;
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(work, unsigned(kGrab));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        SymBlock d{};
+        if (lane < kGrab && base + lane < unsigned(nblocks)) d = blocks[base + lane];
+        int g = 0;
+        while (base < unsigned(nblocks)) {
+            unsigned nbase = 0;
+            if (lane == 0) nbase = atomicAdd(work, unsigned(kGrab));
+            nbase = __shfl_sync(0xffffffffu, nbase, 0);
+            SymBlock nd{};
+            if (lane < kGrab && nbase + lane < unsigned(nblocks)) nd = blocks[nbase + lane];
+            const int cnt = int(min(unsigned(kGrab), unsigned(nblocks) - base));
+            for (int i = 0; i < cnt; ++i, ++g) {
                 const int st = g % NSTAGE;
-                if (g >= NSTAGE) mbar_wait(&empty[st], ((g / NSTAGE) - 1) & 1);
-                const SymBlock d = blocks[blk];
-                const unsigned bytes = unsigned(d.R) * unsigned(d.C) * 8u;
-                mbar_expect_tx(&full[st], bytes);
-                bulk_g2s(ring + st * 4096, d.A, bytes, &full[st]);
+                if (lane == 0 && g >= NSTAGE) mbar_wait(&empty[st], ((g / NSTAGE) - 1) & 1);
+                __syncwarp();
+                const int R = __shfl_sync(0xffffffffu, d.R, i), C = __shfl_sync(0xffffffffu, d.C, i);
+                const long long xt_u = __shfl_sync(0xffffffffu, (long long)d.xt_unit, i);
+                const long long xs_u = __shfl_sync(0xffffffffu, (long long)d.xs_unit, i);
+                double* sx = ring + st * SD + 4096;
+                const double* gxt = src + xt_u * b;
+                const double* gxs = src + xs_u * b;
+                for (int e = lane; e < R * B; e += 32) cp_async8(sx + e, gxt + e, 8);
+                for (int e = lane; e < C * B; e += 32) cp_async8(sx + 64 * B + e, gxs + e, 8);
+                cp_async_mbar_arrive(&full[st]);
+                if (lane == i) {
+                    meta[st] = d;
+                    const unsigned bytes = unsigned(R) * unsigned(C) * 8u;
+                    mbar_expect_tx(&full[st], bytes);   // arrive (release: meta[st] visible with the stage)
+                    bulk_g2s(ring + st * SD, d.A, bytes, &full[st]);
+                }
+                __syncwarp();
             }
+            base = nbase;
+            d = nd;
+        }
+        for (int e = 0; e < NSTAGE; ++e, ++g) {   // end marker in the next NSTAGE stages
+            const int se = g % NSTAGE;
+            if (lane == 0 && g >= NSTAGE) mbar_wait(&empty[se], ((g / NSTAGE) - 1) & 1);
+            __syncwarp();
+            if (lane == 0) meta[se].A = nullptr;
+            mbar_arrive(&full[se]);   // 32 arrivals ...
+            if (lane == 0) mbar_arrive(&full[se]);   // ... + 1
         }
         return;
     }
-    int g = warp;
-    for (int blk = blockIdx.x + warp * gridDim.x; blk < nblocks; blk += NSTAGE * gridDim.x, g += NSTAGE) {
+    for (int g = warp;; g += NSTAGE) {
         const int st = warp;   // == g % NSTAGE
-        const SymBlock d = blocks[blk];
+        mbar_wait(&full[st], (g / NSTAGE) & 1);
+        const SymBlock d = meta[st];
+        if (d.A == nullptr) break;
         const int R = d.R, C = d.C;
-        const double* xs = src + d.xs_unit * b;
-        const double* xt = src + d.xt_unit * b;
+        const double* xt = ring + st * SD + 4096;
+        const double* xs = xt + 64 * B;
         const int rr = lane * 2;
         const bool vr = rr < R;
         double xa[B], xb[B], ua[B], ub[B];
@@ -669,8 +722,7 @@ __global__ void __launch_bounds__((NSTAGE + 1) * 32, 1) sym_tma64_kernel(const S
         }
         const bool want_w = d.w_off >= 0;
         double* w = want_w ? scratch + d.w_off * b : nullptr;
-        const double* A = ring + st * 4096;
-        mbar_wait(&full[st], (g / NSTAGE) & 1);
+        const double* A = ring + st * SD;
 #pragma unroll 2
         for (int j0 = 0; j0 < C; j0 += 8) {
             double p[8][B];
@@ -682,7 +734,7 @@ __global__ void __launch_bounds__((NSTAGE + 1) * 32, 1) sym_tma64_kernel(const S
                 if (vr && vj) a = *reinterpret_cast<const double2*>(A + j * R + rr);
 #pragma unroll
                 for (int q = 0; q < B; ++q) {
-                    const double xj = vj ? __ldg(xs + j + q * C) : 0.0;
+                    const double xj = vj ? xs[j + q * C] : 0.0;
                     ua[q] = fma(a.x, xj, ua[q]);
                     ub[q] = fma(a.y, xj, ub[q]);
                     p[jj][q] = fma(a.x, xa[q], a.y * xb[q]);
@@ -732,6 +784,7 @@ __global__ void __launch_bounds__(256) csr_sum_kernel(const CsrUnit* __restrict_
                                                       const double* __restrict__ scratch, int64_t b, int mode,
                                                       double* __restrict__ out, const int* __restrict__ perm,
                                                       int64_t ldy, double alpha) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // PDL: inputs come from the previous launch
     const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (wid >= nunits) return;
     const CsrUnit u = units[wid];
@@ -1395,25 +1448,44 @@ int num_sms() {
     }();
     return n;
 }
+int g_pdl_small = 1;   // h2b_tune 13: PDL for the few-vector block-pass / slot-sum launches
+// launch with programmatic dependent launch when enabled (the kernel waits with
+// griddepcontrol.wait before reading what the previous launch wrote)
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (g_pdl && g_pdl_small) ? 1 : 0;
+    H2B_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 template <int B, int NSTAGE>
-void launch_sym_tma(const SymBlock* sb, int nitems, const double* src, double* scratch, int64_t b, cudaStream_t s) {
-    constexpr int smem = NSTAGE * 4096 * 8;
+void launch_sym_tma(const SymBlock* sb, int nitems, const double* src, double* scratch, int64_t b, unsigned* work,
+                    cudaStream_t s) {
+    constexpr int smem = NSTAGE * SymTmaStage<B>::kDoubles * 8;
     static const bool attr = [] {
         H2B_CUDA(cudaFuncSetAttribute(sym_tma64_kernel<B, NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         return true;
     }();
     (void)attr;
     const unsigned tg = unsigned(std::min(nitems, num_sms()));
-    sym_tma64_kernel<B, NSTAGE><<<tg, (NSTAGE + 1) * 32, smem, s>>>(sb, nitems, src, scratch, b);
+    H2B_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned), s));
+    sym_tma64_kernel<B, NSTAGE><<<tg, (NSTAGE + 1) * 32, smem, s>>>(sb, nitems, src, scratch, b, work);
 }
 template <int B>
 void launch_sym_tma_depth(int depth, const SymBlock* sb, int nitems, const double* src, double* scratch, int64_t b,
-                          cudaStream_t s) {
+                          unsigned* work, cudaStream_t s) {
     switch (depth) {
-        case 2: launch_sym_tma<B, 2>(sb, nitems, src, scratch, b, s); break;
-        case 3: launch_sym_tma<B, 3>(sb, nitems, src, scratch, b, s); break;
-        case 4: launch_sym_tma<B, 4>(sb, nitems, src, scratch, b, s); break;
-        default: launch_sym_tma<B, kSymStages>(sb, nitems, src, scratch, b, s); break;
+        case 2: launch_sym_tma<B, 2>(sb, nitems, src, scratch, b, work, s); break;
+        case 3: launch_sym_tma<B, 3>(sb, nitems, src, scratch, b, work, s); break;
+        case 4: launch_sym_tma<B, 4>(sb, nitems, src, scratch, b, work, s); break;
+        default: launch_sym_tma<B, kSymStages>(sb, nitems, src, scratch, b, work, s); break;
     }
 }
 bool is_sym_tma(const void* f) {
@@ -1672,12 +1744,14 @@ void reserve_workspace(const HgemvPlan& plan, int64_t n, int64_t b, cudaStream_t
     if (plan.scratch_rows > 0 && ws.scratch.size() < size_t(plan.scratch_rows * b))
         ws.scratch.resize(size_t(plan.scratch_rows * b), stream);
     if (plan.split && ws.ypart.size() < need_x) ws.ypart.resize(need_x, stream);
+    if (ws.work.size() < 1) ws.work.resize(1, stream);
 }
 // the runtime knobs that change the launch sequence of an hgemv
 uint64_t knob_signature() {
     uint64_t s = uint64_t(g_pdl & 0xff) | uint64_t(g_dense_overlap & 0xff) << 8 | uint64_t(g_dense_split & 0xff) << 48 |
                  uint64_t(g_sym_tma & 0xff) << 56;
     for (int i = 0; i < 4; ++i) s |= uint64_t(g_tune[i] & 0xff) << (16 + 8 * i);
+    s ^= uint64_t(g_pdl_small & 1) << 47;
     return s;
 }
 }  // namespace
@@ -1873,30 +1947,35 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
             }
             const unsigned grid = unsigned((nitems + 7) / 8);
             if (ld.kind == 1 && plan->sym32) {
-                if (b == 1) sym_pass32_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
-                else sym_pass32_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, ws.xhat.data(), ws.scratch.data(), b);
+                launch_pdl(b == 1 ? sym_pass32_kernel<1> : sym_pass32_kernel<2>, grid, 256, stream,
+                           static_cast<const SymBlock*>(plan->sym_blocks.data() + ld.item_begin), nitems,
+                           static_cast<const double*>(ws.xhat.data()), ws.scratch.data(), b);
             } else if (ld.kind == 3 && plan->sym64) {
                 const cudaStream_t ds = overlap ? sg.lo : stream;
                 const SymBlock* sb = plan->sym_blocks.data() + ld.item_begin;
                 // bulk-async staged variant (one persistent CTA per SM) when there are enough blocks to
                 // keep every SM's ring full (measured: cfg2 b=1 1.90 -> 1.84 ms; slower on cfg1's 2.5k blocks)
                 if (g_sym_tma > 0 && nitems >= 32 * num_sms()) {
-                    if (b == 1) launch_sym_tma_depth<1>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ds);
-                    else launch_sym_tma_depth<2>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ds);
-                } else if (b == 1) sym_pass64_kernel<1><<<grid, 256, 0, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
-                else sym_pass64_kernel<2><<<grid, 256, 0, ds>>>(sb, nitems, ws.xint.data(), ws.scratch.data(), b);
+                    if (b == 1) launch_sym_tma_depth<1>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ws.work.data(), ds);
+                    else launch_sym_tma_depth<2>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ws.work.data(), ds);
+                } else {
+                    launch_pdl(b == 1 ? sym_pass64_kernel<1> : sym_pass64_kernel<2>, grid, 256, ds, sb, nitems,
+                               static_cast<const double*>(ws.xint.data()), ws.scratch.data(), b);
+                }
             } else if (ld.kind == 1 || ld.kind == 3) {
                 const double* src = ld.kind == 1 ? ws.xhat.data() : ws.xint.data();
-                if (b == 1) sym_pass_kernel<1><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
-                else sym_pass_kernel<2><<<grid, 256, 0, stream>>>(plan->sym_blocks.data() + ld.item_begin, nitems, src, ws.scratch.data(), b);
+                launch_pdl(b == 1 ? sym_pass_kernel<1> : sym_pass_kernel<2>, grid, 256, stream,
+                           static_cast<const SymBlock*>(plan->sym_blocks.data() + ld.item_begin), nitems, src,
+                           ws.scratch.data(), b);
             } else {
                 if (overlap && ld.kind == 4) {   // dense slot sums wait for the dense pass
                     H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
                     H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[2], 0));
                 }
-                csr_sum_kernel<<<grid, 256, 0, stream>>>(plan->csr_units.data() + ld.item_begin, nitems, plan->csr_slots.data(),
-                                                         ws.scratch.data(), b, ld.kind == 2 ? 0 : 1,
-                                                         ld.kind == 2 ? ws.yhat.data() : y, perm, ldy, alpha);
+                launch_pdl(csr_sum_kernel, grid, 256, stream, static_cast<const CsrUnit*>(plan->csr_units.data() + ld.item_begin),
+                           nitems, static_cast<const int64_t*>(plan->csr_slots.data()),
+                           static_cast<const double*>(ws.scratch.data()), b, ld.kind == 2 ? 0 : 1,
+                           ld.kind == 2 ? ws.yhat.data() : y, perm, ldy, alpha);
             }
             H2B_LAUNCH();
             if (timer) timer->mark(stream);
@@ -2202,8 +2281,12 @@ extern "C" int h2b_tune(int which, int value) {
         h2b::g_dense_overlap = value;
         return 0;
     }
-    if (which == 10) {   // few-vector dense block pass: bulk-async ring (1) / register streaming (0)
+    if (which == 10) {   // few-vector dense block pass: bulk-async ring depth in stages (1 = default 6) / register streaming (0)
         h2b::g_sym_tma = value;
+        return 0;
+    }
+    if (which == 13) {   // PDL for the few-vector block-pass / slot-sum launches
+        h2b::g_pdl_small = value;
         return 0;
     }
     if (which == 12) {   // general plans: top-chain node threshold (0 = off); plans rebuild lazily

@@ -30,4 +30,11 @@ for k in qr_kernel jacobi_kernel bgemm_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base function --kernel-name regex:$k \
     --launch-skip 200 --launch-count 1 -f -o $O/hara_$k python tools/hara_launches.py cfg1build 1 > /dev/null 2>&1
 done
+# keep gpurun_out under the 64 MiB copy-back limit: summarise every ncu report, then drop it
+for r in $O/*.ncu-rep gpurun_out/*.ncu-rep; do
+  [ -f "$r" ] || continue
+  python tools/ncu_summary.py "$r" > "${r%.ncu-rep}_summary.txt" 2>&1
+  rm -f "$r"
+done
+du -sh gpurun_out
 ls -la $O
