@@ -1438,6 +1438,7 @@ int g_dense_overlap = 1;
 // few-vector dense block pass staged by bulk-async copies (h2b_tune 10): the ring depth
 // in 32 KB stages (1 = the default kSymStages), 0 the register-streaming kernel
 int g_sym_tma = 1;
+int g_sym_tma_min = 32;   // h2b_tune 14: bulk-async pass only with at least this many blocks per SM
 constexpr int kSymStages = 6;
 int num_sms() {
     static const int n = [] {
@@ -1752,6 +1753,7 @@ uint64_t knob_signature() {
                  uint64_t(g_sym_tma & 0xff) << 56;
     for (int i = 0; i < 4; ++i) s |= uint64_t(g_tune[i] & 0xff) << (16 + 8 * i);
     s ^= uint64_t(g_pdl_small & 1) << 47;
+    s ^= uint64_t(g_sym_tma_min & 0xff) << 40;
     return s;
 }
 }  // namespace
@@ -1955,7 +1957,7 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                 const SymBlock* sb = plan->sym_blocks.data() + ld.item_begin;
                 // bulk-async staged variant (one persistent CTA per SM) when there are enough blocks to
                 // keep every SM's ring full (measured: cfg2 b=1 1.90 -> 1.84 ms; slower on cfg1's 2.5k blocks)
-                if (g_sym_tma > 0 && nitems >= 32 * num_sms()) {
+                if (g_sym_tma > 0 && nitems >= g_sym_tma_min * num_sms()) {
                     if (b == 1) launch_sym_tma_depth<1>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ws.work.data(), ds);
                     else launch_sym_tma_depth<2>(g_sym_tma, sb, nitems, ws.xint.data(), ws.scratch.data(), b, ws.work.data(), ds);
                 } else {
@@ -2283,6 +2285,10 @@ extern "C" int h2b_tune(int which, int value) {
     }
     if (which == 10) {   // few-vector dense block pass: bulk-async ring depth in stages (1 = default 6) / register streaming (0)
         h2b::g_sym_tma = value;
+        return 0;
+    }
+    if (which == 14) {   // few-vector dense pass: bulk-async ring only from this many blocks per SM
+        h2b::g_sym_tma_min = value;
         return 0;
     }
     if (which == 13) {   // PDL for the few-vector block-pass / slot-sum launches
