@@ -335,7 +335,7 @@ def run_b200(args, cfg, world, rank, local, dist):
     if shard_mode:
         # row-subtree sharding: each rank computes its subtree's rows; one NCCL all-to-all per hgemv
         from paper_2003_10173_b200.dist import ShardedHgemv
-        sharded = ShardedHgemv(m)
+        sharded = ShardedHgemv(m, transport=args.transport, max_b=b)
 
     def step():
         if sharded is not None:
@@ -432,7 +432,7 @@ def run_b200(args, cfg, world, rank, local, dist):
         Yos = [torch.empty_like(Xos[0]) for _ in range(3)]
         # one plan (own workspace and exchange buffers) per rotating stream
         from paper_2003_10173_b200.dist import ShardedHgemv
-        shs = [sharded] + [ShardedHgemv(m) for _ in range(2)]
+        shs = [sharded] + [ShardedHgemv(m, transport=args.transport, max_b=b) for _ in range(2)]
     yps = [torch.empty_like(xp).pin_memory() for _ in range(3)]
     streams = [torch.cuda.Stream(dev) for _ in range(3)]
 
@@ -550,8 +550,10 @@ def hgemv_config(cfg, args, n, b, tree_adm, tree_dense, world, recv_bytes=None):
     return {"workload": cfg["workload"], "n": n, "vectors": b, "rank": cfg["rank"], "leaf": cfg["leaf"],
             "kernel": f"{cfg['kind']} ell={cfg['ell']}", "admissible_leaves": int(tree_adm),
             "dense_leaves": int(tree_dense),
-            "parallelism": (f"row-subtree sharded x{world} (one NCCL all-to-all of x-hat / x halos per hgemv, "
-                            f"{recv_bytes} B received by rank 0)") if recv_bytes is not None else "single GPU",
+            "parallelism": (f"row-subtree sharded x{world} (x-hat / x halos per hgemv: "
+                            + ("P2P writes into the peers' receive buffers with device-side signals"
+                               if getattr(args, "transport", "collective") == "peer" else "one NCCL all-to-all")
+                            + f", {recv_bytes} B received by rank 0)") if recv_bytes is not None else "single GPU",
             "l2": ("L2 flushed before every timed step (write of a 256 MB buffer, untimed; each step timed on its own): "
                    "the payload fits in L2") if cfg.get("l2_flush") else
                   "inputs larger than L2 (payload > 2x the 126 MB L2, no flush needed)"}
@@ -961,6 +963,8 @@ def main():
     ap.add_argument("--b", type=int, default=0, help="override the vector count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-shard", action="store_true", help="use the sharded path even at N=1 (testing)")
+    ap.add_argument("--transport", choices=["collective", "peer"], default="collective",
+                    help="sharded exchange: torch.distributed all-to-all (NCCL) or P2P writes with device signals")
     ap.add_argument("--hara-rng", default="device", choices=["device", "reference"],
                     help="cfg3 Gaussian panels: device Philox (perf) or the reference host stream")
     ap.add_argument("--traffic", type=float, default=None,

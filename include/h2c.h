@@ -281,6 +281,23 @@ int h2c_dist_hgemv_end_owned(h2c_dist_plan p, int64_t b, const double* recvbuf, 
                              double alpha, double beta, void* stream);
 int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha,
                        double beta, void* stream);
+/* peer transport (opt-in; NVLink P2P, no collective library): after setup,
+ * begin() with sendbuf == NULL writes each send item straight into the
+ * destination rank's receive buffer and signals it (system-scope release), and
+ * end() with recvbuf == NULL waits for the sources' signals, unpacks and
+ * acknowledges them, so the exchange needs no host call between begin and end.
+ * Setup, per rank: h2c_dist_peer_alloc (receive buffer for up to max_b columns
+ * + a sync block, plain cudaMalloc), h2c_dist_peer_export (128 bytes of CUDA
+ * IPC handles + this rank's nranks receive offsets), exchange those among the
+ * ranks (e.g. an allgather), then h2c_dist_peer_import with every rank's
+ * handles (nranks x 128 bytes, rank order) and offsets (nranks x nranks, row q
+ * = rank q's). Plans of all ranks living in ONE process (tests) are linked with
+ * h2c_dist_peer_link instead. Every rank must call begin/end the same number of
+ * times (the signals count calls). */
+int h2c_dist_peer_alloc(h2c_dist_plan p, int64_t max_b);
+int h2c_dist_peer_export(h2c_dist_plan p, void* handles, int64_t* recv_off);
+int h2c_dist_peer_import(h2c_dist_plan p, const void* handles, const int64_t* recv_offs);
+int h2c_dist_peer_link(h2c_dist_plan* plans, int n);
 /* host-only partition metadata (no device needed): owner rank per cluster node
  * (-1 = replicated top level) and the exchange items rank dst receives from
  * rank src for a matrix with the given upsweep-basis ranks (arr 0 = x rows of

@@ -142,6 +142,10 @@ _sig("h2c_dist_hgemv_local", i32, H, i64, vp)
 _sig("h2c_dist_hgemv_begin_owned", i32, H, i64, vp, i64, vp, vp)
 _sig("h2c_dist_hgemv_end_owned", i32, H, i64, vp, vp, i64, f64, f64, vp)
 _sig("h2c_dist_hgemv_end", i32, H, i64, vp, vp, i64, f64, f64, vp)
+_sig("h2c_dist_peer_alloc", i32, H, i64)
+_sig("h2c_dist_peer_export", i32, H, vp, vp)
+_sig("h2c_dist_peer_import", i32, H, vp, vp)
+_sig("h2c_dist_peer_link", i32, vp, i32)
 _sig("h2c_partition_owner", i32, H, i32, vp)
 _sig("h2c_partition_exchange", i32, H, i32, i32, vp, i32, i32, i32, P(i64), vp, vp, vp)
 

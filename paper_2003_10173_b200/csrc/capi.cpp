@@ -615,6 +615,46 @@ int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double
     });
 }
 
+int h2c_dist_peer_alloc(h2c_dist_plan p, int64_t max_b) {
+    return guard([&] {
+        need(p != nullptr, "null plan");
+        h2b::dist_peer_alloc(*p->p, max_b);
+    });
+}
+int h2c_dist_peer_export(h2c_dist_plan p, void* handles, int64_t* recv_off) {
+    return guard([&] {
+        need(p != nullptr && handles != nullptr && recv_off != nullptr, "null argument");
+        static_assert(sizeof(h2b::PeerHandles) == 128, "two CUDA IPC handles");
+        std::vector<int64_t> off;
+        const h2b::PeerHandles h = h2b::dist_peer_export(*p->p, off);
+        std::memcpy(handles, &h, sizeof(h));
+        std::copy(off.begin(), off.end(), recv_off);
+    });
+}
+int h2c_dist_peer_import(h2c_dist_plan p, const void* handles, const int64_t* recv_offs) {
+    return guard([&] {
+        need(p != nullptr && handles != nullptr && recv_offs != nullptr, "null argument");
+        int64_t P = 0;
+        std::vector<int64_t> s, r;
+        h2b::dist_counts(*p->p, s, r);
+        P = int64_t(s.size());
+        std::vector<h2b::PeerHandles> all(static_cast<size_t>(P));
+        std::memcpy(all.data(), handles, size_t(P) * sizeof(h2b::PeerHandles));
+        h2b::dist_peer_import(*p->p, all, std::vector<int64_t>(recv_offs, recv_offs + P * P));
+    });
+}
+int h2c_dist_peer_link(h2c_dist_plan* plans, int n) {
+    return guard([&] {
+        need(plans != nullptr && n >= 1, "null argument");
+        std::vector<h2b::DistPlan*> v;
+        for (int i = 0; i < n; ++i) {
+            need(plans[i] != nullptr, "null plan");
+            v.push_back(plans[i]->p.get());
+        }
+        h2b::dist_peer_link(v);
+    });
+}
+
 int h2c_dist_hgemv_begin_owned(h2c_dist_plan p, int64_t b, const double* x_owned, int64_t ldx, double* sendbuf,
                                void* stream) {
     return guard([&] {

@@ -144,6 +144,8 @@ struct XItem {
     int arr;
     int node;
     int64_t unit, rows, buf;
+    int peer = 0;   // send item: destination rank; receive item: source rank
+    int pad = 0;
 };
 // items rank `dst` must receive from rank `src` (identical on every rank)
 std::vector<XItem> exchange_items(const H2Dev& h, bool transpose, const DistSpec& all, int src, int dst,
@@ -172,5 +174,21 @@ void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, in
                     cudaStream_t s, bool owned = false);
 int64_t dist_owned_rows(const DistPlan& p, int64_t* begin);
 int dist_launch_count(const DistPlan& p);
+
+// peer transport (NVLink P2P, no collective library): begin() writes each send
+// item straight into the destination rank's receive buffer and signals it; end()
+// waits for the sources' signals, unpacks and acknowledges. Each plan owns a
+// receive buffer for up to max_b columns and a small sync block (both plain
+// cudaMalloc, so they can be exported with CUDA IPC).
+struct PeerHandles {
+    cudaIpcMemHandle_t recv, sync;
+};
+void dist_peer_alloc(DistPlan& p, int64_t max_b);
+PeerHandles dist_peer_export(const DistPlan& p, std::vector<int64_t>& recv_off);
+// all[q] / all_off[q * nranks + r]: rank q's handles and receive offsets (rows)
+void dist_peer_import(DistPlan& p, const std::vector<PeerHandles>& all, const std::vector<int64_t>& all_off);
+// plans of every rank in one process (their buffers reachable directly)
+void dist_peer_link(const std::vector<DistPlan*>& plans);
+bool dist_peer_ready(const DistPlan& p);
 
 }  // namespace h2b

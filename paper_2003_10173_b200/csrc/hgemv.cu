@@ -2135,6 +2135,21 @@ struct DistPlan {
     int nsend = 0, nrecv = 0;
     bool local_pending = false;   // begin() ran, the local near field (5d) not yet
     Workspace ws;
+    // peer transport (dist_peer_*)
+    std::vector<int64_t> send_off, recv_off;   // rows: my segment per peer in my send / receive buffer
+    int64_t peer_max_b = 0;
+    double* peer_recvbuf = nullptr;            // cudaMalloc'd: recv_rows total x peer_max_b
+    unsigned long long* peer_sync = nullptr;   // flags[nranks], acks[nranks], epoch, done_pack, done_unpack
+    bool peers_ready = false;
+    DeviceArray<double*> d_peer_recv;                 // per rank q: q's receive buffer
+    DeviceArray<int64_t> d_remote_off, d_send_off;    // per q: my segment in q's buffer / in my send order
+    DeviceArray<unsigned long long*> d_peer_flags, d_peer_acks;   // per q: q's flag / ack arrays
+    std::vector<void*> opened;                        // IPC mappings to close
+    ~DistPlan() {
+        for (void* v : opened) cudaIpcCloseMemHandle(v);
+        if (peer_recvbuf) cudaFree(peer_recvbuf);
+        if (peer_sync) cudaFree(peer_sync);
+    }
 };
 
 namespace {
@@ -2150,6 +2165,84 @@ __global__ void exchange_kernel(const XItem* __restrict__ items, int64_t b, doub
         for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) p[e] = a[e];
     else
         for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) a[e] = p[e];
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// peer pack: CTA i writes send item i into its destination rank's receive buffer
+// (P2P over NVLink), after that rank acknowledged my previous delivery. The last
+// CTA to finish publishes this call's epoch in every peer's flag array (release,
+// system scope) and advances the local epoch. Launched with at least one CTA so
+// a rank with nothing to send still signals.
+__global__ void peer_pack_kernel(const XItem* __restrict__ items, int nitems, int64_t b, const double* xint,
+                                 const double* xhat, double* const* __restrict__ peer_recv,
+                                 const int64_t* __restrict__ remote_off, const int64_t* __restrict__ send_off,
+                                 unsigned long long* const* __restrict__ peer_flags, unsigned long long* sync,
+                                 int me, int nranks) {
+    unsigned long long* acks = sync + nranks;
+    unsigned long long* epoch = sync + 2 * nranks;
+    unsigned* done = reinterpret_cast<unsigned*>(sync + 2 * nranks + 1);
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(epoch) + 1;
+    if (int(blockIdx.x) < nitems) {
+        const XItem it = items[blockIdx.x];
+        const int q = it.peer;
+        if (threadIdx.x == 0)
+            while (ld_acquire_sys(&acks[q]) + 1 < e) {}   // q has unpacked my previous delivery
+        __syncthreads();
+        const double* a = (it.arr == 0 ? xint : xhat) + it.unit * b;
+        double* dst = peer_recv[q] + (remote_off[q] + (it.buf - send_off[q])) * b;
+        const int64_t cnt = it.rows * b;
+        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = a[i];
+        __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(done, 1u);
+        if (prev == gridDim.x - 1) {   // every item is written
+            __threadfence_system();
+            for (int r = 0; r < nranks; ++r)
+                if (r != me) st_release_sys(peer_flags[r] + me, e);
+            *reinterpret_cast<volatile unsigned long long*>(epoch) = e;
+            *reinterpret_cast<volatile unsigned*>(done) = 0u;
+        }
+    }
+}
+
+// peer unpack: CTA i waits for its item's source to have delivered this call,
+// unpacks it; the last CTA acknowledges every source (they may overwrite my
+// receive buffer from their next call on)
+__global__ void peer_unpack_kernel(const XItem* __restrict__ items, int nitems, int64_t b, double* xint, double* xhat,
+                                   const double* recvbuf, unsigned long long* const* __restrict__ peer_acks,
+                                   unsigned long long* sync, int me, int nranks) {
+    const unsigned long long* flags = sync;
+    const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(sync + 2 * nranks);
+    unsigned* done = reinterpret_cast<unsigned*>(sync + 2 * nranks + 1) + 1;
+    if (int(blockIdx.x) < nitems) {
+        const XItem it = items[blockIdx.x];
+        if (threadIdx.x == 0)
+            while (ld_acquire_sys(&flags[it.peer]) < e) {}
+        __syncthreads();
+        double* a = (it.arr == 0 ? xint : xhat) + it.unit * b;
+        const double* src = recvbuf + it.buf * b;
+        const int64_t cnt = it.rows * b;
+        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) a[i] = __ldcg(src + i);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(done, 1u);
+        if (prev == gridDim.x - 1) {
+            for (int r = 0; r < nranks; ++r)
+                if (r != me) st_release_sys(peer_acks[r] + me, e);
+            *reinterpret_cast<volatile unsigned*>(done) = 0u;
+        }
+    }
 }
 }  // namespace
 
@@ -2168,8 +2261,11 @@ std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nra
     int64_t so = 0, ro = 0;
     for (int q = 0; q < nranks; ++q) {
         auto out = exchange_items(h, transpose, p->spec, rank, q, cu);   // what q needs from me
+        p->send_off.push_back(so);
+        p->recv_off.push_back(ro);
         for (XItem it : out) {
             it.buf += so;
+            it.peer = q;
             snd.push_back(it);
             p->send_rows[size_t(q)] += it.rows;
         }
@@ -2177,6 +2273,7 @@ std::shared_ptr<DistPlan> make_dist_plan(const H2Dev& h, bool transpose, int nra
         auto in = exchange_items(h, transpose, p->spec, q, rank, cu);    // what I need from q
         for (XItem it : in) {
             it.buf += ro;
+            it.peer = q;
             rcv.push_back(it);
             p->recv_rows[size_t(q)] += it.rows;
         }
@@ -2220,6 +2317,15 @@ void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, doub
     hgemv_impl(*p.h, p.transpose, !owned, n, b, xb, ldx, nullptr, owned ? ldx : n, 1.0, 0.0, s, p.ws, nullptr,
                p.plan.get(), 1 | (owned ? 8 : 0));
     p.local_pending = true;
+    if (!sendbuf && p.spec.nranks > 1) {   // peer transport
+        if (!p.peers_ready) throw std::logic_error("dist hgemv: no send buffer and no peer transport set up");
+        if (b > p.peer_max_b) throw std::invalid_argument("dist hgemv: b exceeds the peer buffers' max_b");
+        peer_pack_kernel<<<std::max(p.nsend, 1), 256, 0, s>>>(
+            p.send_items.data(), p.nsend, b, p.ws.xint.data(), p.ws.xhat.data(), p.d_peer_recv.data(),
+            p.d_remote_off.data(), p.d_send_off.data(), p.d_peer_flags.data(), p.peer_sync, p.spec.rank, p.spec.nranks);
+        H2B_LAUNCH();
+        return;
+    }
     if (p.nsend) {
         exchange_kernel<<<p.nsend, 256, 0, s>>>(p.send_items.data(), b, p.ws.xint.data(), p.ws.xhat.data(), sendbuf, 0);
         H2B_LAUNCH();
@@ -2229,7 +2335,14 @@ void dist_hgemv_begin(DistPlan& p, int64_t b, const double* x, int64_t ldx, doub
 void dist_hgemv_end(DistPlan& p, int64_t b, const double* recvbuf, double* y, int64_t ldy, double alpha, double beta,
                     cudaStream_t s, bool owned) {
     const int64_t n = p.h->tree().n;
-    if (p.nrecv) {
+    if (!recvbuf && p.spec.nranks > 1) {   // peer transport
+        if (!p.peers_ready) throw std::logic_error("dist hgemv: no receive buffer and no peer transport set up");
+        peer_unpack_kernel<<<std::max(p.nrecv, 1), 256, 0, s>>>(p.recv_items.data(), p.nrecv, b, p.ws.xint.data(),
+                                                                p.ws.xhat.data(), p.peer_recvbuf,
+                                                                p.d_peer_acks.data(), p.peer_sync, p.spec.rank,
+                                                                p.spec.nranks);
+        H2B_LAUNCH();
+    } else if (p.nrecv) {
         exchange_kernel<<<p.nrecv, 256, 0, s>>>(p.recv_items.data(), b, p.ws.xint.data(), p.ws.xhat.data(),
                                                 const_cast<double*>(recvbuf), 1);
         H2B_LAUNCH();
@@ -2250,6 +2363,99 @@ void dist_hgemv_local(DistPlan& p, int64_t b, cudaStream_t s) {
     hgemv_impl(*p.h, p.transpose, true, n, b, nullptr, n, nullptr, n, 1.0, 0.0, s, p.ws, nullptr, p.plan.get(), 4);
     p.local_pending = false;
 }
+
+void dist_peer_alloc(DistPlan& p, int64_t max_b) {
+    if (max_b < 1) throw std::invalid_argument("dist peer: max_b must be >= 1");
+    if (p.peer_recvbuf) cudaFree(p.peer_recvbuf);
+    if (p.peer_sync) cudaFree(p.peer_sync);
+    p.peer_recvbuf = nullptr;
+    p.peer_sync = nullptr;
+    int64_t rows = 0;
+    for (int64_t r : p.recv_rows) rows += r;
+    H2B_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.peer_recvbuf), size_t(std::max<int64_t>(rows * max_b, 1)) * 8));
+    const size_t nsync = size_t(2 * p.spec.nranks + 2);
+    H2B_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.peer_sync), nsync * sizeof(unsigned long long)));
+    H2B_CUDA(cudaMemset(p.peer_sync, 0, nsync * sizeof(unsigned long long)));
+    H2B_CUDA(cudaDeviceSynchronize());
+    p.peer_max_b = max_b;
+    p.peers_ready = false;
+}
+
+PeerHandles dist_peer_export(const DistPlan& p, std::vector<int64_t>& recv_off) {
+    if (!p.peer_recvbuf) throw std::logic_error("dist peer: call dist_peer_alloc first");
+    PeerHandles h{};
+    H2B_CUDA(cudaIpcGetMemHandle(&h.recv, p.peer_recvbuf));
+    H2B_CUDA(cudaIpcGetMemHandle(&h.sync, p.peer_sync));
+    recv_off = p.recv_off;
+    return h;
+}
+
+namespace {
+void upload_peers(DistPlan& p, const std::vector<double*>& recv, const std::vector<unsigned long long*>& sync,
+                  const std::vector<int64_t>& all_off, int64_t max_b) {
+    const int P = p.spec.nranks, me = p.spec.rank;
+    if (max_b != p.peer_max_b) throw std::invalid_argument("dist peer: ranks disagree on max_b");
+    std::vector<int64_t> remote(static_cast<size_t>(P), 0);
+    std::vector<unsigned long long*> flags(static_cast<size_t>(P)), acks(static_cast<size_t>(P));
+    for (int q = 0; q < P; ++q) {
+        remote[size_t(q)] = all_off[size_t(q) * size_t(P) + size_t(me)];   // my segment in q's receive buffer
+        flags[size_t(q)] = sync[size_t(q)];
+        acks[size_t(q)] = sync[size_t(q)] + P;
+    }
+    p.d_peer_recv.upload(recv);
+    p.d_remote_off.upload(remote);
+    p.d_send_off.upload(p.send_off);
+    p.d_peer_flags.upload(flags);
+    p.d_peer_acks.upload(acks);
+    H2B_CUDA(cudaDeviceSynchronize());
+    p.peers_ready = true;
+}
+}  // namespace
+
+void dist_peer_import(DistPlan& p, const std::vector<PeerHandles>& all, const std::vector<int64_t>& all_off) {
+    const int P = p.spec.nranks, me = p.spec.rank;
+    if (int(all.size()) != P || int64_t(all_off.size()) != int64_t(P) * P)
+        throw std::invalid_argument("dist peer: need every rank's handles and offsets");
+    if (!p.peer_recvbuf) throw std::logic_error("dist peer: call dist_peer_alloc first");
+    for (void* v : p.opened) cudaIpcCloseMemHandle(v);
+    p.opened.clear();
+    std::vector<double*> recv(static_cast<size_t>(P));
+    std::vector<unsigned long long*> sync(static_cast<size_t>(P));
+    for (int q = 0; q < P; ++q) {
+        if (q == me) {
+            recv[size_t(q)] = p.peer_recvbuf;
+            sync[size_t(q)] = p.peer_sync;
+            continue;
+        }
+        void* r = nullptr;
+        void* y = nullptr;
+        H2B_CUDA(cudaIpcOpenMemHandle(&r, all[size_t(q)].recv, cudaIpcMemLazyEnablePeerAccess));
+        H2B_CUDA(cudaIpcOpenMemHandle(&y, all[size_t(q)].sync, cudaIpcMemLazyEnablePeerAccess));
+        p.opened.push_back(r);
+        p.opened.push_back(y);
+        recv[size_t(q)] = static_cast<double*>(r);
+        sync[size_t(q)] = static_cast<unsigned long long*>(y);
+    }
+    upload_peers(p, recv, sync, all_off, p.peer_max_b);
+}
+
+void dist_peer_link(const std::vector<DistPlan*>& plans) {
+    const int P = int(plans.size());
+    std::vector<int64_t> all_off;
+    std::vector<double*> recv;
+    std::vector<unsigned long long*> sync;
+    for (int q = 0; q < P; ++q) {
+        DistPlan& d = *plans[size_t(q)];
+        if (d.spec.nranks != P || d.spec.rank != q) throw std::invalid_argument("dist peer link: plans must be ranks 0..P-1");
+        if (!d.peer_recvbuf) throw std::logic_error("dist peer: call dist_peer_alloc first");
+        all_off.insert(all_off.end(), d.recv_off.begin(), d.recv_off.end());
+        recv.push_back(d.peer_recvbuf);
+        sync.push_back(d.peer_sync);
+    }
+    for (int q = 0; q < P; ++q) upload_peers(*plans[size_t(q)], recv, sync, all_off, plans[0]->peer_max_b);
+}
+
+bool dist_peer_ready(const DistPlan& p) { return p.peers_ready; }
 
 int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
     auto plan = select_plan(h, transpose, b);   // the plan hgemv actually runs at this b

@@ -5,7 +5,10 @@ hgemv; every compute step runs in lib/libh2b200.so.
 Rank r of P owns the subtree under the r-th node of level log2 P (its rows of
 x and y); the top log2 P levels are replicated. The exchange carries the
 x-hat of remote clusters that owned couplings / the replicated top upsweep read
-and the x rows of remote near-field leaves (h2c.h, h2c_dist_*)."""
+and the x rows of remote near-field leaves (h2c.h, h2c_dist_*). It runs either
+through torch.distributed (all_to_all_single) or, with transport="peer", as P2P
+writes straight into the other GPUs' receive buffers with device-side signals
+(h2c_dist_peer_*), so the exchange rides inside the begin / end kernels."""
 import ctypes as C
 
 import numpy as np
@@ -65,20 +68,46 @@ class DistPlan:
         check(lib.h2c_dist_plan_launches(self._h, C.byref(v)))
         return v.value
 
+    # ---- peer transport (h2c_dist_peer_*): P2P writes + signals, no collective call
+    def peer_alloc(self, max_b):
+        check(lib.h2c_dist_peer_alloc(self._h, int(max_b)))
+
+    def peer_export(self):
+        """(128 bytes of CUDA IPC handles, this rank's receive offsets in rows)."""
+        hb = (C.c_char * 128)()
+        off = np.zeros(self.nranks, np.int64)
+        check(lib.h2c_dist_peer_export(self._h, C.cast(hb, C.c_void_p), off.ctypes.data_as(C.c_void_p)))
+        return bytes(hb), off
+
+    def peer_import(self, handles, offsets):
+        """handles: every rank's export bytes (rank order); offsets: every rank's offsets."""
+        hb = b"".join(handles)
+        off = np.ascontiguousarray(np.stack(offsets), np.int64)
+        check(lib.h2c_dist_peer_import(self._h, C.c_char_p(hb), off.ctypes.data_as(C.c_void_p)))
+
+    @staticmethod
+    def peer_link(plans):
+        """Link the plans of every rank held by this process (ranks 0..P-1, tests)."""
+        arr = (C.c_void_p * len(plans))(*[C.cast(p._h, C.c_void_p).value for p in plans])
+        check(lib.h2c_dist_peer_link(arr, len(plans)))
+
     def begin(self, x, sendbuf, b, stream=None, owned=False):
-        """owned: x holds only this rank's owned_rows rows, in cluster order."""
+        """owned: x holds only this rank's owned_rows rows, in cluster order.
+        sendbuf None: peer transport (requires peer setup)."""
         _, ldx = col_major_geom(x)
         fn = lib.h2c_dist_hgemv_begin_owned if owned else lib.h2c_dist_hgemv_begin
-        check(fn(self._h, int(b), x.data_ptr(), ldx, sendbuf.data_ptr(), stream))
+        check(fn(self._h, int(b), x.data_ptr(), ldx, None if sendbuf is None else sendbuf.data_ptr(), stream))
 
     def local(self, b, stream=None):
         """Near-field products with this rank's own source rows (overlaps the exchange)."""
         check(lib.h2c_dist_hgemv_local(self._h, int(b), stream))
 
     def end(self, recvbuf, y, b, alpha=1.0, beta=0.0, stream=None, owned=False):
+        """recvbuf None: peer transport (requires peer setup)."""
         _, ldy = col_major_geom(y)
         fn = lib.h2c_dist_hgemv_end_owned if owned else lib.h2c_dist_hgemv_end
-        check(fn(self._h, int(b), recvbuf.data_ptr(), y.data_ptr(), ldy, float(alpha), float(beta), stream))
+        check(fn(self._h, int(b), None if recvbuf is None else recvbuf.data_ptr(), y.data_ptr(), ldy, float(alpha),
+                 float(beta), stream))
 
 
 class ShardedHgemv:
@@ -94,7 +123,11 @@ class ShardedHgemv:
     on NCCL's stream, concurrent with the local near field); other backends
     (gloo) stage the buffers through host memory."""
 
-    def __init__(self, m, group=None, transpose=False):
+    def __init__(self, m, group=None, transpose=False, transport="collective", max_b=64):
+        """transport "collective": the all-to-all through torch.distributed (NCCL on
+        device buffers, host-staged for gloo); "peer": P2P writes into the other GPUs'
+        receive buffers with device-side signals (CUDA IPC handles exchanged once
+        with an allgather over `group`; every GPU must be peer-accessible)."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -103,6 +136,16 @@ class ShardedHgemv:
         self.plan = DistPlan(m, world, rank, transpose)
         self.device_collective = dist.is_initialized() and dist.get_backend(group) == "nccl"
         self._bufs = {}
+        if transport not in ("collective", "peer"):
+            raise ValueError("transport must be 'collective' or 'peer'")
+        self.peer = transport == "peer" and world > 1
+        self.max_b = int(max_b)
+        if self.peer:
+            self.plan.peer_alloc(self.max_b)
+            mine = self.plan.peer_export()
+            allv = [None] * world
+            dist.all_gather_object(allv, mine, group=group)
+            self.plan.peer_import([a[0] for a in allv], [a[1] for a in allv])
 
     def _buffers(self, b, device):
         import torch
@@ -117,8 +160,15 @@ class ShardedHgemv:
         only this rank's plan.owned_rows rows, in cluster order."""
         import torch
         b = x.shape[1] if x.dim() == 2 else 1
-        send, recv = self._buffers(b, x.device)
         s = torch.cuda.current_stream(x.device).cuda_stream
+        if self.peer:   # the exchange is device-side: no host call between begin and end
+            if b > self.max_b:
+                raise ValueError(f"peer transport: b={b} exceeds max_b={self.max_b}")
+            self.plan.begin(x, None, b, s, owned)
+            self.plan.local(b, s)
+            self.plan.end(None, y, b, alpha, beta, s, owned)
+            return
+        send, recv = self._buffers(b, x.device)
         self.plan.begin(x, send, b, s, owned)
         if self.plan.nranks > 1:
             ns, nr = int(self.plan.send_rows.sum()) * b, int(self.plan.recv_rows.sum()) * b

@@ -224,3 +224,52 @@ def test_sharded_hgemv_two_processes_gloo(cuda, sym):
         pr.join(timeout=120)
     assert isinstance(res, float), res
     assert res <= 1e-12
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("case", list(CASES))
+def test_peer_transport_equals_collective(cuda, P, case):
+    """Peer transport (h2c_dist_peer_*): begin writes every send item straight into
+    its destination plan's receive buffer and signals it; end waits for the signals,
+    unpacks and acknowledges. The P plans live in this process on one GPU and are
+    linked directly; all begins are enqueued before any end, so no kernel ever waits
+    on work that has not already run. Three calls exercise the epoch counters and the
+    acknowledgements; the result is bitwise the collective path's."""
+    import torch
+    mk, leaf, weak = CASES[case]
+    pts = mk()
+    ct = build_cluster_tree(pts, leaf)
+    bt = build_block_tree(ct, ct, 1.0, Admissibility.weak if weak else Admissibility.strong)
+    ref = O.Tree(pts, leaf, 1.0, weak)
+    ora = O.H2.random(ref, False, 12, 8)
+    rr, cr = ora.ranks()
+    m = H2Matrix.from_packed(bt, False, rr, cr, ora.export())
+    n, b = pts.shape[0], 5
+    plans = [DistPlan(m, P, r) for r in range(P)]
+    for p in plans:
+        p.peer_alloc(8)
+    DistPlan.peer_link(plans)
+    for call in range(3):
+        xc = torch.randn(b, n, dtype=torch.float64, device=cuda).t()
+        y_coll = torch.zeros(b, n, dtype=torch.float64, device=cuda).t()
+        simulate(m, P, xc, y_coll, b, local=True)
+        y = torch.full((b, n), 3.0, dtype=torch.float64, device=cuda).t()
+        for p in plans:
+            p.begin(xc, None, b)
+            p.local(b)
+        for p in plans:
+            p.end(None, y, b)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_coll), float((y - y_coll).abs().max())
+
+
+def test_peer_transport_needs_setup(cuda):
+    import torch
+    pts = O.grid2d(32, 32)
+    ct = build_cluster_tree(pts, 32)
+    bt = build_block_tree(ct, ct, 1.0)
+    m = H2Matrix.kernel(bt, pts, "gaussian", 0.1, 8)
+    p = DistPlan(m, 2, 0)
+    x = torch.randn(2, pts.shape[0], dtype=torch.float64, device=cuda).t()
+    with pytest.raises(NotImplementedError):   # std::logic_error: no buffer and no peer transport
+        p.begin(x, None, 2)

@@ -24,8 +24,11 @@ yps = [torch.empty(b, n, dtype=torch.float64).pin_memory() for _ in range(3)]
 X = xp.cuda()
 Y = torch.empty_like(X)
 streams = [torch.cuda.Stream() for _ in range(3)]
-for graph in (0, 1):
-    lib.h2b_tune(3, graph)
+# KNOB=which VALS=v1,v2 (default: graph replay off / on)
+knob = int(os.environ.get("KNOB", "3"))
+vals = [int(v) for v in os.environ.get("VALS", "0,1").split(",")]
+for graph in vals + vals:
+    lib.h2b_tune(knob, graph)
     for _ in range(3):
         check(lib.h2c_hgemv(m._h, 0, 0, n, b, X.data_ptr(), n, Y.data_ptr(), n, 1.0, 0.0, None))
     torch.cuda.synchronize()
@@ -60,6 +63,6 @@ for graph in (0, 1):
         yps[0].copy_(X, non_blocking=True)
     torch.cuda.synchronize()
     tdh = (time.perf_counter() - t0) / 5
-    print(f"graph={graph}: device {td*1e3:.2f} ms, sync host {ts*1e3:.2f} ms, async3 {ta*1e3:.2f} ms, "
+    print(f"knob{knob}={graph}: device {td*1e3:.2f} ms, sync host {ts*1e3:.2f} ms, async3 {ta*1e3:.2f} ms, "
           f"H2D {th*1e3:.2f} ms ({8*n*b/th/1e9:.1f} GB/s), D2H {tdh*1e3:.2f} ms ({8*n*b/tdh/1e9:.1f} GB/s)",
           flush=True)
