@@ -292,8 +292,8 @@ int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double
  * ranks (e.g. an allgather), then h2c_dist_peer_import with every rank's
  * handles (nranks x 128 bytes, rank order) and offsets (nranks x nranks, row q
  * = rank q's). Plans of all ranks living in ONE process (tests) are linked with
- * h2c_dist_peer_link instead. Every rank must call begin/end the same number of
- * times (the signals count calls). */
+ * h2c_dist_peer_link instead. Every rank must use the same max_b and call
+ * begin/end the same number of times with the same b (the signals count calls). */
 int h2c_dist_peer_alloc(h2c_dist_plan p, int64_t max_b);
 int h2c_dist_peer_export(h2c_dist_plan p, void* handles, int64_t* recv_off);
 int h2c_dist_peer_import(h2c_dist_plan p, const void* handles, const int64_t* recv_offs);
