@@ -241,6 +241,80 @@ private:
     std::shared_ptr<h2c_matrix_s> h_;
 };
 
+// ---- row-subtree sharded hgemv (the reference is single-process) ----
+// One plan per rank (one process per GPU). begin() (owned upsweep + pack) ->
+// the exchange -> local() (near field of owned source rows, optional, while the
+// exchange is in flight) -> end() (unpack, couplings, downsweep, remaining near
+// field, owned rows of y). The exchange is either the caller's collective on
+// send / receive buffers (sizes send_rows() / recv_rows() times b doubles,
+// peers in rank order) or, after the peer setup below, device-side P2P writes
+// and signals: begin(..., nullptr) / end(nullptr, ...).
+class ShardedPlan {
+public:
+    ShardedPlan(const H2Matrix& h, int nranks, int rank, bool transpose = false) : nranks_(nranks), rank_(rank) {
+        h2c_dist_plan p = nullptr;
+        detail::check(h2c_dist_plan_create(h.handle(), transpose ? 1 : 0, nranks, rank, &p));
+        h_.reset(p, [](h2c_dist_plan q) { h2c_dist_plan_destroy(q); });
+        send_.assign(size_t(nranks), 0);
+        recv_.assign(size_t(nranks), 0);
+        int64_t ob = 0, orows = 0;
+        detail::check(h2c_dist_plan_counts(p, send_.data(), recv_.data(), &ob, &orows));
+        owned_begin_ = ob;
+        owned_rows_ = orows;
+    }
+    int nranks() const { return nranks_; }
+    int rank() const { return rank_; }
+    const std::vector<int64_t>& send_rows() const { return send_; }
+    const std::vector<int64_t>& recv_rows() const { return recv_; }
+    Index owned_begin() const { return owned_begin_; }   // internal (cluster) row range of this rank
+    Index owned_rows() const { return owned_rows_; }
+    // x_dev / y_dev: full n x b user-order device matrices (owned = false) or this rank's
+    // owned_rows() rows in cluster order (owned = true)
+    void begin(Index b, const double* x_dev, Index ldx, double* sendbuf, void* stream = nullptr, bool owned = false) {
+        detail::check(owned ? h2c_dist_hgemv_begin_owned(h_.get(), b, x_dev, ldx, sendbuf, stream)
+                            : h2c_dist_hgemv_begin(h_.get(), b, x_dev, ldx, sendbuf, stream));
+    }
+    void local(Index b, void* stream = nullptr) { detail::check(h2c_dist_hgemv_local(h_.get(), b, stream)); }
+    void end(Index b, const double* recvbuf, double* y_dev, Index ldy, double alpha = 1.0, double beta = 0.0,
+             void* stream = nullptr, bool owned = false) {
+        detail::check(owned ? h2c_dist_hgemv_end_owned(h_.get(), b, recvbuf, y_dev, ldy, alpha, beta, stream)
+                            : h2c_dist_hgemv_end(h_.get(), b, recvbuf, y_dev, ldy, alpha, beta, stream));
+    }
+    // peer transport: alloc on every rank (same max_b), export, allgather the exports,
+    // import all of them (or link the plans of every rank held by one process)
+    struct PeerInfo {
+        std::vector<unsigned char> handles;   // 128 bytes (CUDA IPC)
+        std::vector<int64_t> recv_off;        // nranks entries (rows)
+    };
+    void peer_alloc(Index max_b) { detail::check(h2c_dist_peer_alloc(h_.get(), max_b)); }
+    PeerInfo peer_export() const {
+        PeerInfo i{std::vector<unsigned char>(128), std::vector<int64_t>(size_t(nranks_))};
+        detail::check(h2c_dist_peer_export(h_.get(), i.handles.data(), i.recv_off.data()));
+        return i;
+    }
+    void peer_import(const std::vector<PeerInfo>& all) {
+        std::vector<unsigned char> hb;
+        std::vector<int64_t> off;
+        for (const PeerInfo& i : all) {
+            hb.insert(hb.end(), i.handles.begin(), i.handles.end());
+            off.insert(off.end(), i.recv_off.begin(), i.recv_off.end());
+        }
+        detail::check(h2c_dist_peer_import(h_.get(), hb.data(), off.data()));
+    }
+    static void peer_link(const std::vector<ShardedPlan*>& plans) {
+        std::vector<h2c_dist_plan> hs;
+        for (ShardedPlan* p : plans) hs.push_back(p->h_.get());
+        detail::check(h2c_dist_peer_link(hs.data(), int(hs.size())));
+    }
+    h2c_dist_plan handle() const { return h_.get(); }
+
+private:
+    int nranks_ = 1, rank_ = 0;
+    std::vector<int64_t> send_, recv_;
+    Index owned_begin_ = 0, owned_rows_ = 0;
+    std::shared_ptr<h2c_dist_plan_s> h_;
+};
+
 inline H2Matrix orthogonalize(const H2Matrix& h) {   // algebra.hpp:72-113
     h2c_matrix o = nullptr;
     detail::check(h2c_orthogonalize(h.handle(), &o));

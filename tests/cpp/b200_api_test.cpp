@@ -4,6 +4,8 @@
 #include <cmath>
 #include <random>
 
+#include <cuda_runtime.h>
+
 #include "../../include/h2b200.hpp"
 #include "mini_test.hpp"
 
@@ -295,4 +297,73 @@ TEST_CASE("diffusion oracle: registry, symmetric PSD Hessian, two marches per so
     // HARA on the device operator (the cfg3 pipeline at desk scale)
     auto res = peel_construct(*o.op, o.default_block_tree(), PeelConfig{1e-6});
     CHECK(estimate_relative_error(*o.op, res.matrix) <= 3e-6);
+}
+
+TEST_CASE("sharded hgemv through the C++ mirror: collective buffers and peer transport") {
+    // two ranks held by this process on one GPU: the collective exchange is done by
+    // device copies in rank order; the peer transport links the plans directly and
+    // enqueues both begins before either end (nothing waits on work that has not run)
+    std::mt19937_64 rng(77);
+    const Index n = 256, b = 3;
+    Matrix g = random_matrix(n, n, rng);
+    Matrix a = mul(g, g, true);
+    for (Index i = 0; i < n; ++i) a(i, i) += double(n);
+    auto op = DenseOperator(a, true);
+    PeelConfig tight;
+    tight.eps = 1e-10;
+    auto h = peel_construct(op, tree1d(n, 16, Admissibility::weak), tight).matrix;
+    Matrix x = random_matrix(n, b, rng);
+    const Matrix y_ref = h.matvec(x);
+    double *dx = nullptr, *dy = nullptr;
+    CHECK(cudaMalloc(reinterpret_cast<void**>(&dx), sizeof(double) * n * b) == cudaSuccess);
+    CHECK(cudaMalloc(reinterpret_cast<void**>(&dy), sizeof(double) * n * b) == cudaSuccess);
+    cudaMemcpy(dx, x.data(), sizeof(double) * n * b, cudaMemcpyHostToDevice);
+    std::vector<ShardedPlan> plans{ShardedPlan(h, 2, 0), ShardedPlan(h, 2, 1)};
+    CHECK(plans[0].owned_rows() + plans[1].owned_rows() == n);
+    // collective layout: rank r receives, in source order, what each q sends to r
+    std::vector<double*> send(2), recv(2);
+    for (int r = 0; r < 2; ++r) {
+        int64_t ns = 0, nr = 0;
+        for (int q = 0; q < 2; ++q) {
+            ns += plans[size_t(r)].send_rows()[size_t(q)];
+            nr += plans[size_t(r)].recv_rows()[size_t(q)];
+        }
+        cudaMalloc(reinterpret_cast<void**>(&send[size_t(r)]), sizeof(double) * std::max<int64_t>(ns * b, 1));
+        cudaMalloc(reinterpret_cast<void**>(&recv[size_t(r)]), sizeof(double) * std::max<int64_t>(nr * b, 1));
+    }
+    for (int r = 0; r < 2; ++r) plans[size_t(r)].begin(b, dx, n, send[size_t(r)]);
+    for (int r = 0; r < 2; ++r) {
+        int64_t at = 0;
+        for (int q = 0; q < 2; ++q) {
+            int64_t off = 0;
+            for (int s = 0; s < r; ++s) off += plans[size_t(q)].send_rows()[size_t(s)];
+            const int64_t rows = plans[size_t(q)].send_rows()[size_t(r)];
+            CHECK(rows == plans[size_t(r)].recv_rows()[size_t(q)]);
+            cudaMemcpy(recv[size_t(r)] + at * b, send[size_t(q)] + off * b, sizeof(double) * rows * b,
+                       cudaMemcpyDeviceToDevice);
+            at += rows;
+        }
+        plans[size_t(r)].end(b, recv[size_t(r)], dy, n);
+    }
+    Matrix y(n, b);
+    cudaMemcpy(y.data(), dy, sizeof(double) * n * b, cudaMemcpyDeviceToHost);
+    CHECK(rel_err(y, y_ref) < 1e-12);
+    // peer transport, twice (epochs and acknowledgements): bitwise the collective result
+    for (ShardedPlan& p : plans) p.peer_alloc(4);
+    ShardedPlan::peer_link({&plans[0], &plans[1]});
+    for (int call = 0; call < 2; ++call) {
+        cudaMemset(dy, 0, sizeof(double) * n * b);
+        for (ShardedPlan& p : plans) {
+            p.begin(b, dx, n, nullptr);
+            p.local(b);
+        }
+        for (ShardedPlan& p : plans) p.end(b, nullptr, dy, n);
+        Matrix yp(n, b);
+        cudaMemcpy(yp.data(), dy, sizeof(double) * n * b, cudaMemcpyDeviceToHost);
+        CHECK(rel_err(yp, y) == 0.0);
+    }
+    for (double* p : send) cudaFree(p);
+    for (double* p : recv) cudaFree(p);
+    cudaFree(dx);
+    cudaFree(dy);
 }

@@ -14,7 +14,8 @@ def build():
     subprocess.run(["g++", "-std=c++17", "-O3", "-march=x86-64-v3", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
                     "-I/usr/local/cuda/include", os.path.join(ROOT, "tests", "cpp", "b200_api_test.cpp"),
                     "-L" + os.path.join(ROOT, "paper_2003_10173_b200", "lib"), "-lh2b200",
-                    "-Wl,-rpath," + os.path.join(ROOT, "paper_2003_10173_b200", "lib"), "-o", BIN], check=True)
+                    "-Wl,-rpath," + os.path.join(ROOT, "paper_2003_10173_b200", "lib"),
+                    "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", BIN], check=True)
 
 
 def test_cpp_api_compiles_and_links():
