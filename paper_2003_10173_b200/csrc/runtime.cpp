@@ -24,19 +24,17 @@ void ensure_mem_pool() {
 
 namespace {
 // Bump allocator over a pinned host ring, mirrored by a device ring of the
-// same size for descriptor lists. Each put records an event (from a reused
-// pool); when the ring wraps, every recorded event is waited for, and if the
-// device ring was used the device is synchronised as well (a kernel may still
-// read descriptors a later copy would overwrite, possibly from another stream).
+// same size for descriptor lists. Puts only copy into the ring and enqueue the
+// H2D copy; when the ring wraps, the device is synchronised once (every copy out
+// of the ring, and every kernel that may still read a device-ring descriptor
+// list, has finished), after which the whole ring is free again. No per-put
+// event: HARA issues thousands of small uploads per build.
 struct Staging {
     std::mutex mu;
     char* buf = nullptr;    // pinned host ring
     char* dbuf = nullptr;   // device ring (descriptor lists)
     size_t cap = 0, head = 0;
-    std::vector<cudaEvent_t> events;
-    size_t nev = 0;
-    bool dev_used = false;
-    static constexpr size_t kMaxEvents = 8192;
+    size_t wraps = 0, puts = 0;
 
     void init() {
         if (buf) return;
@@ -44,28 +42,19 @@ struct Staging {
         H2B_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&buf), cap, cudaHostAllocPortable));
     }
     void drain() {
-        for (size_t i = 0; i < nev; ++i) H2B_CUDA(cudaEventSynchronize(events[i]));
-        if (dev_used) H2B_CUDA(cudaDeviceSynchronize());
-        nev = 0;
+        H2B_CUDA(cudaDeviceSynchronize());
         head = 0;
-        dev_used = false;
+        ++wraps;
     }
     // pinned copy of `host`; returns the ring offset
     size_t reserve(const void* host, size_t bytes) {
         const size_t b = (bytes + 255) & ~size_t(255);
-        if (head + b > cap || nev == kMaxEvents) drain();
+        if (head + b > cap) drain();
         const size_t off = head;
         head += b;
+        ++puts;
         std::memcpy(buf + off, host, bytes);
         return off;
-    }
-    void record(cudaStream_t s) {
-        if (nev == events.size()) {
-            cudaEvent_t e;
-            H2B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            events.push_back(e);
-        }
-        H2B_CUDA(cudaEventRecord(events[nev++], s));
     }
     void* put(const void* host, size_t bytes, void* dst, cudaStream_t s) {
         std::lock_guard<std::mutex> g(mu);
@@ -76,7 +65,6 @@ struct Staging {
         init();
         const size_t off = reserve(host, bytes);
         H2B_CUDA(cudaMemcpyAsync(dst, buf + off, bytes, cudaMemcpyHostToDevice, s));
-        record(s);
         return dst;
     }
     const void* put_dev(const void* host, size_t bytes, cudaStream_t s) {
@@ -86,8 +74,6 @@ struct Staging {
         if (!dbuf) H2B_CUDA(cudaMalloc(reinterpret_cast<void**>(&dbuf), cap));
         const size_t off = reserve(host, bytes);
         H2B_CUDA(cudaMemcpyAsync(dbuf + off, buf + off, bytes, cudaMemcpyHostToDevice, s));
-        record(s);
-        dev_used = true;
         return dbuf + off;
     }
 };
@@ -101,8 +87,21 @@ void* stage_to_device(const void* host, size_t bytes, void* dev_dst, cudaStream_
     return staging().put(host, bytes, dev_dst, s);
 }
 
+void Staging_stats(long long* puts, long long* wraps) {
+    Staging& st = staging();
+    std::lock_guard<std::mutex> g(st.mu);
+    if (puts) *puts = static_cast<long long>(st.puts);
+    if (wraps) *wraps = static_cast<long long>(st.wraps);
+}
+
 const void* stage_descriptors(const void* host, size_t bytes, cudaStream_t s) {
     return staging().put_dev(host, bytes, s);
 }
 
 }  // namespace h2b
+
+// diagnostics hook: uploads through the staging ring and ring wraps (device syncs) so far
+extern "C" int h2b_staging_stats(long long* puts, long long* wraps) {
+    h2b::Staging_stats(puts, wraps);
+    return 0;
+}
