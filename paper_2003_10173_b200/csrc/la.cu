@@ -1,3 +1,6 @@
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 // Batched small dense linear algebra for HARA / recompression on sm_100a.
 // See la.hpp. All kernels take descriptor lists; one CTA (or one tile) per
 // independent problem. Reductions are done in a fixed order (deterministic:
@@ -325,6 +328,10 @@ struct SvdJob {
     int ldu;
 };
 
+constexpr int kJacobiSweeps = 30;
+// diagnostics: sweeps run and problems solved by jacobi_kernel (h2b_jacobi_stats)
+__device__ unsigned long long g_jacobi_sweeps = 0, g_jacobi_problems = 0, g_jacobi_capped = 0;
+
 template <bool SMEM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__ jobs) {
     extern __shared__ double sm[];
@@ -332,8 +339,8 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
     const SvdJob jb = jobs[blockIdx.x];
     const int r = jb.rows, c = jb.cols, ce = c + (c & 1);
     double* M = SMEM ? sm : jb.work;           // r x ce
-    double* V = M + int64_t(r) * ce;           // ce x ce
-    double* nrm = V + int64_t(ce) * ce;        // ce
+    double* V = M + int64_t(r) * ce;           // ce x ce (only when right vectors are asked for)
+    double* nrm = V + (jb.V ? int64_t(ce) * ce : 0);   // ce
     int* order = reinterpret_cast<int*>(nrm + ce);   // c (selection order)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
     for (int64_t e = tid; e < int64_t(r) * ce; e += blockDim.x) {
@@ -342,9 +349,16 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
         if (j < c) v = jb.trans ? jb.A[j + int64_t(i) * jb.lda] : jb.A[i + int64_t(j) * jb.lda];
         M[e] = v;
     }
-    for (int64_t e = tid; e < int64_t(ce) * ce; e += blockDim.x) V[e] = (e % ce) == (e / ce) ? 1.0 : 0.0;
+    if (jb.V)
+        for (int64_t e = tid; e < int64_t(ce) * ce; e += blockDim.x) V[e] = (e % ce) == (e / ce) ? 1.0 : 0.0;
     __syncthreads();
-    for (int sweep = 0; sweep < 60 && ce >= 2; ++sweep) {
+    // convergence: a pair rotates only while |gamma| > tol sqrt(alpha beta), tol = max(1e-15,
+    // sqrt(rows) eps) (dgesvj's choice; a stricter one can cycle on rounding noise), at most
+    // kJacobiSweeps sweeps (dgesvj's NSWEEP: the columns still rotating by then are the ones at
+    // the rounding-noise floor, whose rotations against large columns keep re-injecting noise)
+    const double tol = fmax(1e-15, sqrt(double(r)) * 1.1102230246251565e-16);
+    int sweep = 0;
+    for (; sweep < kJacobiSweeps && ce >= 2; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int round = 0; round < ce - 1; ++round) {
@@ -364,7 +378,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
                 al = warp_sum(al);
                 be = warp_sum(be);
                 ga = warp_sum(ga);
-                if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
                 if (lane == 0) rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -388,6 +402,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
         }
         if (!rotated) break;
         __syncthreads();
+    }
+    if (tid == 0) {
+        atomicAdd(&g_jacobi_sweeps, (unsigned long long)(sweep + 1));
+        atomicAdd(&g_jacobi_problems, 1ull);
+        if (sweep == kJacobiSweeps) atomicAdd(&g_jacobi_capped, 1ull);
     }
     for (int j = warp; j < c; j += nw) {
         const double* mj = M + int64_t(j) * r;
@@ -425,7 +444,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
         }
 }
 
-constexpr size_t kSmemCap = 200 * 1024;   // bytes of dynamic shared memory per CTA
+constexpr size_t kSmemCap = 226 * 1024;   // bytes of dynamic shared memory per CTA (227 KB max - static)
 constexpr int kWideCols = 40;              // QR / Jacobi problems with this many columns run on 1024 threads
 
 __global__ void permute_rows_kernel(const double* __restrict__ in, int64_t ldi, double* __restrict__ out,
@@ -560,13 +579,15 @@ void qr_direct(const std::vector<QrDesc>& d, cudaStream_t s) {
     }
 }
 
-// rows per TSQR chunk for an n-column problem (a chunk and its Q fit in smem)
-int tsqr_chunk_rows(int n) {
-    const int cap = int(kSmemCap / sizeof(double)) - 64;
-    int ch = cap / (2 * n);
+// rows per TSQR chunk for an n-column problem: the largest that keeps the chunk
+// (and its Q, when Q is wanted) in shared memory, at least 1.25 n so the stacked
+// R factors shrink level by level (below that the chunk runs from global memory)
+int tsqr_chunk_rows(int n, bool q) {
+    const int cap = int(kSmemCap / sizeof(double)) - n - 64;
+    int ch = cap / (q ? 2 * n : n);
     ch = std::min(ch, 1024);
     ch -= ch % 8;
-    return std::max(ch, 2 * n);   // >= 2n so the stacked R shrinks
+    return std::max(ch, n + (n + 3) / 4);
 }
 }  // namespace
 
@@ -574,7 +595,7 @@ void bqr(const std::vector<QrDesc>& d, cudaStream_t s) {
     std::vector<QrDesc> direct, tall;
     for (const QrDesc& q : d) {
         if (q.m <= 0 || q.n <= 0) continue;
-        if (q.m <= tsqr_chunk_rows(q.n)) direct.push_back(q);
+        if (q.m <= tsqr_chunk_rows(q.n, q.Q != nullptr)) direct.push_back(q);
         else tall.push_back(q);
     }
     qr_direct(direct, s);
@@ -591,7 +612,7 @@ void bqr(const std::vector<QrDesc>& d, cudaStream_t s) {
     for (const QrDesc& q : tall) {
         Plan p;
         p.q = q;
-        const int ch = tsqr_chunk_rows(q.n);
+        const int ch = tsqr_chunk_rows(q.n, q.Q != nullptr);
         for (int r0 = 0; r0 < q.m; r0 += ch) {
             const int rows = std::min(ch, q.m - r0);
             p.r0.push_back(r0);
@@ -644,14 +665,14 @@ void bqr(const std::vector<QrDesc>& d, cudaStream_t s) {
 void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     std::vector<SvdJob> sj, gj;
     size_t smax = 0, gtot = 0;
-    auto need = [](int r, int c) {   // doubles: M, V, norms, and the int selection order
+    auto need = [](int r, int c, bool v) {   // doubles: M, V (only when asked for), norms, the int selection order
         const size_t ce = size_t(c + (c & 1));
-        return size_t(r) * ce + ce * ce + ce + ce / 2;
+        return size_t(r) * ce + (v ? ce * ce : 0) + ce + ce / 2;
     };
     for (const SvdDesc& q : d) {
         if (q.rows <= 0 || q.cols <= 0) continue;
         SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr, q.U, q.ldu};
-        const size_t nd = need(q.rows, q.cols);
+        const size_t nd = need(q.rows, q.cols, q.V != nullptr);
         if (nd * sizeof(double) <= kSmemCap) {
             sj.push_back(j);
             smax = std::max(smax, nd);
@@ -672,7 +693,7 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
         for (const SvdJob& j : sj) {
             const int c = j.cols >= kWideCols ? 1 : 0;
             cls[c].push_back(j);
-            cmax[c] = std::max(cmax[c], need(j.rows, j.cols));
+            cmax[c] = std::max(cmax[c], need(j.rows, j.cols, j.V != nullptr));
         }
         for (int c = 0; c < 2; ++c) {
             if (cls[c].empty()) continue;
@@ -686,7 +707,7 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
         size_t off = 0;
         for (SvdJob& j : gj) {
             j.work = work.data() + off;
-            off += need(j.rows, j.cols);
+            off += need(j.rows, j.cols, j.V != nullptr);
         }
         DevVec<SvdJob> dj(gj, s);
         jacobi_kernel<false><<<unsigned(gj.size()), 256, 0, s>>>(dj.p);
@@ -789,11 +810,34 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
         first.push_back(cp[ci++]);
         if (q.P && q.c > q.m) last.push_back(cp[ci++]);
     }
+    static const bool trace = std::getenv("H2_TRACE_SVD") != nullptr;   // diagnostics: per-step times
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&]() {
+        H2B_CUDA(cudaStreamSynchronize(s));
+        const auto t = std::chrono::steady_clock::now();
+        const double ms = std::chrono::duration<double, std::milli>(t - t0).count();
+        t0 = t;
+        return ms;
+    };
+    double tq = 0, tj = 0, tc = 0;
+    if (trace) lap();
     bcopy(first, s);
+    if (trace) tc += lap();
     bqr(qrs, s);
+    if (trace) tq = lap();
     bcopy(last, s);
     bjacobi(svs, s);
+    if (trace) tj = lap();
     bgemm(gm, s);
+    if (trace && !d.empty()) {
+        int mm = 0, cm = 0;
+        for (const LeftSvdDesc& q : d) {
+            mm = std::max(mm, q.m);
+            cm = std::max(cm, q.c);
+        }
+        std::fprintf(stderr, "left_svd problems=%zu mmax=%d cmax=%d copy=%.3f qr=%.3f jacobi=%.3f\n", d.size(), mm, cm,
+                     tc, tq, tj);
+    }
     std::vector<SignJob> sg;
     for (const LeftSvdDesc& q : d)
         if (q.m > 0 && q.c > 0 && q.U) sg.push_back(SignJob{q.U, q.m, std::min(q.m, q.c), q.ldu});
@@ -806,3 +850,11 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
 
 }  // namespace la
 }  // namespace h2b
+
+// diagnostics hook: Jacobi sweeps / problems / problems that hit the sweep cap so far
+extern "C" int h2b_jacobi_stats(unsigned long long* out3) {
+    H2B_CUDA(cudaMemcpyFromSymbol(out3, h2b::la::g_jacobi_sweeps, sizeof(unsigned long long)));
+    H2B_CUDA(cudaMemcpyFromSymbol(out3 + 1, h2b::la::g_jacobi_problems, sizeof(unsigned long long)));
+    H2B_CUDA(cudaMemcpyFromSymbol(out3 + 2, h2b::la::g_jacobi_capped, sizeof(unsigned long long)));
+    return 0;
+}

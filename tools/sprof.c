@@ -1,7 +1,7 @@
 // Minimal sampling profiler for host code (no perf/gdb in this image).
 //   gcc -O2 -shared -fPIC -o tools/sprof.so tools/sprof.c -ldl
 //   LD_PRELOAD=tools/sprof.so SPROF_OUT=gpurun_out/sprof.txt python ...
-// Every 1 ms of process CPU time (ITIMER_PROF) the interrupted thread's stack is
+// Every 1 ms of process CPU time (ITIMER_PROF; SPROF_REAL=1: of wall time, ITIMER_REAL) the interrupted thread's stack is
 // captured with backtrace(); at exit each sample is written (to $SPROF_OUT.<pid>) as one line of
 // "object+offset" frames (innermost first). tools/sprof_report.py symbolizes
 // the offsets with addr2line and prints self / inclusive counts per function.
@@ -21,6 +21,7 @@ static void* g_frames[MAXS][DEPTH];
 static int g_depth[MAXS];
 static volatile int g_n = 0;
 static int g_on = 0;
+static int g_real = 0;
 
 static void on_prof(int sig) {
     (void)sig;
@@ -37,16 +38,19 @@ __attribute__((constructor)) static void sprof_init(void) {
     memset(&sa, 0, sizeof sa);
     sa.sa_handler = on_prof;
     sa.sa_flags = SA_RESTART;
-    sigaction(SIGPROF, &sa, NULL);
+    // SPROF_REAL=1: sample every 1 ms of WALL time (SIGALRM), so time blocked in
+    // synchronisations shows up too; default: every 1 ms of process CPU time
+    g_real = getenv("SPROF_REAL") != NULL;
+    sigaction(g_real ? SIGALRM : SIGPROF, &sa, NULL);
     struct itimerval it = {{0, 1000}, {0, 1000}};
-    setitimer(ITIMER_PROF, &it, NULL);
+    setitimer(g_real ? ITIMER_REAL : ITIMER_PROF, &it, NULL);
     g_on = 1;
 }
 
 __attribute__((destructor)) static void sprof_fini(void) {
     if (!g_on) return;
     struct itimerval off = {{0, 0}, {0, 0}};
-    setitimer(ITIMER_PROF, &off, NULL);
+    setitimer(g_real ? ITIMER_REAL : ITIMER_PROF, &off, NULL);
     int n = g_n < MAXS ? g_n : MAXS;
     if (n == 0) return;
     char path[4096];
