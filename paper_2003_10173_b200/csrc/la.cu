@@ -358,7 +358,66 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
     // the rounding-noise floor, whose rotations against large columns keep re-injecting noise)
     const double tol = fmax(1e-15, sqrt(double(r)) * 1.1102230246251565e-16);
     int sweep = 0;
-    for (; sweep < kJacobiSweeps && ce >= 2; ++sweep) {
+    // wide problems (>= 64 columns, 32 warps): a half-warp per pair, so 64 pairs rotate at once,
+    // and the column norms are carried through the rotations (alpha' = alpha - t gamma,
+    // beta' = beta + t gamma; exact again at every sweep start): one dot product per pair
+    const bool wide = ce >= 64 && nw == 32;
+    if (wide) {
+        const int grp = tid >> 4, gl = tid & 15, ng = blockDim.x >> 4;
+        const unsigned hm = lane < 16 ? 0x0000ffffu : 0xffff0000u;
+        for (; sweep < kJacobiSweeps; ++sweep) {
+            for (int j = warp; j < ce; j += nw) {
+                const double* mj = M + int64_t(j) * r;
+                double q = 0;
+                for (int i = lane; i < r; i += 32) q += mj[i] * mj[i];
+                q = warp_sum(q);
+                if (lane == 0) nrm[j] = q;
+            }
+            if (tid == 0) rotated = 0;
+            __syncthreads();
+            for (int round = 0; round < ce - 1; ++round) {
+                for (int p = grp; p < ce / 2; p += ng) {
+                    int a = p == 0 ? 0 : 1 + (p - 1 + round) % (ce - 1);
+                    int b = 1 + (ce - 2 - p + round) % (ce - 1);
+                    if (a > b) { const int x = a; a = b; b = x; }
+                    double* ma = M + int64_t(a) * r;
+                    double* mb = M + int64_t(b) * r;
+                    double ga = 0;
+                    for (int i = gl; i < r; i += 16) ga += ma[i] * mb[i];
+#pragma unroll
+                    for (int o = 8; o >= 1; o >>= 1) ga += __shfl_xor_sync(hm, ga, o);
+                    const double al = nrm[a], be = nrm[b];
+                    if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+                    const double zeta = (be - al) / (2.0 * ga);
+                    const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+                    for (int i = gl; i < r; i += 16) {
+                        const double x = ma[i], y = mb[i];
+                        ma[i] = cs * x - sn * y;
+                        mb[i] = sn * x + cs * y;
+                    }
+                    if (jb.V) {
+                        double* va = V + int64_t(a) * ce;
+                        double* vb = V + int64_t(b) * ce;
+                        for (int i = gl; i < ce; i += 16) {
+                            const double x = va[i], y = vb[i];
+                            va[i] = cs * x - sn * y;
+                            vb[i] = sn * x + cs * y;
+                        }
+                    }
+                    if (gl == 0) {
+                        nrm[a] = fmax(al - t * ga, 0.0);
+                        nrm[b] = be + t * ga;
+                        rotated = 1;
+                    }
+                }
+                __syncthreads();
+            }
+            if (!rotated) break;
+            __syncthreads();
+        }
+    }
+    for (; !wide && sweep < kJacobiSweeps && ce >= 2; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int round = 0; round < ce - 1; ++round) {
