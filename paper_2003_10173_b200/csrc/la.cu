@@ -632,8 +632,12 @@ void qr_direct(const std::vector<QrDesc>& d, cudaStream_t s) {
             j.work = work.data() + off;
             off += qr_doubles(j.m, j.n, j.Q != nullptr);
         }
+        // problems too large for shared memory: 32 warps when they are wide (the working set
+        // stays in L2; the column updates are spread over more warps)
+        int nmax = 0;
+        for (const QrJob& j : gj) nmax = std::max(nmax, j.n);
         DevVec<QrJob> dj(gj, s);
-        qr_kernel<false><<<unsigned(gj.size()), 256, 0, s>>>(dj.p);
+        qr_kernel<false><<<unsigned(gj.size()), nmax >= kWideCols ? 1024 : 256, 0, s>>>(dj.p);
         H2B_LAUNCH();
     }
 }
@@ -769,7 +773,9 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
             off += need(j.rows, j.cols, j.V != nullptr);
         }
         DevVec<SvdJob> dj(gj, s);
-        jacobi_kernel<false><<<unsigned(gj.size()), 256, 0, s>>>(dj.p);
+        int cmx = 0;
+        for (const SvdJob& j : gj) cmx = std::max(cmx, j.cols);
+        jacobi_kernel<false><<<unsigned(gj.size()), cmx >= kWideCols ? 1024 : 256, 0, s>>>(dj.p);
         H2B_LAUNCH();
     }
 }
