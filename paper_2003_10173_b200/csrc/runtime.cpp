@@ -87,7 +87,7 @@ void* stage_to_device(const void* host, size_t bytes, void* dev_dst, cudaStream_
     return staging().put(host, bytes, dev_dst, s);
 }
 
-void Staging_stats(long long* puts, long long* wraps) {
+void staging_stats(long long* puts, long long* wraps) {
     Staging& st = staging();
     std::lock_guard<std::mutex> g(st.mu);
     if (puts) *puts = static_cast<long long>(st.puts);
@@ -102,6 +102,6 @@ const void* stage_descriptors(const void* host, size_t bytes, cudaStream_t s) {
 
 // diagnostics hook: uploads through the staging ring and ring wraps (device syncs) so far
 extern "C" int h2b_staging_stats(long long* puts, long long* wraps) {
-    h2b::Staging_stats(puts, wraps);
+    h2b::staging_stats(puts, wraps);
     return 0;
 }
