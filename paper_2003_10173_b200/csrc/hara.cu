@@ -408,8 +408,12 @@ Truncation truncation_bases(const H2Dev& g, bool row_side, double eps, double le
                                       ld1(kpar), k, 0, 0, 1.0, 0.0});
                 at += pc[size_t(par)];
             }
+            // columns 1000x below the smallest possible truncation threshold
+            // (tau = eps sigma_0 / level_corr >= eps ||G||_F / (sqrt(min(k, c)) level_corr)) are
+            // discarded, so the SVD need not converge among them (eps = 0: no such columns)
+            const double skip = 1e-3 * eps / (std::sqrt(double(std::min(k, c))) * level_corr);
             sv.push_back(LeftSvdDesc{Gv, k, c, k, U.at(size_t(v)), k, sg.at(size_t(v)),
-                                     c > k ? P.at(size_t(v)) : nullptr, k});
+                                     c > k ? P.at(size_t(v)) : nullptr, k, skip});
         }
         const auto tl = Clock::now();
         bcopy(cp, s);

@@ -326,11 +326,13 @@ struct SvdJob {
     double* work;
     double* U;
     int ldu;
+    double skip_rel;
 };
 
 constexpr int kJacobiSweeps = 30;
 // diagnostics: sweeps run and problems solved by jacobi_kernel (h2b_jacobi_stats)
 __device__ unsigned long long g_jacobi_sweeps = 0, g_jacobi_problems = 0, g_jacobi_capped = 0;
+__device__ unsigned long long g_jacobi_wide_sweeps = 0, g_jacobi_wide_problems = 0;   // >= 64 columns
 
 template <bool SMEM>
 __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__ jobs) {
@@ -357,6 +359,16 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
     // kJacobiSweeps sweeps (dgesvj's NSWEEP: the columns still rotating by then are the ones at
     // the rounding-noise floor, whose rotations against large columns keep re-injecting noise)
     const double tol = fmax(1e-15, sqrt(double(r)) * 1.1102230246251565e-16);
+    // pairs whose columns are both below skip_rel ||M||_F (discarded by the caller) keep rotating
+    // while sweeps run but do not keep the sweeps going: their rotations against each other and
+    // against large columns re-inject rounding noise, so they may never meet tol
+    double floor2 = 0;
+    if (jb.skip_rel > 0) {
+        __shared__ double fro_red[33];
+        double fpart = 0;
+        for (int64_t e = tid; e < int64_t(r) * ce; e += blockDim.x) fpart += M[e] * M[e];
+        floor2 = jb.skip_rel * jb.skip_rel * block_sum(fpart, fro_red);
+    }
     int sweep = 0;
     // wide problems (>= 64 columns, 32 warps): a half-warp per pair, so 64 pairs rotate at once,
     // and the column norms are carried through the rotations (alpha' = alpha - t gamma,
@@ -408,7 +420,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
                     if (gl == 0) {
                         nrm[a] = fmax(al - t * ga, 0.0);
                         nrm[b] = be + t * ga;
-                        rotated = 1;
+                        if (fmax(al, be) > floor2) rotated = 1;
                     }
                 }
                 __syncthreads();
@@ -438,7 +450,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
                 be = warp_sum(be);
                 ga = warp_sum(ga);
                 if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
-                if (lane == 0) rotated = 1;
+                if (lane == 0 && fmax(al, be) > floor2) rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
@@ -466,6 +478,10 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
         atomicAdd(&g_jacobi_sweeps, (unsigned long long)(sweep + 1));
         atomicAdd(&g_jacobi_problems, 1ull);
         if (sweep == kJacobiSweeps) atomicAdd(&g_jacobi_capped, 1ull);
+        if (wide) {
+            atomicAdd(&g_jacobi_wide_sweeps, (unsigned long long)(sweep + 1));
+            atomicAdd(&g_jacobi_wide_problems, 1ull);
+        }
     }
     for (int j = warp; j < c; j += nw) {
         const double* mj = M + int64_t(j) * r;
@@ -734,7 +750,7 @@ void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s) {
     };
     for (const SvdDesc& q : d) {
         if (q.rows <= 0 || q.cols <= 0) continue;
-        SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr, q.U, q.ldu};
+        SvdJob j{q.A, q.rows, q.cols, q.lda, q.trans, q.sigma, q.V, q.ldv, nullptr, q.U, q.ldu, q.skip_rel};
         const size_t nd = need(q.rows, q.cols, q.V != nullptr);
         if (nd * sizeof(double) <= kSmemCap) {
             sj.push_back(j);
@@ -855,7 +871,7 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
             qrs.push_back(QrDesc{At, q.c, q.m, q.c, R, p, nullptr, 0});
             // one-sided Jacobi on R^T (converges in far fewer sweeps than on R); its
             // normalised rotated columns are the right singular vectors of R = left of A
-            svs.push_back(SvdDesc{R, p, p, p, 1, q.sigma, nullptr, 0, q.U, q.ldu});
+            svs.push_back(SvdDesc{R, p, p, p, 1, q.sigma, nullptr, 0, q.U, q.ldu, q.skip_rel});
             if (q.P && q.c > q.m) cp.push_back(CopyDesc{R, q.P, p, p, p, q.ldp, 1});
         } else {
             double* Q = qb.data() + qo;
@@ -863,7 +879,7 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
             double* V = vb.data() + vo;
             vo += size_t(p) * p;
             qrs.push_back(QrDesc{q.A, q.m, q.c, q.lda, R, p, Q, q.m});
-            svs.push_back(SvdDesc{R, p, p, p, 1, q.sigma, V, p});
+            svs.push_back(SvdDesc{R, p, p, p, 1, q.sigma, V, p, nullptr, 0, q.skip_rel});
             gm.push_back(GemmDesc{Q, V, q.U, q.m, p, p, q.m, p, q.ldu, 0, 0, 1.0, 0.0});
         }
     }
@@ -916,10 +932,64 @@ void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s) {
 }  // namespace la
 }  // namespace h2b
 
-// diagnostics hook: Jacobi sweeps / problems / problems that hit the sweep cap so far
+// diagnostics hook: Jacobi sweeps / problems / problems that hit the sweep cap, and sweeps /
+// problems of the wide (>= 64 columns) ones, so far (5 counters)
 extern "C" int h2b_jacobi_stats(unsigned long long* out3) {
     H2B_CUDA(cudaMemcpyFromSymbol(out3, h2b::la::g_jacobi_sweeps, sizeof(unsigned long long)));
     H2B_CUDA(cudaMemcpyFromSymbol(out3 + 1, h2b::la::g_jacobi_problems, sizeof(unsigned long long)));
     H2B_CUDA(cudaMemcpyFromSymbol(out3 + 2, h2b::la::g_jacobi_capped, sizeof(unsigned long long)));
+    H2B_CUDA(cudaMemcpyFromSymbol(out3 + 3, h2b::la::g_jacobi_wide_sweeps, sizeof(unsigned long long)));
+    H2B_CUDA(cudaMemcpyFromSymbol(out3 + 4, h2b::la::g_jacobi_wide_problems, sizeof(unsigned long long)));
+    return 0;
+}
+
+namespace {
+// diagnostics: a deterministic graded upper-triangular test matrix (entry (i, j) for i <= j is
+// a hash in [-1, 1] times 10^(-12 j / n): singular values spread over 12 decades)
+__global__ void bench_fill_kernel(double* a, int n, int nprob) {
+    const int64_t tot = int64_t(n) * n * nprob;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < tot; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = e % (int64_t(n) * n);
+        const int i = int(q % n), j = int(q / n);
+        uint64_t h = uint64_t(e) * 0x9E3779B97F4A7C15ull;
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        const double u = double(h >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+        a[e] = i <= j ? u * pow(10.0, -12.0 * j / n) : 0.0;
+    }
+}
+}  // namespace
+
+// diagnostics hook: time bjacobi on nprob graded n x n upper-triangular problems (op = A^T when
+// trans, left vectors only, like the truncation SVDs); returns ms per call over `reps` calls
+extern "C" int h2b_bench_jacobi(int n, int nprob, int trans, int reps, double* ms) {
+    using namespace h2b;
+    double *a = nullptr, *sg = nullptr, *u = nullptr;
+    H2B_CUDA(cudaMalloc(&a, sizeof(double) * n * n * nprob));
+    H2B_CUDA(cudaMalloc(&sg, sizeof(double) * n * nprob));
+    H2B_CUDA(cudaMalloc(&u, sizeof(double) * n * n * nprob));
+    bench_fill_kernel<<<1024, 256>>>(a, n, nprob);
+    std::vector<la::SvdDesc> d;
+    for (int p = 0; p < nprob; ++p)
+        d.push_back(la::SvdDesc{a + int64_t(p) * n * n, n, n, n, trans, sg + int64_t(p) * n, nullptr, 0,
+                                u + int64_t(p) * n * n, n});
+    la::bjacobi(d, nullptr);
+    H2B_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) la::bjacobi(d, nullptr);
+    cudaEventRecord(e1);
+    H2B_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms = double(t) / std::max(reps, 1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(a);
+    cudaFree(sg);
+    cudaFree(u);
     return 0;
 }

@@ -108,6 +108,9 @@ struct SvdDesc {
     int ldv;
     double* U = nullptr;   // optional: left singular vectors, the normalised rotated columns (rows x cols)
     int ldu = 0;
+    // convergence is judged only on pairs with a column above skip_rel * ||A||_F (the caller
+    // discards everything below it); pairs below are still rotated while sweeps run. 0 = all pairs
+    double skip_rel = 0;
 };
 void bjacobi(const std::vector<SvdDesc>& d, cudaStream_t s);
 
@@ -122,6 +125,7 @@ struct LeftSvdDesc {
     double* sigma;
     double* P;    // optional (only written when c > m)
     int ldp;
+    double skip_rel = 0;   // see SvdDesc::skip_rel
 };
 void bleft_svd(const std::vector<LeftSvdDesc>& d, cudaStream_t s);
 

@@ -23,7 +23,7 @@ cfg = dict(bench.CONFIGS["cfg5"])
 o, a0, X = bench.inversion_problem(a.surface, cfg)
 pc = PeelConfig(eps=cfg["eps"], rng=1)
 bench.inversion_step(a0, X, cfg, pc)   # warm-up
-st0 = (C.c_ulonglong * 3)()
+st0 = (C.c_ulonglong * 5)()
 lib.h2b_jacobi_stats(st0)
 lib.h2b_hara_phase_reset()
 lib.h2b_plan_build_ms.restype = C.c_double
@@ -38,7 +38,8 @@ print(f"surface{a.surface}: wall {wall:.3f} s, steps {t}, iterations {len(res.tr
 for i, nm in enumerate(NAMES):
     print(f"  {nm:18s} {ph[i] / 1e3:8.3f} s")
 print(f"  hgemv plan builds  {lib.h2b_plan_build_ms(1) / 1e3:8.3f} s")
-st1 = (C.c_ulonglong * 3)()
+st1 = (C.c_ulonglong * 5)()
 lib.h2b_jacobi_stats(st1)
-sw, pr, cap = (st1[i] - st0[i] for i in range(3))
-print(f"  jacobi: {pr} problems, {sw / max(pr, 1):.2f} sweeps on average, {cap} hit the sweep cap")
+sw, pr, cap, wsw, wpr = (st1[i] - st0[i] for i in range(5))
+print(f"  jacobi: {pr} problems, {sw / max(pr, 1):.2f} sweeps on average, {cap} hit the sweep cap; "
+      f"{wpr} with >= 64 columns: {wsw / max(wpr, 1):.2f} sweeps on average")
