@@ -433,15 +433,18 @@ def run_b200(args, cfg, world, rank, local, dist):
         # one plan (own workspace and exchange buffers) per rotating stream
         from paper_2003_10173_b200.dist import ShardedHgemv
         shs = [sharded] + [ShardedHgemv(m, transport=args.transport, max_b=b) for _ in range(2)]
-    yps = [torch.empty_like(xp).pin_memory() for _ in range(3)]
-    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    # rotating streams of the e2e leg (measured on cfg2: 2 -> 7.86, 3 -> 6.03-6.29, 4 -> 5.95-6.02,
+    # 6 -> 6.04-6.07 ms per step; tools/ab/e2e_streams.py)
+    NS = 4 if sharded is None else 3
+    yps = [torch.empty_like(xp).pin_memory() for _ in range(NS)]
+    streams = [torch.cuda.Stream(dev) for _ in range(NS)]
 
     def e2e_step(i):
         if sharded is None:
-            # pipelined public API: step i on stream i % 3, so its H2D / D2H overlap the
+            # pipelined public API: step i on stream i % NS, so its H2D / D2H overlap the
             # neighbouring steps' hgemv (per-stream workspaces inside the library)
-            check(lib.h2c_matvec_host_async(m._h, 0, 0, n, b, xp.data_ptr(), yps[i % 3].data_ptr(),
-                                            streams[i % 3].cuda_stream))
+            check(lib.h2c_matvec_host_async(m._h, 0, 0, n, b, xp.data_ptr(), yps[i % NS].data_ptr(),
+                                            streams[i % NS].cuda_stream))
         else:
             # each rank's slice of x / y (its owned rows, cluster order) lives in pinned host memory;
             # step i on stream i % 3 with its own plan, so copies overlap the neighbouring steps
@@ -473,7 +476,7 @@ def run_b200(args, cfg, world, rank, local, dist):
 
     # warm-up: three calls per stream (eager, graph capture, first replay), so the timed
     # region replays captured graphs on every stream
-    tw = e2e_run(9 if sharded is None else 6)
+    tw = e2e_run(3 * NS if sharded is None else 6)
     if dist:
         dist.barrier()
     ke = max(4, min(args.steps, 20))
@@ -494,7 +497,7 @@ def run_b200(args, cfg, world, rank, local, dist):
     io_rows = n if sharded is None else sharded.plan.owned_rows * world
     e2e = {"value": F / te / 1e9, "unit": "GFLOP/s", "ms_per_step": te * 1e3,
            "h2d_bytes_per_step": 8 * io_rows * b, "d2h_bytes_per_step": 8 * io_rows * b,
-           "path": ("h2c_matvec_host_async on 3 rotating streams: per step pinned host x -> HBM, hgemv, "
+           "path": ("h2c_matvec_host_async on 4 rotating streams: per step pinned host x -> HBM, hgemv, "
                     "HBM -> pinned host y (copies of one step overlap the hgemv of the next)") if sharded is None else
                    "per rank, 3 rotating streams with a plan each: its owned rows of x (pinned host, cluster order) "
                    "-> HBM, sharded hgemv (NCCL all-to-all overlapped with the local near field), owned rows of y "
