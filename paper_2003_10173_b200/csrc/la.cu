@@ -389,8 +389,13 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
             __syncthreads();
             for (int round = 0; round < ce - 1; ++round) {
                 for (int p = grp; p < ce / 2; p += ng) {
-                    int a = p == 0 ? 0 : 1 + (p - 1 + round) % (ce - 1);
-                    int b = 1 + (ce - 2 - p + round) % (ce - 1);
+                    // tournament pairing; the indices stay below 2 (ce - 1), so one conditional
+                    // subtraction replaces the integer modulo
+                    int a = p - 1 + round, b = ce - 2 - p + round;
+                    if (a >= ce - 1) a -= ce - 1;
+                    if (b >= ce - 1) b -= ce - 1;
+                    a = p == 0 ? 0 : a + 1;
+                    b += 1;
                     if (a > b) { const int x = a; a = b; b = x; }
                     double* ma = M + int64_t(a) * r;
                     double* mb = M + int64_t(b) * r;
@@ -399,10 +404,12 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
 #pragma unroll
                     for (int o = 8; o >= 1; o >>= 1) ga += __shfl_xor_sync(hm, ga, o);
                     const double al = nrm[a], be = nrm[b];
-                    if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+                    // |gamma| <= tol sqrt(alpha beta), squared (no square root); the rotation
+                    // needs one division, one square root and one reciprocal square root
+                    if (ga == 0.0 || ga * ga <= tol * tol * (al * be)) continue;
                     const double zeta = (be - al) / (2.0 * ga);
-                    const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+                    const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                    const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
                     for (int i = gl; i < r; i += 16) {
                         const double x = ma[i], y = mb[i];
                         ma[i] = cs * x - sn * y;
