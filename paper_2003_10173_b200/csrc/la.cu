@@ -242,28 +242,57 @@ __global__ void __launch_bounds__(1024) qr_kernel(const QrJob* __restrict__ jobs
         W[e] = jb.A[i + int64_t(j) * jb.lda];
     }
     __syncthreads();
+    // 32-warp configuration (wide problems): warp 0 alone forms each reflector (norm by a warp
+    // reduction, no block-wide sum), one barrier publishes it, one closes the column's update
+    const bool warp_reflector = nw == 32;
     for (int j = 0; j < kp; ++j) {
         double* cj = W + int64_t(j) * m;
-        double part = 0;
-        for (int i = j + 1 + tid; i < m; i += blockDim.x) part += cj[i] * cj[i];
-        const double tail = block_sum(part, red);
-        const double c0 = cj[j];
-        double t, inv = 0, beta = c0;
-        if (tail <= DBL_MIN) {
-            t = 0;
+        double t;
+        if (warp_reflector) {
+            if (warp == 0) {
+                double part = 0;
+                for (int i = j + 1 + lane; i < m; i += 32) part += cj[i] * cj[i];
+                const double tail = warp_sum(part);
+                const double c0 = cj[j];
+                double tt, inv = 0, beta = c0;
+                if (tail <= DBL_MIN) {
+                    tt = 0;
+                } else {
+                    beta = sqrt(c0 * c0 + tail);
+                    if (c0 >= 0) beta = -beta;
+                    inv = 1.0 / (c0 - beta);
+                    tt = (beta - c0) / beta;
+                }
+                for (int i = j + 1 + lane; i < m; i += 32) cj[i] = tt == 0 ? 0.0 : cj[i] * inv;
+                if (lane == 0) {
+                    cj[j] = beta;
+                    tau[j] = tt;
+                }
+            }
+            __syncthreads();
+            t = tau[j];
         } else {
-            beta = sqrt(c0 * c0 + tail);
-            if (c0 >= 0) beta = -beta;
-            inv = 1.0 / (c0 - beta);
-            t = (beta - c0) / beta;
+            double part = 0;
+            for (int i = j + 1 + tid; i < m; i += blockDim.x) part += cj[i] * cj[i];
+            const double tail = block_sum(part, red);
+            const double c0 = cj[j];
+            double inv = 0, beta = c0;
+            if (tail <= DBL_MIN) {
+                t = 0;
+            } else {
+                beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0) beta = -beta;
+                inv = 1.0 / (c0 - beta);
+                t = (beta - c0) / beta;
+            }
+            __syncthreads();
+            for (int i = j + 1 + tid; i < m; i += blockDim.x) cj[i] = t == 0 ? 0.0 : cj[i] * inv;
+            if (tid == 0) {
+                cj[j] = beta;
+                tau[j] = t;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        for (int i = j + 1 + tid; i < m; i += blockDim.x) cj[i] = t == 0 ? 0.0 : cj[i] * inv;
-        if (tid == 0) {
-            cj[j] = beta;
-            tau[j] = t;
-        }
-        __syncthreads();
         if (t != 0) {
             for (int c = j + 1 + warp; c < n; c += nw) {
                 double* cc = W + int64_t(c) * m;
