@@ -470,9 +470,12 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
         __syncthreads();
         for (int round = 0; round < ce - 1; ++round) {
             for (int p = warp; p < ce / 2; p += nw) {
-                // tournament pairing: fixed element 0, others rotate
-                int a = p == 0 ? 0 : 1 + (p - 1 + round) % (ce - 1);
-                int b = 1 + (ce - 2 - p + round) % (ce - 1);
+                // tournament pairing: fixed element 0, others rotate (modulo-free, as above)
+                int a = p - 1 + round, b = ce - 2 - p + round;
+                if (a >= ce - 1) a -= ce - 1;
+                if (b >= ce - 1) b -= ce - 1;
+                a = p == 0 ? 0 : a + 1;
+                b += 1;
                 if (a > b) { const int x = a; a = b; b = x; }
                 double* ma = M + int64_t(a) * r;
                 double* mb = M + int64_t(b) * r;
@@ -485,11 +488,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
                 al = warp_sum(al);
                 be = warp_sum(be);
                 ga = warp_sum(ga);
-                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+                if (ga == 0.0 || ga * ga <= tol * tol * (al * be)) continue;
                 if (lane == 0 && fmax(al, be) > floor2) rotated = 1;
                 const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+                const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
                 for (int i = lane; i < r; i += 32) {
                     const double x = ma[i], y = mb[i];
                     ma[i] = cs * x - sn * y;
