@@ -657,6 +657,41 @@ def hara_operator(cfg, n):
     return H2Operator(src), bt, src
 
 
+def hara_roofline():
+    """The construction's batched kernels from their committed ncu captures (not live: one
+    capture per kernel, tools/round_evidence.sh). They are small batched problems, latency-bound;
+    the build is bounded by the black-box operator and the per-panel decisions."""
+    import re
+    out = {"bound": "tensor", "unit": "TFLOP/s", "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
+           "live": False, "per_kernel": []}
+    for k in ("bgemm_kernel", "qr_kernel", "jacobi_kernel"):
+        f = os.path.join(ROOT, "profiles", "r02", f"ncu_full_hara_{k}_r02.txt")
+        if not os.path.exists(f):
+            continue
+        txt = open(f).read()
+
+        def num(name, txt=txt):
+            m = re.search(re.escape(name) + r"\s*=\s*([0-9.eE+-]+)\s*(\S*)", txt)
+            return (float(m.group(1)), m.group(2)) if m else (None, "")
+        dur, du = num("gpu__time_duration.sum")
+        sec = dur * {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}.get(du, 1e-6) if dur else None
+        ops, _ = num("sm__ops_path_tensor_src_fp64.sum")
+        fp64, _ = num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+        dmma, _ = num("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active")
+        grid, _ = num("launch__grid_size")
+        ent = {"kernel": k, "duration_us": None if sec is None else sec * 1e6, "grid": grid,
+               "dmma_pipe_active_pct": dmma, "fp64_pipe_active_pct": fp64, "source": os.path.relpath(f, ROOT)}
+        if ops and sec:
+            ent["achieved_tflops"] = ops / sec / 1e12
+            ent["frac"] = ent["achieved_tflops"] / FP64_PEAK_TFLOPS
+        out["per_kernel"].append(ent)
+    if out["per_kernel"] and "achieved_tflops" in out["per_kernel"][0]:
+        out["kernel"] = "bgemm_kernel (the construction's DMMA batched GEMM)"
+        out["achieved"] = out["per_kernel"][0]["achieved_tflops"]
+        out["frac"] = out["per_kernel"][0]["frac"]
+    return out
+
+
 def run_hara(args, cfg, world, rank, local, dist):
     """cfg3: HARA build time on the B200 (one step = one peel_construct)."""
     import torch
@@ -678,7 +713,9 @@ def run_hara(args, cfg, world, rank, local, dist):
     _l.h2b_plan_build_ms.argtypes = [C.c_int]
     _l.h2b_plan_sync_ms.restype = C.c_double
     _l.h2b_plan_sync_ms.argtypes = [C.c_int]
-    times, opms = [], []
+    _l.h2b_kernel_launches.restype = C.c_longlong
+    _l.h2b_kernel_launches.argtypes = [C.c_int]
+    times, opms, launches = [], [], []
     with ClockSampler(local) as clk:
         for _ in range(steps):
             op.reset_counter()
@@ -686,10 +723,12 @@ def run_hara(args, cfg, world, rank, local, dist):
             _l.h2b_plan_build_ms(1)
             _l.h2b_plan_sync_ms(1)
             _l.h2b_plan_parts_ms((C.c_double * 4)(), 1)
+            _l.h2b_kernel_launches(1)
             t0 = time.perf_counter()
             res = peel_construct(op, bt, pc)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
+            launches.append(int(_l.h2b_kernel_launches(0)))
             opms.append(res.op_ms)
     t = statistics.median(times)
     if dist:
@@ -735,6 +774,9 @@ def run_hara(args, cfg, world, rank, local, dist):
            "hara": {"op_s": statistics.median(opms) / 1e3, "construction_s": t - statistics.median(opms) / 1e3,
                     "samples": res.stats.total, "relative_error_2norm": err, "rank_profile": prof,
                     "level_samples": [lv.samples for lv in res.stats.levels], "phases_s": phases},
+           "gpu_launches": int(statistics.median(launches)) * steps,
+           "gpu_launches_per_build": int(statistics.median(launches)),
+           "roofline": hara_roofline(),
            "clocks": clk.summary()}
     if cfg.get("pde"):
         out["hara"]["pde_solves"] = keep.diffusion.pde_solves()
@@ -798,10 +840,16 @@ def run_inversion(args, cfg, world, rank, local, dist):
     n = o.op.dim()
     pc = PeelConfig(eps=cfg["eps"], rng=1)
     inversion_step(a0, X, cfg, pc)
-    times = []
+    import ctypes as C
+    from paper_2003_10173_b200._lib import lib as _l
+    _l.h2b_kernel_launches.restype = C.c_longlong
+    _l.h2b_kernel_launches.argtypes = [C.c_int]
+    times, launches = [], []
     with ClockSampler(local) as clk:
         for _ in range(max(1, min(args.steps, 2))):
+            _l.h2b_kernel_launches(1)
             t, res, au = inversion_step(a0, X, cfg, pc)
+            launches.append(int(_l.h2b_kernel_launches(0)))
             times.append(t)
     tot = [sum(t.values()) for t in times]
     i = int(np.argsort(tot)[len(tot) // 2])
@@ -819,6 +867,7 @@ def run_inversion(args, cfg, world, rank, local, dist):
                           "samples": res.trace.total_samples(),
                           "rows": [(r.iter, r.residual, r.eps_k, r.samples, round(r.wall_seconds, 4)) for r in rows],
                           "rank_profile": [int(v) for v in res.X.rank_profile()], "setup_s": setup},
+            "gpu_launches": int(sum(launches)), "gpu_launches_per_step": launches,
             "clocks": clk.summary()}
 
 

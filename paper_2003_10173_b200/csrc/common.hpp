@@ -4,6 +4,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -30,8 +31,15 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
         throw cuda_error(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " at " + file + ":" +
                          std::to_string(line));
 }
+// kernel launches issued so far (diagnostics for bench.py's gpu_launches): every H2B_LAUNCH
+// counts one, except while a CUDA graph is being captured; graph replays add their kernel nodes
+extern std::atomic<long long> g_kernel_launches;
+extern thread_local bool t_capturing;
+inline void note_launch(long long k = 1) {
+    if (!t_capturing) g_kernel_launches.fetch_add(k, std::memory_order_relaxed);
+}
 #define H2B_CUDA(x) ::h2b::cuda_check((x), #x, __FILE__, __LINE__)
-#define H2B_LAUNCH() ::h2b::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define H2B_LAUNCH() (::h2b::note_launch(), ::h2b::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__))
 
 // Device allocations come from the device's stream-ordered memory pool
 // (cudaMallocAsync / cudaFreeAsync) with the release threshold raised, so the

@@ -86,6 +86,7 @@ struct HgemvGraph {
     // priority) beside the sweep chain on `hi` (greatest priority)
     cudaStream_t hi = nullptr, lo = nullptr;
     int greatest = 0;     // numeric value of the greatest stream priority
+    long long kernels = 0;   // kernel nodes of exec (launch accounting of replays)
     int prio_mode = 0;    // last hgemv_impl: 1 few-vector overlap, 2 top chain (graph node priorities)
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ~HgemvGraph() {

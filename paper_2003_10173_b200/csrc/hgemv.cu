@@ -1789,6 +1789,7 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     k.knobs = knob_signature();
     if (g.exec && g.key == k) {
         H2B_CUDA(cudaGraphLaunch(g.exec, stream));
+        note_launch(g.kernels);
         return;
     }
     if (!g_tune[3] || !(g.last == k)) {   // first call with these arguments: run eagerly
@@ -1804,14 +1805,29 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     if (!g.cap) H2B_CUDA(cudaStreamCreateWithFlags(&g.cap, cudaStreamNonBlocking));
     cudaGraph_t graph = nullptr;
     H2B_CUDA(cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal));
+    t_capturing = true;   // captured launches are counted when the graph replays
     try {
         hgemv_impl(h, transpose, user_order, n, b, x, ldx, y, ldy, alpha, beta, g.cap, ws, nullptr);
     } catch (...) {
+        t_capturing = false;
         cudaStreamEndCapture(g.cap, &graph);
         if (graph) cudaGraphDestroy(graph);
         throw;
     }
+    t_capturing = false;
     H2B_CUDA(cudaStreamEndCapture(g.cap, &graph));
+    {
+        size_t nn = 0;
+        H2B_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        H2B_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        g.kernels = 0;
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            H2B_CUDA(cudaGraphNodeGetType(nd, &ty));
+            if (ty == cudaGraphNodeTypeKernel) ++g.kernels;
+        }
+    }
     unsigned long long iflags = 0;
     if (g.prio_mode == 1) {   // keep the overlapped few-vector path's priorities inside the graph
         set_node_priorities(graph);
@@ -1823,6 +1839,7 @@ void hgemv(const H2Dev& h, bool transpose, bool user_order, int64_t n, int64_t b
     cudaGraphDestroy(graph);
     g.key = k;
     H2B_CUDA(cudaGraphLaunch(g.exec, stream));
+    note_launch(g.kernels);
 }
 
 namespace {

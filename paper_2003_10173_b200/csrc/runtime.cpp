@@ -8,6 +8,9 @@
 
 namespace h2b {
 
+std::atomic<long long> g_kernel_launches{0};
+thread_local bool t_capturing = false;
+
 void ensure_mem_pool() {
     static std::mutex mu;
     static std::unordered_set<int> done;
@@ -104,4 +107,9 @@ const void* stage_descriptors(const void* host, size_t bytes, cudaStream_t s) {
 extern "C" int h2b_staging_stats(long long* puts, long long* wraps) {
     h2b::staging_stats(puts, wraps);
     return 0;
+}
+
+// diagnostics hook: kernel launches so far (H2B_LAUNCH sites + replayed graph kernel nodes)
+extern "C" long long h2b_kernel_launches(int reset) {
+    return reset ? h2b::g_kernel_launches.exchange(0) : h2b::g_kernel_launches.load();
 }
