@@ -884,6 +884,7 @@ struct HgemvPlan {
     // stage 5 split: the near field (5d) writes blocked partial sums to the
     // workspace's ypart, the leaf expansion (5u) adds them in its epilogue
     bool split = false;
+    bool small_ypart = false;   // few-vector plan: the dense slot sums go to ypart (leaf expansion adds them)
     int chain_level = 0;      // > 0: levels above it form the top chain (LaunchDesc::chain)
     int chain_nodes = 0;      // g_chain_nodes the plan was built with
     std::once_flag accounted;
@@ -1314,6 +1315,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
     // adds ypart in its epilogue before the single user-order scatter
     split = split && !small;
     plan->split = split;
+    long leaf_exp = -1;   // few-vector plans: index of the leaf-expansion launch (moved last below)
     {
         auto near_here = [&](int src) { return split && (!ds || ds->owner[size_t(src)] == ds->rank); };
         EntryCsr by_leaf(nn), by_near(nn);
@@ -1380,6 +1382,7 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
         const size_t nl = pb.launches.size();
         pb.emit(outs, by_leaf.pool, kModeY, 3, 5);
         if (split && pb.launches.size() > nl) pb.launches.back().yadd = true;
+        if (small && pb.launches.size() > nl) leaf_exp = long(pb.launches.size()) - 1;
     }
     if (small) {
         std::vector<int> lv, lr;
@@ -1398,6 +1401,16 @@ std::shared_ptr<HgemvPlan> build_plan(const H2Dev& h, bool transpose, const Dist
                    (reinterpret_cast<uintptr_t>(sb.A) % 16) == 0;
         }
         plan->sym64 = ok64;
+        // the dense slot sums (kind 4) write blocked partial sums (ypart) right after the
+        // dense pass, on its stream; the leaf expansion runs last and adds them in its
+        // epilogue (yadd), so the chain never waits for the slot sums
+        if (leaf_exp >= 0) {
+            LaunchDesc le = pb.launches[size_t(leaf_exp)];
+            pb.launches.erase(pb.launches.begin() + leaf_exp);
+            le.yadd = true;
+            pb.launches.push_back(le);
+            plan->small_ypart = true;
+        }
         plan->sym_blocks.upload(sblocks);
         plan->csr_units.upload(sunits);
         plan->csr_slots.upload(sslots);
@@ -1744,7 +1757,7 @@ void reserve_workspace(const HgemvPlan& plan, int64_t n, int64_t b, cudaStream_t
     if (ws.yhat.size() < std::max<size_t>(need_d, 1)) ws.yhat.resize(std::max<size_t>(need_d, 1), stream);
     if (plan.scratch_rows > 0 && ws.scratch.size() < size_t(plan.scratch_rows * b))
         ws.scratch.resize(size_t(plan.scratch_rows * b), stream);
-    if (plan.split && ws.ypart.size() < need_x) ws.ypart.resize(need_x, stream);
+    if ((plan.split || plan.small_ypart) && ws.ypart.size() < need_x) ws.ypart.resize(need_x, stream);
     if (ws.work.size() < 1) ws.work.resize(1, stream);
 }
 // the runtime knobs that change the launch sequence of an hgemv
@@ -1987,14 +2000,14 @@ void hgemv_impl(const H2Dev& h, bool transpose, bool user_order, int64_t n, int6
                            static_cast<const SymBlock*>(plan->sym_blocks.data() + ld.item_begin), nitems, src,
                            ws.scratch.data(), b);
             } else {
-                if (overlap && ld.kind == 4) {   // dense slot sums wait for the dense pass
-                    H2B_CUDA(cudaEventRecord(sg.ev[2], sg.lo));
-                    H2B_CUDA(cudaStreamWaitEvent(stream, sg.ev[2], 0));
-                }
-                launch_pdl(csr_sum_kernel, grid, 256, stream, static_cast<const CsrUnit*>(plan->csr_units.data() + ld.item_begin),
+                // kind 2: coupling slot sums set y-hat; kind 4: dense slot sums set the blocked
+                // partial sums (ypart) on the dense pass's stream, added by the leaf expansion
+                const bool dense = ld.kind == 4;
+                launch_pdl(csr_sum_kernel, grid, 256, (overlap && dense) ? sg.lo : stream,
+                           static_cast<const CsrUnit*>(plan->csr_units.data() + ld.item_begin),
                            nitems, static_cast<const int64_t*>(plan->csr_slots.data()),
-                           static_cast<const double*>(ws.scratch.data()), b, ld.kind == 2 ? 0 : 1,
-                           ld.kind == 2 ? ws.yhat.data() : y, perm, ldy, alpha);
+                           static_cast<const double*>(ws.scratch.data()), b, 0,
+                           dense ? ws.ypart.data() : ws.yhat.data(), perm, ldy, alpha);
             }
             H2B_LAUNCH();
             if (timer) timer->mark(stream);
