@@ -558,6 +558,80 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const SvdJob* __restrict__
         }
 }
 
+// ---------------------------------------------------------------------------
+// TSQR combine: R of [R1; R2] for R1 upper triangular n x n and R2 upper
+// trapezoidal k2 x n (k2 <= n), both held packed in shared memory. Householder
+// column by column on the nonzeros only: reflector j acts on row j of R1 and rows
+// 0..min(j, k2-1) of R2 (the zero entries of the dense stacked QR contribute
+// nothing), so R2 stays upper trapezoidal until it is eliminated. One CTA per
+// pair; warp 0 forms each reflector, every warp updates trailing columns.
+// ---------------------------------------------------------------------------
+struct PairJob {
+    const double* R1;   // n x n upper triangular (ld1)
+    const double* R2;   // k2 x n upper trapezoidal (ld2)
+    double* out;        // n x n upper triangular result (ldo; zeros written below the diagonal)
+    int n, k2, ld1, ld2, ldo;
+};
+
+__device__ __forceinline__ int64_t pk1(int i, int j) { return int64_t(j) * (j + 1) / 2 + i; }   // i <= j
+__device__ __forceinline__ int64_t pk2(int i, int j, int k2) {                                  // i <= min(j, k2-1)
+    return (j < k2 ? int64_t(j) * (j + 1) / 2 : int64_t(k2) * (k2 + 1) / 2 + int64_t(j - k2) * k2) + i;
+}
+
+__global__ void __launch_bounds__(1024) qr_pair_kernel(const PairJob* __restrict__ jobs) {
+    extern __shared__ double sm[];
+    __shared__ double tau_s;
+    const PairJob jb = jobs[blockIdx.x];
+    const int n = jb.n, k2 = jb.k2;
+    double* A1 = sm;                            // packed R1
+    double* A2 = sm + int64_t(n) * (n + 1) / 2;   // packed R2
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+    for (int j = warp; j < n; j += nw) {
+        for (int i = lane; i <= j; i += 32) A1[pk1(i, j)] = jb.R1[i + int64_t(j) * jb.ld1];
+        for (int i = lane; i <= j && i < k2; i += 32) A2[pk2(i, j, k2)] = jb.R2[i + int64_t(j) * jb.ld2];
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        const int len = min(j + 1, k2);
+        double* v = A2 + pk2(0, j, k2);
+        if (warp == 0) {
+            double part = 0;
+            for (int i = lane; i < len; i += 32) part += v[i] * v[i];
+            const double tail = warp_sum(part);
+            const double c0 = A1[pk1(j, j)];
+            double t = 0, inv = 0, beta = c0;
+            if (tail > DBL_MIN) {
+                beta = sqrt(c0 * c0 + tail);
+                if (c0 >= 0) beta = -beta;
+                inv = 1.0 / (c0 - beta);
+                t = (beta - c0) / beta;
+            }
+            for (int i = lane; i < len; i += 32) v[i] = t == 0 ? 0.0 : v[i] * inv;
+            if (lane == 0) {
+                A1[pk1(j, j)] = beta;
+                tau_s = t;
+            }
+        }
+        __syncthreads();
+        const double t = tau_s;
+        if (t != 0) {
+            for (int c = j + 1 + warp; c < n; c += nw) {
+                double* a2 = A2 + pk2(0, c, k2);
+                double sacc = 0;
+                for (int i = lane; i < len; i += 32) sacc += v[i] * a2[i];
+                sacc = (warp_sum(sacc) + A1[pk1(j, c)]) * t;
+                if (lane == 0) A1[pk1(j, c)] -= sacc;
+                for (int i = lane; i < len; i += 32) a2[i] -= sacc * v[i];
+            }
+        }
+        __syncthreads();
+    }
+    for (int64_t e = tid; e < int64_t(n) * n; e += blockDim.x) {
+        const int i = int(e % n), j = int(e / n);
+        jb.out[i + int64_t(j) * jb.ldo] = i <= j ? A1[pk1(i, j)] : 0.0;
+    }
+}
+
 constexpr size_t kSmemCap = 226 * 1024;   // bytes of dynamic shared memory per CTA (227 KB max - static)
 constexpr int kWideCols = 40;              // QR / Jacobi problems with this many columns run on 1024 threads
 
@@ -764,7 +838,65 @@ void bqr(const std::vector<QrDesc>& d, cudaStream_t s) {
                              p.q.Q ? q2.data() + p.q2off : nullptr, p.srows});
     }
     qr_direct(lvl, s);
-    bqr(rec, s);
+    // R-only problems whose two packed triangles fit in shared memory: combine the chunk R's
+    // pairwise (a binary tree of structured QRs) instead of re-factoring the dense stack
+    std::vector<QrDesc> rest;
+    std::vector<size_t> pair_plans;
+    for (size_t i = 0; i < plans.size(); ++i) {
+        const Plan& p = plans[i];
+        const bool pairable = !p.q.Q && size_t(p.q.n) * (p.q.n + 1) * sizeof(double) <= kSmemCap &&
+                              p.rows.size() >= 2 && p.kp[0] == p.q.n;
+        if (pairable) pair_plans.push_back(i);
+        else rest.push_back(rec[i]);
+    }
+    bqr(rest, s);
+    if (!pair_plans.empty()) {
+        static const bool pair_attr = [] {
+            H2B_CUDA(cudaFuncSetAttribute(qr_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemCap)));
+            return true;
+        }();
+        (void)pair_attr;
+        struct Rref { const double* p; int k, ld; };
+        std::vector<std::vector<Rref>> cur(pair_plans.size());
+        size_t tmp_tot = 0;
+        for (size_t q = 0; q < pair_plans.size(); ++q) {
+            const Plan& p = plans[pair_plans[q]];
+            for (size_t c = 0; c < p.rows.size(); ++c)
+                cur[q].push_back(Rref{stack.data() + p.stoff + p.soff[c], p.kp[c], p.srows});
+            tmp_tot += size_t(p.q.n) * p.q.n * p.rows.size();   // every generation's outputs (< #chunks R's)
+        }
+        DBuf tmp(tmp_tot, s);   // combined R's are never overwritten: an odd one may wait a generation
+        size_t off = 0;
+        for (;;) {
+            std::vector<PairJob> jobs;
+            size_t smax = 0;
+            bool more = false;
+            for (size_t q = 0; q < pair_plans.size(); ++q) {
+                const Plan& p = plans[pair_plans[q]];
+                const int n = p.q.n;
+                std::vector<Rref>& v = cur[q];
+                if (v.size() < 2) continue;
+                std::vector<Rref> nxt;
+                const bool last = v.size() == 2;
+                for (size_t c = 0; c + 1 < v.size(); c += 2) {
+                    double* o = last ? p.q.R : tmp.data() + off;
+                    const int ldo = last ? p.q.ldr : n;
+                    if (!last) off += size_t(n) * n;
+                    jobs.push_back(PairJob{v[c].p, v[c + 1].p, o, n, v[c + 1].k, v[c].ld, v[c + 1].ld, ldo});
+                    nxt.push_back(Rref{o, n, ldo});
+                    smax = std::max(smax, size_t(n) * (n + 1));
+                }
+                if (v.size() % 2) nxt.push_back(v.back());   // the odd one (possibly trapezoidal) moves up
+                v = std::move(nxt);
+                more = more || v.size() > 1;
+            }
+            if (jobs.empty()) break;
+            DevVec<PairJob> dj(jobs, s);
+            qr_pair_kernel<<<unsigned(jobs.size()), 1024, smax * sizeof(double), s>>>(dj.p);
+            H2B_LAUNCH();
+            if (!more) break;
+        }
+    }
     // Q = blockdiag(Q_chunk) * Q_stack
     std::vector<GemmDesc> g;
     for (Plan& p : plans) {
