@@ -1164,3 +1164,24 @@ extern "C" int h2b_bench_jacobi(int n, int nprob, int trans, int reps, double* m
     cudaFree(u);
     return 0;
 }
+
+// test hook: R factor of one m x n host matrix through the batched QR driver (TSQR with the
+// pairwise combine when m exceeds a shared-memory chunk), downloaded to R_host (n x n, ld n)
+extern "C" int h2b_test_qr_r(const double* a_host, int m, int n, double* r_host) {
+    using namespace h2b;
+    try {
+        double *a = nullptr, *r = nullptr;
+        H2B_CUDA(cudaMalloc(&a, sizeof(double) * size_t(m) * n));
+        H2B_CUDA(cudaMalloc(&r, sizeof(double) * size_t(n) * n));
+        H2B_CUDA(cudaMemcpy(a, a_host, sizeof(double) * size_t(m) * n, cudaMemcpyHostToDevice));
+        H2B_CUDA(cudaMemset(r, 0, sizeof(double) * size_t(n) * n));
+        la::bqr({la::QrDesc{a, m, n, m, r, n, nullptr, 0}}, nullptr);
+        H2B_CUDA(cudaDeviceSynchronize());
+        H2B_CUDA(cudaMemcpy(r_host, r, sizeof(double) * size_t(n) * n, cudaMemcpyDeviceToHost));
+        cudaFree(a);
+        cudaFree(r);
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}

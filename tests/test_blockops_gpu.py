@@ -270,3 +270,23 @@ def test_validate_flags_false_orthonormal_claim(cuda):
     assert all("not orthonormal" in v for v in rep.violations)
     assert bogus.validate(ortho_cap=10).ok()   # above the cap the claim is not checked
     assert orthogonalize(m).validate().ok()
+
+
+@pytest.mark.parametrize("m,n", [(3000, 64), (3584, 128), (5000, 96), (900, 160), (2001, 40), (700, 170)])
+def test_batched_qr_r_factor(cuda, m, n):
+    """The batched QR's R factor (TSQR over shared-memory row chunks, then the pairwise
+    structured combine of the chunk triangles for R-only problems with n <= 167, or the dense
+    re-factorisation of the stacked R's above that) satisfies R^T R = A^T A and is upper
+    triangular with Householder's sign convention (R_jj of the sign opposite to the pivot)."""
+    import ctypes as C
+    from paper_2003_10173_b200._lib import lib
+    rng = np.random.default_rng(m * 7 + n)
+    a = np.asfortranarray(rng.standard_normal((m, n)) * np.logspace(0, -8, n))
+    r = np.zeros((n, n), order="F")
+    assert lib.h2b_test_qr_r(a.ctypes.data_as(C.c_void_p), m, n, r.ctypes.data_as(C.c_void_p)) == 0
+    assert np.all(np.tril(r, -1) == 0)
+    g = a.T @ a
+    assert np.linalg.norm(r.T @ r - g) <= 1e-13 * np.linalg.norm(g)
+    # same R as a dense Householder QR up to the row signs
+    rq = np.linalg.qr(a, mode="r")
+    assert np.allclose(np.abs(r), np.abs(rq), rtol=0, atol=1e-12 * np.abs(rq).max())
