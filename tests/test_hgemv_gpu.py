@@ -358,3 +358,30 @@ def test_top_chain_matches(cuda, sym, b, transpose):
     assert rel(outs[0], expect) <= TOL
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("b", [1, 32])
+def test_kernel_launch_accounting(cuda, b):
+    """h2b_kernel_launches counts every launch site, and a replayed CUDA graph adds its kernel
+    nodes (captured launches are not counted twice): after a first call (eager, and the plan
+    build's own U E product launch), 5 calls (1 captured and replayed, 4 replays) launch exactly
+    5 x m.launches(b) kernels."""
+    import ctypes as C
+    import torch
+    from paper_2003_10173_b200._lib import lib
+    lib.h2b_kernel_launches.restype = C.c_longlong
+    lib.h2b_kernel_launches.argtypes = [C.c_int]
+    pts = O.grid2d(64, 64)
+    ct = build_cluster_tree(pts, 32)
+    bt = build_block_tree(ct, ct, 1.0)
+    m = H2Matrix.kernel(bt, pts, "gaussian", 0.1, 12)
+    n = pts.shape[0]
+    xt = torch.randn(b, n, dtype=torch.float64, device=cuda).t()
+    yt = torch.zeros(b, n, dtype=torch.float64, device=cuda).t()
+    m.hgemv(xt, yt)
+    torch.cuda.synchronize()
+    lib.h2b_kernel_launches(1)
+    for _ in range(5):
+        m.hgemv(xt, yt)
+    torch.cuda.synchronize()
+    assert lib.h2b_kernel_launches(0) == 5 * m.launches(b)
