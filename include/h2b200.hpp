@@ -280,6 +280,13 @@ public:
         detail::check(owned ? h2c_dist_hgemv_end_owned(h_.get(), b, recvbuf, y_dev, ldy, alpha, beta, stream)
                             : h2c_dist_hgemv_end(h_.get(), b, recvbuf, y_dev, ldy, alpha, beta, stream));
     }
+    // the whole sharded hgemv with the exchange on the caller's ncclComm_t (passed as void*)
+    void hgemv_nccl(void* nccl_comm, Index b, const double* x_dev, Index ldx, double* y_dev, Index ldy,
+                    double alpha = 1.0, double beta = 0.0, void* stream = nullptr, bool owned = false) {
+        detail::check(owned ? h2c_dist_hgemv_nccl_owned(h_.get(), nccl_comm, b, x_dev, ldx, y_dev, ldy, alpha, beta,
+                                                        stream)
+                            : h2c_dist_hgemv_nccl(h_.get(), nccl_comm, b, x_dev, ldx, y_dev, ldy, alpha, beta, stream));
+    }
     // peer transport: alloc on every rank (same max_b), export, allgather the exports,
     // import all of them (or link the plans of every rank held by one process)
     struct PeerInfo {

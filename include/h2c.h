@@ -294,6 +294,16 @@ int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double
  * = rank q's). Plans of all ranks living in ONE process (tests) are linked with
  * h2c_dist_peer_link instead. Every rank must use the same max_b and call
  * begin/end the same number of times with the same b (the signals count calls). */
+/* the whole sharded hgemv with the exchange done inside the library on the
+ * caller's NCCL communicator (an ncclComm_t of nranks ranks whose rank order is
+ * the plans' ranks; every rank calls it with the same b). NCCL is resolved at
+ * run time from the process (the libnccl.so.2 already loaded, i.e. the instance
+ * that created the communicator), so libh2b200 does not link NCCL; the grouped
+ * send / receive runs on a side stream beside the local near field. */
+int h2c_dist_hgemv_nccl(h2c_dist_plan p, void* nccl_comm, int64_t b, const double* x, int64_t ldx, double* y,
+                        int64_t ldy, double alpha, double beta, void* stream);
+int h2c_dist_hgemv_nccl_owned(h2c_dist_plan p, void* nccl_comm, int64_t b, const double* x_owned, int64_t ldx,
+                              double* y_owned, int64_t ldy, double alpha, double beta, void* stream);
 int h2c_dist_peer_alloc(h2c_dist_plan p, int64_t max_b);
 int h2c_dist_peer_export(h2c_dist_plan p, void* handles, int64_t* recv_off);
 int h2c_dist_peer_import(h2c_dist_plan p, const void* handles, const int64_t* recv_offs);

@@ -142,6 +142,8 @@ _sig("h2c_dist_hgemv_local", i32, H, i64, vp)
 _sig("h2c_dist_hgemv_begin_owned", i32, H, i64, vp, i64, vp, vp)
 _sig("h2c_dist_hgemv_end_owned", i32, H, i64, vp, vp, i64, f64, f64, vp)
 _sig("h2c_dist_hgemv_end", i32, H, i64, vp, vp, i64, f64, f64, vp)
+_sig("h2c_dist_hgemv_nccl", i32, H, vp, i64, vp, i64, vp, i64, f64, f64, vp)
+_sig("h2c_dist_hgemv_nccl_owned", i32, H, vp, i64, vp, i64, vp, i64, f64, f64, vp)
 _sig("h2c_dist_peer_alloc", i32, H, i64)
 _sig("h2c_dist_peer_export", i32, H, vp, vp)
 _sig("h2c_dist_peer_import", i32, H, vp, vp)

@@ -615,6 +615,24 @@ int h2c_dist_hgemv_end(h2c_dist_plan p, int64_t b, const double* recvbuf, double
     });
 }
 
+int h2c_dist_hgemv_nccl(h2c_dist_plan p, void* nccl_comm, int64_t b, const double* x, int64_t ldx, double* y,
+                        int64_t ldy, double alpha, double beta, void* stream) {
+    return guard([&] {
+        need(p != nullptr && x != nullptr && y != nullptr, "null argument");
+        need(b >= 1, "matvec: need at least one column");
+        h2b::dist_hgemv_nccl(*p->p, nccl_comm, b, x, ldx, y, ldy, alpha, beta, static_cast<cudaStream_t>(stream));
+    });
+}
+int h2c_dist_hgemv_nccl_owned(h2c_dist_plan p, void* nccl_comm, int64_t b, const double* x_owned, int64_t ldx,
+                              double* y_owned, int64_t ldy, double alpha, double beta, void* stream) {
+    return guard([&] {
+        need(p != nullptr && x_owned != nullptr && y_owned != nullptr, "null argument");
+        need(b >= 1, "matvec: need at least one column");
+        h2b::dist_hgemv_nccl(*p->p, nccl_comm, b, x_owned, ldx, y_owned, ldy, alpha, beta,
+                             static_cast<cudaStream_t>(stream), true);
+    });
+}
+
 int h2c_dist_peer_alloc(h2c_dist_plan p, int64_t max_b) {
     return guard([&] {
         need(p != nullptr, "null plan");

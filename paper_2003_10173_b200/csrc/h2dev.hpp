@@ -191,5 +191,8 @@ void dist_peer_import(DistPlan& p, const std::vector<PeerHandles>& all, const st
 // plans of every rank in one process (their buffers reachable directly)
 void dist_peer_link(const std::vector<DistPlan*>& plans);
 bool dist_peer_ready(const DistPlan& p);
+// the whole sharded hgemv with the exchange on the caller's ncclComm_t (NCCL resolved from the process)
+void dist_hgemv_nccl(DistPlan& p, void* comm, int64_t b, const double* x, int64_t ldx, double* y, int64_t ldy,
+                     double alpha, double beta, cudaStream_t s, bool owned = false);
 
 }  // namespace h2b

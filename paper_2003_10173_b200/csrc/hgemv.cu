@@ -4,6 +4,8 @@
 // gather (cluster_tree.hpp:82-86) is one blocked-layout pass over x and the
 // scatter back to user order (cluster_tree.hpp:88-92) is fused into the
 // leaf/dense epilogue together with alpha/beta.
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <atomic>
 #include <map>
@@ -2175,7 +2177,14 @@ struct DistPlan {
     DeviceArray<int64_t> d_remote_off, d_send_off;    // per q: my segment in q's buffer / in my send order
     DeviceArray<unsigned long long*> d_peer_flags, d_peer_acks;   // per q: q's flag / ack arrays
     std::vector<void*> opened;                        // IPC mappings to close
+    // NCCL exchange inside the library (dist_hgemv_nccl)
+    DeviceArray<double> nccl_send, nccl_recv;
+    cudaStream_t xs = nullptr;
+    cudaEvent_t xev[2] = {nullptr, nullptr};
     ~DistPlan() {
+        if (xs) cudaStreamDestroy(xs);
+        for (cudaEvent_t e : xev)
+            if (e) cudaEventDestroy(e);
         for (void* v : opened) cudaIpcCloseMemHandle(v);
         if (peer_recvbuf) cudaFree(peer_recvbuf);
         if (peer_sync) cudaFree(peer_sync);
@@ -2486,6 +2495,91 @@ void dist_peer_link(const std::vector<DistPlan*>& plans) {
 }
 
 bool dist_peer_ready(const DistPlan& p) { return p.peers_ready; }
+
+// ---------------------------------------------------------------------------
+// one sharded hgemv with the exchange on the caller's NCCL communicator. NCCL is
+// resolved at run time from the process (the library instance that created the
+// communicator: dlopen RTLD_NOLOAD of libnccl.so.2 first), so libh2b200 does not
+// link it. The grouped send / receive runs on a side stream while the local
+// near field runs on the caller's stream.
+// ---------------------------------------------------------------------------
+namespace {
+struct NcclApi {
+    using Group = int (*)();
+    using SendRecv = int (*)(const void*, size_t, int, int, void*, cudaStream_t);
+    using Recv = int (*)(void*, size_t, int, int, void*, cudaStream_t);
+    using ErrStr = const char* (*)(int);
+    Group start = nullptr, end = nullptr;
+    SendRecv send = nullptr;
+    Recv recv = nullptr;
+    ErrStr err = nullptr;
+    bool ok = false;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.start = reinterpret_cast<NcclApi::Group>(dlsym(h, "ncclGroupStart"));
+        a.end = reinterpret_cast<NcclApi::Group>(dlsym(h, "ncclGroupEnd"));
+        a.send = reinterpret_cast<NcclApi::SendRecv>(dlsym(h, "ncclSend"));
+        a.recv = reinterpret_cast<NcclApi::Recv>(dlsym(h, "ncclRecv"));
+        a.err = reinterpret_cast<NcclApi::ErrStr>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.start && a.end && a.send && a.recv;
+        return a;
+    }();
+    return api;
+}
+void nccl_check(int r, const char* what) {
+    if (r != 0) {
+        const NcclApi& a = nccl_api();
+        throw cuda_error(std::string("NCCL error in ") + what + ": " + (a.err ? a.err(r) : std::to_string(r)));
+    }
+}
+}  // namespace
+
+void dist_hgemv_nccl(DistPlan& p, void* comm, int64_t b, const double* x, int64_t ldx, double* y, int64_t ldy,
+                     double alpha, double beta, cudaStream_t s, bool owned) {
+    const int P = p.spec.nranks;
+    int64_t ns = 0, nr = 0;
+    for (int q = 0; q < P; ++q) {
+        ns += p.send_rows[size_t(q)];
+        nr += p.recv_rows[size_t(q)];
+    }
+    if (p.nccl_send.size() < size_t(std::max<int64_t>(ns * b, 1))) p.nccl_send.resize(size_t(std::max<int64_t>(ns * b, 1)), s);
+    if (p.nccl_recv.size() < size_t(std::max<int64_t>(nr * b, 1))) p.nccl_recv.resize(size_t(std::max<int64_t>(nr * b, 1)), s);
+    dist_hgemv_begin(p, b, x, ldx, p.nccl_send.data(), s, owned);
+    if (P > 1) {
+        const NcclApi& api = nccl_api();
+        if (!api.ok) throw std::logic_error("dist hgemv nccl: libnccl.so.2 not found in the process");
+        if (!p.xs) {
+            int least = 0, greatest = 0;
+            H2B_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            H2B_CUDA(cudaStreamCreateWithPriority(&p.xs, cudaStreamNonBlocking, greatest));
+            H2B_CUDA(cudaEventCreateWithFlags(&p.xev[0], cudaEventDisableTiming));
+            H2B_CUDA(cudaEventCreateWithFlags(&p.xev[1], cudaEventDisableTiming));
+        }
+        H2B_CUDA(cudaEventRecord(p.xev[0], s));   // the send buffer is packed
+        H2B_CUDA(cudaStreamWaitEvent(p.xs, p.xev[0], 0));
+        constexpr int kFloat64 = 8;   // ncclFloat64
+        nccl_check(api.start(), "ncclGroupStart");
+        for (int q = 0; q < P; ++q) {
+            const int64_t so = p.send_off[size_t(q)], ro = p.recv_off[size_t(q)];
+            if (p.send_rows[size_t(q)] > 0)
+                nccl_check(api.send(p.nccl_send.data() + so * b, size_t(p.send_rows[size_t(q)] * b), kFloat64, q, comm, p.xs),
+                           "ncclSend");
+            if (p.recv_rows[size_t(q)] > 0)
+                nccl_check(api.recv(p.nccl_recv.data() + ro * b, size_t(p.recv_rows[size_t(q)] * b), kFloat64, q, comm, p.xs),
+                           "ncclRecv");
+        }
+        nccl_check(api.end(), "ncclGroupEnd");
+        H2B_CUDA(cudaEventRecord(p.xev[1], p.xs));
+        dist_hgemv_local(p, b, s);                 // beside the exchange
+        H2B_CUDA(cudaStreamWaitEvent(s, p.xev[1], 0));
+    }
+    dist_hgemv_end(p, b, p.nccl_recv.data(), y, ldy, alpha, beta, s, owned);
+}
 
 int hgemv_launch_count(const H2Dev& h, bool transpose, int64_t b) {
     auto plan = select_plan(h, transpose, b);   // the plan hgemv actually runs at this b

@@ -68,6 +68,14 @@ class DistPlan:
         check(lib.h2c_dist_plan_launches(self._h, C.byref(v)))
         return v.value
 
+    def hgemv_nccl(self, comm, x, y, b, alpha=1.0, beta=0.0, stream=None, owned=False):
+        """The whole sharded hgemv with the exchange on an ncclComm_t handle (an int / c_void_p
+        from the process's NCCL), done inside the library (h2c_dist_hgemv_nccl)."""
+        _, ldx = col_major_geom(x)
+        _, ldy = col_major_geom(y)
+        fn = lib.h2c_dist_hgemv_nccl_owned if owned else lib.h2c_dist_hgemv_nccl
+        check(fn(self._h, comm, int(b), x.data_ptr(), ldx, y.data_ptr(), ldy, float(alpha), float(beta), stream))
+
     # ---- peer transport (h2c_dist_peer_*): P2P writes + signals, no collective call
     def peer_alloc(self, max_b):
         check(lib.h2c_dist_peer_alloc(self._h, int(max_b)))

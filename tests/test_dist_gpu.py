@@ -273,3 +273,34 @@ def test_peer_transport_needs_setup(cuda):
     x = torch.randn(2, pts.shape[0], dtype=torch.float64, device=cuda).t()
     with pytest.raises(NotImplementedError):   # std::logic_error: no buffer and no peer transport
         p.begin(x, None, 2)
+
+
+def test_nccl_entry_single_rank(cuda):
+    """h2c_dist_hgemv_nccl on a one-rank NCCL communicator (ncclCommInitAll from the NCCL the
+    process already loaded): the library resolves NCCL at run time, packs, exchanges nothing and
+    matches the single-GPU hgemv. (More ranks need more GPUs than this environment has.)"""
+    import ctypes as C
+    import torch
+    torch.zeros(1, device=cuda)
+    import torch.cuda.nccl  # noqa: F401  loads torch's libnccl.so.2
+    try:
+        nccl = C.CDLL("libnccl.so.2", mode=C.RTLD_GLOBAL)
+    except OSError:
+        pytest.skip("no libnccl.so.2 in the process")
+    comm = C.c_void_p()
+    devs = (C.c_int * 1)(torch.cuda.current_device())
+    assert nccl.ncclCommInitAll(C.byref(comm), 1, devs) == 0
+    pts = O.grid2d(64, 64)
+    ct = build_cluster_tree(pts, 32)
+    bt = build_block_tree(ct, ct, 1.0)
+    m = H2Matrix.kernel(bt, pts, "gaussian", 0.1, 12)
+    n, b = pts.shape[0], 7
+    x = torch.randn(b, n, dtype=torch.float64, device=cuda).t()
+    y_ref = torch.zeros(b, n, dtype=torch.float64, device=cuda).t()
+    m.hgemv(x, y_ref)
+    p = DistPlan(m, 1, 0)
+    y = torch.zeros(b, n, dtype=torch.float64, device=cuda).t()
+    p.hgemv_nccl(comm, x, y, b)
+    torch.cuda.synchronize()
+    nccl.ncclCommDestroy(comm)
+    assert close(y, y_ref, 1)
