@@ -385,3 +385,24 @@ def test_kernel_launch_accounting(cuda, b):
         m.hgemv(xt, yt)
     torch.cuda.synchronize()
     assert lib.h2b_kernel_launches(0) == 5 * m.launches(b)
+
+
+@pytest.mark.parametrize("b", [1, 2])
+@pytest.mark.parametrize("alpha,beta", [(-1.0, 1.0), (2.5, -0.5)])
+def test_few_vector_alpha_beta_through_graph(cuda, b, alpha, beta):
+    """The few-vector symmetric path (dense slot sums into blocked partial sums, added by the leaf
+    expansion's epilogue before alpha / beta and the user-order scatter) with general alpha, beta,
+    eagerly and through the captured-graph replays (4 identical calls)."""
+    import torch
+    pts = O.grid2d(48, 48)
+    ora, m, _ = pair(pts, 24, False, True, 10, seed=31)
+    n = pts.shape[0]
+    x = O.gaussian(51 + b, n, b)
+    y0 = O.gaussian(61 + b, n, b)
+    expect = alpha * ora.matvec(x) + beta * y0
+    xt = torch.from_numpy(x.T.copy()).to(cuda).t()
+    for _ in range(4):
+        yt = torch.from_numpy(y0.T.copy()).to(cuda).t()
+        m.hgemv(xt, yt, alpha=alpha, beta=beta)
+        torch.cuda.synchronize()
+        assert rel(yt.cpu().numpy(), expect) <= TOL
